@@ -1,0 +1,320 @@
+"""Decode engine parity on the GPU against the oracle and the reference's
+golden traces (mirrors reference tests/test_runtime.py and the hot-path
+acceptance criteria C5/C8)."""
+
+import numpy as np
+import pytest
+
+from oracle import dpq_oracle as O
+from paper_2508_06041_b200 import model as M
+from paper_2508_06041_b200 import quant as Q
+from paper_2508_06041_b200 import runtime as R
+
+from conftest import plan_path
+from helpers import EPS_DECISION, canon, decision_mismatches, oracle_engine, oracle_eval, trace_arrays
+
+pytestmark = pytest.mark.gpu
+LOGIT_TOL = 2e-5          # max |dlogit| / max |logit|
+LOSS_TOL = 1e-5           # per-token loss, absolute (nats)
+
+
+def forced_from_oracle(eng_o, ids):
+    return [np.array([r.bits[O.key(l)] for l in ids], dtype=np.int8) for r in eng_o.records]
+
+
+def device_eval_forced(weights, store, plan, tokens, forced, **kw):
+    """eval_perplexity with the decisions replayed from `forced` (list per step)."""
+    eng = R.DecodeEngine(weights, store, plan, **kw)
+    logits = eng.step(int(tokens[0]), dynamic=False)
+    losses, all_logits = [], [logits]
+    for i in range(1, len(tokens)):
+        z = logits - logits.max()
+        losses.append(float(np.log(np.exp(z).sum()) - z[tokens[i]]))
+        if i < len(tokens) - 1:
+            logits = eng.step(int(tokens[i]), dynamic=True, forced_bits=forced[i - 1])
+            all_logits.append(logits)
+    return losses, eng, np.array(all_logits)
+
+
+def Ts(plan, ids):
+    return np.array([plan.layers[l].T for l in ids], dtype=np.float64)
+
+
+@pytest.mark.parametrize("name", ["dp_t3.5", "dp_t4", "llm_mq_t3.5", "hawq_v2_t4"])
+def test_report_numbers_on_device(report_setup, golden_summary, name):
+    """report.csv rows: perplexity / effective bits / estimator ops, with the
+    device following the oracle's decisions (forced replay) and the device's
+    own decisions checked against the oracle under the eps rule."""
+    S = report_setup
+    plan = R.load_plan(plan_path(name), S.store)
+    ids = canon(S.store.layers)
+    T = Ts(plan, ids)
+    losses, effs, ops = [], [], 0
+    for toks in S.chunks:
+        _, ls_o, eng_o = oracle_eval(S.weights, S.store, plan, toks)
+        forced = forced_from_oracle(eng_o, ids)
+        ls, eng, _ = device_eval_forced(S.weights, S.store, plan, toks, forced, store_hash=S.store_hash,
+                                        g_dtype="f32")
+        np.testing.assert_allclose(ls, ls_o, atol=LOSS_TOL)
+        losses.extend(ls)
+        effs.append(eng.trace.mean_effective_bits())
+        ops += eng.trace.estimator_ops
+        # device estimates vs oracle, and the decisions they imply
+        bits_o, est_o = trace_arrays(eng_o.records, ids)
+        _, est_d = trace_arrays(eng.trace.steps, ids)
+        np.testing.assert_allclose(est_d, est_o, rtol=1e-4, equal_nan=True)
+        implied = np.where(np.isnan(est_d), bits_o, np.where(est_d > T, [plan.layers[l].pair[1] for l in ids],
+                                                               [plan.layers[l].pair[0] for l in ids]))
+        assert not decision_mismatches(implied, bits_o, est_o, T, EPS_DECISION["f32"])
+    exp = golden_summary["plans"][name]
+    assert float(np.exp(np.mean(losses))) == pytest.approx(exp["perplexity"], rel=1e-6)
+    assert float(np.mean(effs)) == pytest.approx(exp["effective_bits"], abs=1e-12)
+    assert ops == exp["estimator_ops"]
+
+
+def test_free_running_dynamic_plan(report_setup, golden_traces):
+    """Unforced device run of dp_t3.5: decisions equal the reference's until
+    the first tie (|est - T| <= eps |T|), f16 G."""
+    S = report_setup
+    plan = R.load_plan(plan_path("dp_t3.5"), S.store)
+    ppl, tr = R.eval_perplexity(S.weights, S.store, S.chunks[0], "dynamic", plan=plan,
+                                store_hash=S.store_hash)
+    ids = [M.LayerId.from_name(n) for n in golden_traces["dp_t3.5_layers"]]
+    bits_d, _ = trace_arrays(tr.steps, ids)
+    bits_r, est_r = golden_traces["dp_t3.5_bits"], golden_traces["dp_t3.5_est"]
+    T = Ts(plan, ids)
+    for s in range(len(bits_r)):
+        bad = decision_mismatches(bits_d[s:s + 1], bits_r[s:s + 1], est_r[s:s + 1], T, EPS_DECISION["f16"])
+        assert not bad, bad
+        if not np.array_equal(bits_d[s], bits_r[s]):
+            break           # a tie: trajectories may diverge from here on
+    assert np.isfinite(ppl)
+
+
+def test_decode_matches_golden(report_setup, golden_traces):
+    S = report_setup
+    plan = R.load_plan(plan_path("dp_t3.5"), S.store)
+    ids = [M.LayerId.from_name(n) for n in golden_traces["decode_layers"]]
+    prompt = golden_traces["decode_prompt"]
+    gold_toks = golden_traces["decode_tokens"]
+    # step API with the reference decisions replayed: logits per step
+    eng = R.DecodeEngine(S.weights, S.store, plan, S.store_hash, g_dtype="f32")
+    logits = eng.prefill(prompt)
+    lg = [logits]
+    for s, tok in enumerate(gold_toks):
+        logits = eng.step(int(tok), dynamic=True, forced_bits=golden_traces["decode_bits"][s])
+        lg.append(logits)
+    lg = np.array(lg)
+    ref = golden_traces["decode_logits"]
+    assert np.max(np.abs(lg - ref)) <= LOGIT_TOL * np.max(np.abs(ref))
+    assert [int(np.argmax(v)) for v in lg[:-1]] == gold_toks.tolist()
+    # device greedy loop (argmax fed back on the GPU)
+    out, tr = R.decode(S.weights, S.store, plan, prompt, len(gold_toks), store_hash=S.store_hash,
+                       g_dtype="f32")
+    bits_d, _ = trace_arrays(tr.steps, ids)
+    if np.array_equal(bits_d, golden_traces["decode_bits"]):
+        assert out == gold_toks.tolist()
+    assert len(out) == len(gold_toks) == len(tr.steps)
+
+
+@pytest.mark.parametrize("rule", ["prev_step", "prev_block"])
+def test_exact_async_plan_on_device(report_setup, golden_traces, golden_summary, rule):
+    S = report_setup
+    plan = R.load_plan(plan_path("exact_async_t4"), S.store)
+    ids = [M.LayerId.from_name(n) for n in golden_traces[f"exact_{rule}_layers"]]
+    forced = list(golden_traces[f"exact_{rule}_bits"].astype(np.int8))
+    ls, eng, _ = device_eval_forced(S.weights, S.store, plan, S.chunks[0], forced, track_exact=True,
+                                    async_rule=rule, g_dtype="f32")
+    np.testing.assert_allclose(ls, golden_traces[f"exact_{rule}_losses"], atol=LOSS_TOL)
+    _, est_d = trace_arrays(eng.trace.steps, ids)
+    np.testing.assert_allclose(est_d, golden_traces[f"exact_{rule}_est"], rtol=1e-4, atol=1e-9,
+                               equal_nan=True)
+    xids = [M.LayerId.from_name(n) for n in golden_traces[f"exact_{rule}_xlayers"]]
+    xerr = np.array([[r.exact_errors[l] for l in xids] for r in eng.trace.steps])
+    np.testing.assert_allclose(xerr, golden_traces[f"exact_{rule}_xerr"], rtol=1e-4, atol=1e-9)
+    assert eng.trace.estimator_ops == golden_summary[f"exact_{rule}_estimator_ops"]
+    cmp = R.incurred_error_comparison(eng.trace, plan)
+    assert cmp
+    for dyn, matched, m, n in cmp.values():
+        assert 0 <= m <= n
+
+
+def test_linear_plan_on_device(report_setup, golden_traces, golden_summary):
+    S = report_setup
+    plan = R.load_plan(plan_path("linear_t3.5"), S.store)
+    ids = [M.LayerId.from_name(n) for n in golden_traces["linear_layers"]]
+    toks = S.chunks[golden_summary["linear_chunk"]]
+    forced = list(golden_traces["linear_bits"].astype(np.int8))
+    ls, eng, _ = device_eval_forced(S.weights, S.store, plan, toks, forced, g_dtype="f32")
+    np.testing.assert_allclose(ls, golden_traces["linear_losses"], atol=LOSS_TOL)
+    _, est_d = trace_arrays(eng.trace.steps, ids)
+    np.testing.assert_allclose(est_d, golden_traces["linear_est"], rtol=1e-5, equal_nan=True)
+    # unforced: decisions identical outside eps
+    _, tr = R.eval_perplexity(S.weights, S.store, toks, "dynamic", plan=plan)
+    bits_d, _ = trace_arrays(tr.steps, ids)
+    s_end = len(bits_d)
+    for s in range(len(bits_d)):
+        if not np.array_equal(bits_d[s], golden_traces["linear_bits"][s]):
+            s_end = s + 1
+            break
+    assert not decision_mismatches(bits_d[:s_end], golden_traces["linear_bits"][:s_end],
+                                   golden_traces["linear_est"][:s_end], Ts(plan, ids), EPS_DECISION["f32"])
+
+
+def test_fp_mode(report_setup, golden_summary):
+    losses = []
+    for toks in report_setup.chunks:
+        _, tr = R.eval_perplexity(report_setup.weights, report_setup.store, toks, "fp")
+        losses.extend(tr.token_losses)
+    assert float(np.exp(np.mean(losses))) == pytest.approx(golden_summary["fp_perplexity"], rel=1e-10)
+
+
+def _mixed_bits(store):
+    return {lid: (4 if lid.kind in ("q", "k", "v") else 5) for lid in store.layers}
+
+
+def test_stepwise_matches_batch_forward(toy_weights, toy_store):
+    bits = _mixed_bits(toy_store)
+    toks = np.random.default_rng(0).integers(0, 256, 30)
+    layers = {O.key(l): O.as_layer(q) for l, q in toy_store.layers.items()}
+    mats = {k: O.dequantize(layers[k], bits[M.LayerId(*k)]) for k in layers}
+    logits = O.forward(toy_weights.config, toy_weights.embed, toy_weights.lm_head, lambda k: mats[k], toks)
+    ref = O.token_losses(logits, toks)
+    from paper_2508_06041_b200.runtime import sentinel_static_plan
+    asg = type("A", (), {"bits": bits})()
+    ppl, tr = R.eval_perplexity(toy_weights, toy_store, toks, "static", assignment=asg)
+    np.testing.assert_allclose(tr.token_losses, ref, atol=LOSS_TOL)
+    assert ppl == pytest.approx(float(np.exp(ref.mean())), rel=1e-5)
+
+
+def test_sentinel_dynamic_equals_static_exactly(toy_weights, toy_store):
+    bits = _mixed_bits(toy_store)
+    toks = np.arange(25)
+    asg = type("A", (), {"bits": bits})()
+    ppl_s, tr_s = R.eval_perplexity(toy_weights, toy_store, toks, "static", assignment=asg)
+    plan = R.sentinel_static_plan(bits, toy_store.param_counts(), 4.5)
+    ppl_d, tr_d = R.eval_perplexity(toy_weights, toy_store, toks, "dynamic", plan=plan)
+    assert ppl_d == ppl_s
+    assert tr_d.token_losses == tr_s.token_losses
+    assert [s.bits for s in tr_d.steps] == [s.bits for s in tr_s.steps]
+
+
+def test_forced_static_equivalence_c8(toy_weights, toy_store):
+    """Acceptance C8 (tests/test_acceptance.py:234-272): +inf on (a, a+1) and
+    -inf on (a-1, a) reproduce the static assignment exactly, device vs device."""
+    rng = np.random.default_rng(8)
+    bits = {lid: int(rng.integers(3, 7)) for lid in toy_store.layers}
+    counts = toy_store.param_counts()
+    toks = rng.integers(0, 256, 20)
+    asg = type("A", (), {"bits": bits})()
+    ppl_s, tr_s = R.eval_perplexity(toy_weights, toy_store, toks, "static", assignment=asg)
+    lo = {lid: R.PlanLayer(lid, a, float(a), (a, min(a + 1, 6)), np.inf, 1.0, None) for lid, a in bits.items()}
+    hi = {lid: R.PlanLayer(lid, a, float(a), (max(a - 1, 3), a), -np.inf, 0.0, None) for lid, a in bits.items()}
+    for layers in (lo, hi):
+        plan = R.PrecisionPlan("x", 4.0, float("nan"), layers, counts)
+        ppl_f, tr_f = R.eval_perplexity(toy_weights, toy_store, toks, "dynamic", plan=plan)
+        assert ppl_f == ppl_s and tr_f.token_losses == tr_s.token_losses
+        assert all(s.bits[lid] == bits[lid] for s in tr_f.steps for lid in s.bits)
+    out_s, _ = R.decode(toy_weights, toy_store, R.sentinel_static_plan(bits, counts, 4.0), toks[:6], 8)
+    out_f, _ = R.decode(toy_weights, toy_store, R.PrecisionPlan("x", 4.0, float("nan"), lo, counts),
+                        toks[:6], 8)
+    assert out_s == out_f
+
+
+def test_effective_bits_and_trace_csv(tmp_path, toy_weights, toy_store):
+    plan = R.sentinel_static_plan({l: 4 for l in toy_store.layers}, toy_store.param_counts(), 4.0)
+    _, tr = R.eval_perplexity(toy_weights, toy_store, np.arange(10), "dynamic", plan=plan)
+    assert np.isclose(tr.mean_effective_bits(), 4.0)
+    p = str(tmp_path / "t.csv")
+    tr.export_csv(p)
+    lines = open(p).read().splitlines()
+    assert lines[0] == "step,layer,bit,estimate"
+    assert len(lines) == 1 + len(tr.steps) * len(plan.layers)
+
+
+def test_greedy_deterministic_and_cap(toy_weights, toy_store):
+    plan = R.sentinel_static_plan({l: 4 for l in toy_store.layers}, toy_store.param_counts(), 4.0)
+    a, tr = R.decode(toy_weights, toy_store, plan, np.arange(5), 12)
+    b, _ = R.decode(toy_weights, toy_store, plan, np.arange(5), 12)
+    assert a == b and len(a) == 12 and len(tr.steps) == 12
+    eng = R.DecodeEngine(toy_weights, toy_store, plan)
+    for t in range(toy_weights.config.seq_cap):
+        eng.step(t % 256, dynamic=False, want_logits=False)
+    with pytest.raises(ValueError):
+        eng.step(0)
+
+
+def synthetic_projection_plan(store, pairs, k=16, seed=0, T_scale=None):
+    """Projection plan with G = A dW (oracle float64) and T picked per layer."""
+    layers, Ms = {}, store.param_counts()
+    rng = np.random.default_rng(seed)
+    for i, lid in enumerate(canon(store.layers)):
+        q = O.as_layer(store.layers[lid])
+        l, h = pairs[lid]
+        A = rng.standard_normal((k, q.shape[0])) / np.sqrt(k)
+        G = A @ O.delta_weights(q, l, h)
+        est = R.E.ErrorEstimator(R.E.ProjectionEstimator(G, k, seed), R.E.IMMEDIATE, (l, h))
+        layers[lid] = R.PlanLayer(lid, h, l + 0.5, (l, h), 1.0, 0.5, est)
+    return R.PrecisionPlan("dp", 3.5, 4.0, layers, Ms)
+
+
+def calibrate_T(weights, store, plan, tokens, q=0.5):
+    """T := per-layer quantile of the oracle's estimates over a calibration run."""
+    for pl in plan.layers.values():
+        pl.T = 1e300
+    _, _, eng = oracle_eval(weights, store, plan, tokens)
+    for lid, pl in plan.layers.items():
+        vals = np.sort([r.estimates[O.key(lid)] for r in eng.records])
+        pl.T = float(vals[int(q * (len(vals) - 1))])
+    return plan
+
+
+@pytest.mark.parametrize("gqa", [False, True])
+def test_cfg1_model_forced_and_free(gqa):
+    """cfg1 shapes (2 blocks, d=512, d_ff=1792, 4/3-bit store) and a GQA
+    variant: logits vs the oracle under forced replay; free-run decisions."""
+    cfg = M.ModelConfig(n_blocks=2, d_model=512, n_heads=8, d_ff=1792, vocab=256, seq_cap=64,
+                        n_kv_heads=2 if gqa else None)
+    w = M.init_model(0, cfg)
+    store = Q.quantize_model(w, 4, 3)
+    plan = synthetic_projection_plan(store, {l: (3, 4) for l in store.layers}, k=64)
+    toks = np.random.default_rng(3).integers(0, 256, 24)
+    calibrate_T(w, store, plan, toks[:12])
+    ids = canon(store.layers)
+    _, ls_o, eng_o = oracle_eval(w, store, plan, toks)
+    forced = forced_from_oracle(eng_o, ids)
+    ls, eng, lg = device_eval_forced(w, store, plan, toks, forced, g_dtype="f32")
+    np.testing.assert_allclose(ls, ls_o, atol=LOSS_TOL)
+    bits_o, est_o = trace_arrays(eng_o.records, ids)
+    _, est_d = trace_arrays(eng.trace.steps, ids)
+    np.testing.assert_allclose(est_d, est_o, rtol=1e-4)
+    # free run with f16 G: decisions until the first eps-tie
+    _, tr = R.eval_perplexity(w, store, toks, "dynamic", plan=plan)
+    bits_d, _ = trace_arrays(tr.steps, ids)
+    for s in range(len(bits_o)):
+        assert not decision_mismatches(bits_d[s:s + 1], bits_o[s:s + 1], est_o[s:s + 1], Ts(plan, ids),
+                                       EPS_DECISION["f16"])
+        if not np.array_equal(bits_d[s], bits_o[s]):
+            break
+
+
+def test_async_prev_step_and_prev_block_projection(toy_weights, toy_store):
+    """Previous-residual projection estimators through the snapshot path."""
+    plan = synthetic_projection_plan(toy_store, {l: (3, 4) for l in toy_store.layers}, k=8, seed=2)
+    for lid, pl in plan.layers.items():
+        if lid.residual_fed and lid.block > 0:
+            pl.estimator.input_source = R.E.PREVIOUS_RESIDUAL
+    toks = np.random.default_rng(5).integers(0, 256, 20)
+    calibrate_T(toy_weights, toy_store, plan, toks[:10])
+    ids = canon(toy_store.layers)
+    for rule in ("prev_step", "prev_block"):
+        for prime in (True, False):
+            _, ls_o, eng_o = oracle_eval(toy_weights, toy_store, plan, toks, async_rule=rule,
+                                         prime_from_prefill=prime)
+            forced = forced_from_oracle(eng_o, ids)
+            ls, eng, _ = device_eval_forced(toy_weights, toy_store, plan, toks, forced, async_rule=rule,
+                                            prime_from_prefill=prime, g_dtype="f32")
+            np.testing.assert_allclose(ls, ls_o, atol=LOSS_TOL)
+            _, est_o = trace_arrays(eng_o.records, ids)
+            _, est_d = trace_arrays(eng.trace.steps, ids)
+            np.testing.assert_allclose(est_d, est_o, rtol=1e-4)
