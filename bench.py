@@ -1,0 +1,398 @@
+"""Decode benchmark for the B200 DP-LLM hot path.
+
+Workload (BASELINE.json configs[3], single-GPU leg): Llama-3-8B-shaped
+random-init model (32 blocks, d=4096, 32 heads / 8 KV heads, d_ff=14336,
+vocab 256 as in the reference), 4-bit nested store (b_min 3), DP plan with
+(3,4) pairs on every linear layer, k=64 projection estimators (fp16 G on the
+device), thresholds calibrated so ~50% of decisions are high (3.5-bit
+effective target), batch-1 greedy decode.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0). ``value`` = decode tokens/s summed over ranks
+(device-resident loop: one CUDA graph per token, argmax fed back on the GPU,
+CUDA events on the decode stream, max over ranks). The weights (3.5 GB of
+bitplanes) exceed L2 (126 MB), so no flush is needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode tokens/s & per-layer GEMV HBM GB/s (% of 8 TB/s) at target bitwidth"
+UNIT = "tokens/s"
+PROMPT = 16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=256)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llama3_8b", choices=["llama3_8b", "llama2_7b", "cfg1", "llama2_70b_slice"])
+    ap.add_argument("--target", type=float, default=3.5)
+    ap.add_argument("--g-dtype", default="f16", choices=["f32", "f16", "e4m3"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-static", action="store_true")
+    return ap.parse_args()
+
+
+def model_config(name):
+    from paper_2508_06041_b200 import model as M
+    if name == "llama3_8b":
+        return M.ModelConfig(32, 4096, 32, 14336, vocab=256, seq_cap=1024, n_kv_heads=8), 4, 3
+    if name == "llama2_7b":
+        return M.ModelConfig(32, 4096, 32, 11008, vocab=256, seq_cap=1024), 6, 3
+    if name == "llama2_70b_slice":
+        return M.ModelConfig(8, 8192, 64, 28672, vocab=256, seq_cap=1024, n_kv_heads=8), 6, 3
+    return M.ModelConfig(2, 512, 8, 1792, vocab=256, seq_cap=1024), 4, 3
+
+
+def pairs_for_target(store, target):
+    """(floor, ceil) pair per layer; prefill at the high bit; ~ (target - l)
+    of the decisions high (SURVEY 8d synthetic plans)."""
+    lo = int(np.floor(target))
+    hi = lo + 1 if target > lo else lo
+    ids = store.ordered_ids()
+    pairs = {l: (lo, hi) for l in ids}
+    prefill = {l: hi for l in ids}
+    return pairs, prefill, (target - lo) if hi > lo else 0.0
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4)
+                          if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def op_bytes(store, plan, bits_row, ids, g_bytes_per_el):
+    """Algorithmic bytes of the 4 fused ops of each block at the selected bits
+    (SURVEY 8d): rows*cols*b/8 + 8 rows (lo, span) + 4 cols (x) + 4 rows (y)
+    + selector 2*k*cols (fp16 G) for dynamic projection layers."""
+    per_layer = []
+    for i, lid in enumerate(ids):
+        rows, cols = store.layers[lid].shape
+        b = int(bits_row[i])
+        by = rows * cols * b / 8 + 8 * rows + 4 * rows
+        pl = plan.layers[lid]
+        if pl.estimator is not None and np.isfinite(pl.T):
+            by += g_bytes_per_el * pl.estimator.kind.k * cols
+        per_layer.append((lid, by, cols))
+    ops = []
+    nb = len(ids) // 7
+    for b in range(nb):
+        grp = [[0, 1, 2], [3], [4, 5], [6]]
+        for g in grp:
+            tot = sum(per_layer[7 * b + k][1] for k in g) + 4 * per_layer[7 * b + g[0]][2]
+            ops.append(tot)
+    return np.array(ops)
+
+
+def cpu_slice_oracle(cfg, host_layers, plan, weights, n_tokens=6, seed=0):
+    """Reference CPU path (oracle port, float64 dense dequantized matvec, numpy
+    BLAS on all host threads) on a 2-block slice of the same model and plan;
+    tokens/s extrapolated x n_blocks/2. Returns (tokens_per_s, seconds, sample)."""
+    from oracle import dpq_oracle as O
+    from paper_2508_06041_b200 import model as M
+    nb = max(l.block for l in host_layers) + 1
+    scfg = M.ModelConfig(nb, cfg.d_model, cfg.n_heads, cfg.d_ff, cfg.vocab, cfg.seq_cap, cfg.norm_eps,
+                         cfg.n_kv_heads)
+    w = M.ModelWeights(scfg, weights.embed, weights.lm_head, {})
+    pls = {l: plan.layers[l] for l in host_layers}
+    Ms = {l: plan.M[l] for l in host_layers}
+    eng = O.Engine(w, host_layers, pls, Ms)
+    toks = np.random.default_rng(seed).integers(0, cfg.vocab, n_tokens + 3)
+    t0 = time.perf_counter()
+    eng.step(int(toks[0]), dynamic=False)            # prefill: warms the prefill-bit caches
+    eng.step(int(toks[1]))                           # warms the dynamic bit caches
+    eng.step(int(toks[2]))
+    warm = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    for t in toks[3:]:
+        eng.step(int(t))
+    dt = (time.perf_counter() - t1) / n_tokens
+    per_token_full = dt * cfg.n_blocks / nb
+    sample = (f"{n_tokens} warm decode steps of a {nb}-block slice of the same model and plan "
+              f"(dequant caches warmed in {warm:.1f}s), extrapolated x{cfg.n_blocks / nb:g} blocks")
+    return 1.0 / per_token_full, sample
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU implementation (oracle port) of the
+    path, timed on this host's cores, same metric/config."""
+    import torch  # noqa: F401
+    from oracle import dpq_oracle as O
+    from paper_2508_06041_b200 import estimator as E
+    from paper_2508_06041_b200 import model as M
+    from paper_2508_06041_b200 import runtime as R
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg, n_bits, b_min = model_config(args.config)
+    nb = 2
+    rng = np.random.default_rng(0)
+    host, plan_layers = {}, {}
+    d = cfg.d_model
+    embed = rng.normal(0.0, 1.0, (cfg.vocab, d)).astype(np.float32)
+    lm = (rng.normal(0.0, 1.0, (cfg.vocab, d)) * (0.1 / np.sqrt(d))).astype(np.float32)
+    lo_b = int(np.floor(args.target))
+    for b in range(nb):
+        for k in M.KINDS:
+            lid = M.LayerId(b, k)
+            rows, cols = M.layer_shape(cfg, lid)
+            W = rng.standard_normal((rows, cols), dtype=np.float32) * np.float32(1 / np.sqrt(cols))
+            q = O.quantize_layer(W, n_bits, b_min)
+            host[lid] = q
+            Gs = rng.standard_normal((64, cols)) * 1e-3
+            est = E.ErrorEstimator(E.ProjectionEstimator(Gs, 64, 0), E.IMMEDIATE, (lo_b, lo_b + 1))
+            plan_layers[lid] = R.PlanLayer(lid, lo_b + 1, args.target, (lo_b, lo_b + 1), 0.0, 0.5, est)
+    scfg = M.ModelConfig(nb, d, cfg.n_heads, cfg.d_ff, cfg.vocab, cfg.seq_cap, cfg.norm_eps, cfg.n_kv_heads)
+    w = M.ModelWeights(scfg, embed, lm, {})
+    Ms = {l: int(np.prod(q.shape)) for l, q in host.items()}
+    eng = O.Engine(w, host, plan_layers, Ms)
+    toks = rng.integers(0, cfg.vocab, args.warmup + args.steps + 1)
+    eng.step(int(toks[0]), dynamic=False)
+    for t in toks[1:1 + args.warmup]:
+        eng.step(int(t))
+    t0 = time.perf_counter()
+    for t in toks[1 + args.warmup:]:
+        eng.step(int(t))
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    full = dt * cfg.n_blocks / nb
+    v = 1.0 / full
+    cores = os.cpu_count()
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": full * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic random-init weights (init_model law), synthetic tokens",
+            "config": {"workload": f"{args.config}-shaped decode, batch 1, {args.target}-bit DP plan "
+                                   f"(2-block slice, extrapolated x{cfg.n_blocks // nb})",
+                       "n_blocks": cfg.n_blocks, "d_model": cfg.d_model, "d_ff": cfg.d_ff},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{args.steps} decode steps of a 2-block slice after {args.warmup} "
+                                       f"warm-up steps, extrapolated x{cfg.n_blocks // nb}"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2508_06041_b200 import runtime as R
+    from paper_2508_06041_b200 import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg, n_bits, b_min = model_config(args.config)
+    t_build = time.perf_counter()
+    keep = 2 if (rank == 0 and not args.no_cpu_baseline) else 0
+    weights, store, host = synth.random_device_model(cfg, n_bits, b_min, seed=1234, keep_host_blocks=keep)
+    pairs, prefill, high = pairs_for_target(store, args.target)
+    plan = synth.projection_plan(store, pairs, prefill, k=64, seed=0, target=args.target)
+    calib = np.random.default_rng(7).integers(0, cfg.vocab, 48)
+    synth.calibrate_thresholds(weights, store, plan, calib, high_rate=high, g_dtype=args.g_dtype)
+    build_s = time.perf_counter() - t_build
+
+    ids = store.ordered_ids()
+    eng = R.DecodeEngine(weights, store, plan, g_dtype=args.g_dtype)
+    stream = torch.cuda.Stream()
+    prompt = np.random.default_rng(11 + rank).integers(0, cfg.vocab, PROMPT)
+    eng.prefill(prompt)
+    from paper_2508_06041_b200 import _lib
+    import ctypes as C
+    sp = C.c_void_p(stream.cuda_stream)
+    total = args.warmup + args.steps
+    if PROMPT + total + 4 > cfg.seq_cap:
+        raise SystemExit("steps exceed seq_cap")
+    _lib.call("dpq_session_launch_steps", eng._h, args.warmup, sp)
+    stream.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    _lib.call("dpq_session_launch_steps", eng._h, args.steps, sp)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    eng._pos += total
+    eng.trace.estimator_ops += eng._ops_per_step * total
+    eng._sync_trace()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * 1000.0 / ms_per_step
+    eff_bits = float(np.mean([s.effective_bits for s in eng.trace.steps[-args.steps:]]))
+    high_frac = float(np.mean([[s.bits[l] == plan.layers[l].pair[1] for l in ids]
+                               for s in eng.trace.steps[-args.steps:]]))
+
+    # ---- roofline of the dominant kernel: per-launch CUDA-event times of the
+    # fused selector+GEMV ops on one eager step (profile_ops)
+    n_ops = 4 * cfg.n_blocks
+    op_ms = np.zeros(n_ops, dtype=np.float32)
+    nout = C.c_int()
+    tok = int(np.random.default_rng(3).integers(0, cfg.vocab))
+    reps = []
+    for rep in range(3):
+        _lib.call("dpq_session_profile_ops", eng._h, tok, 1, C.c_void_p(op_ms.ctypes.data), n_ops, C.byref(nout))
+        eng._pos += 1
+        eng.trace.estimator_ops += eng._ops_per_step
+        eng._sync_trace()
+        bits_row = [eng.trace.steps[-1].bits[l] for l in ids]
+        by = op_bytes(store, plan, bits_row, ids, {"f32": 4, "f16": 2, "e4m3": 1}[args.g_dtype])
+        reps.append((op_ms[:nout.value].copy(), by[:nout.value]))
+    op_t = np.mean([r[0] for r in reps], axis=0)
+    op_b = np.mean([r[1] for r in reps], axis=0)
+    achieved = float(op_b.sum() / (op_t.sum() * 1e-3) / 1e9)
+    peak, peak_kind = measured_peak()
+    gemv_share = float(op_t.sum())
+
+    # ---- selector overhead: static sentinel plans at l and h, interpolated at
+    # the realized effective bits (same per-layer pairs, no estimators)
+    overhead = None
+    static_ms = {}
+    if not args.skip_static:
+        from paper_2508_06041_b200.runtime import sentinel_static_plan
+        for bit in sorted(set(p for pr in pairs.values() for p in pr)):
+            sp_plan = sentinel_static_plan({l: bit for l in ids}, store.param_counts(), float(bit))
+            e2 = R.DecodeEngine(weights, store, sp_plan)
+            e2.prefill(prompt)
+            _lib.call("dpq_session_launch_steps", e2._h, args.warmup, sp)
+            stream.synchronize()
+            e0.record(stream)
+            _lib.call("dpq_session_launch_steps", e2._h, args.steps, sp)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            static_ms[bit] = e0.elapsed_time(e1) / args.steps
+            e2.close()
+        bl = sorted(static_ms)
+        if len(bl) == 2:
+            t_static = static_ms[bl[0]] + (static_ms[bl[1]] - static_ms[bl[0]]) * (eff_bits - bl[0]) / (bl[1] - bl[0])
+        else:
+            t_static = static_ms[bl[0]]
+        overhead = (ms_per_step - t_static) / t_static
+
+    # ---- e2e through the public step API: host token in, host logits out
+    n_e2e = min(32, cfg.seq_cap - eng._pos - 1)
+    toks = np.random.default_rng(5).integers(0, cfg.vocab, n_e2e)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for t in toks:
+        eng.step(int(t), dynamic=True)
+    e2e_s = (time.perf_counter() - t0) / n_e2e
+    e2e_value = world * 1.0 / e2e_s
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: random-init Llama-3-8B-shaped weights (W ~ N(0,1/cols)), random tokens",
+            "config": {"workload": f"{args.config}-shaped batch-1 greedy decode, DP plan {args.target}-bit "
+                                   f"target, (3,4) pairs, k=64 projection selector ({args.g_dtype} G)",
+                       "n_blocks": cfg.n_blocks, "d_model": cfg.d_model, "n_heads": cfg.n_heads,
+                       "n_kv_heads": cfg.kv_heads, "d_ff": cfg.d_ff, "vocab": cfg.vocab,
+                       "n_bits": n_bits, "b_min": b_min, "prompt": PROMPT,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2_policy": "weights (3.5 GB of bitplanes) >> 126 MB L2; no flush needed",
+                       "realized_effective_bits": eff_bits, "high_decision_rate": high_frac,
+                       "selector_overhead": overhead, "static_ms_per_step": static_ms,
+                       "build_s": build_s},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "op_kernel (fused selector + bitplane GEMV)",
+                         "ops_per_step": int(nout.value), "op_ms_per_step": gemv_share,
+                         "op_bytes_per_step": float(op_b.sum())},
+            "clocks": clk,
+            "gpu_launches": int(args.steps * (2 + 5 * cfg.n_blocks)),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 12,
+                    "d2h_bytes_per_step": 4 * cfg.vocab}}
+    if rank == 0 and not args.no_cpu_baseline and host:
+        v, sample = cpu_slice_oracle(cfg, host, plan, weights)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                                "sample": sample}
+    traffic_path = os.path.join(ROOT, "profiles", "op_kernel_traffic.json")
+    if os.path.exists(traffic_path):
+        try:
+            line["roofline"]["traffic"] = json.load(open(traffic_path)).get("bytes_per_launch")
+        except Exception:
+            pass
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -138,6 +138,11 @@ int dpq_session_launch_steps(dpq_session* ss, int n, void* stream);
  * exact errors f32, each [n_steps][n_layers]. */
 int dpq_session_trace(dpq_session* ss, int* n_steps, int8_t* bits, float* est, float* exact);
 int dpq_session_position(dpq_session* ss, int* pos);
+/* Diagnostics: run one step eagerly (no graph) with CUDA events around every
+ * fused selector+GEMV op launch; op_ms receives the per-launch device time
+ * in schedule order (4 ops per block: qkv, o, up|gate, down). */
+int dpq_session_profile_ops(dpq_session* ss, int token, int dynamic, float* op_ms, int max_ops,
+                            int* n_ops);
 int dpq_session_logits_dev(dpq_session* ss, float** logits_dev);
 
 /* Host-side reference of the device plane layout (test infrastructure for the

@@ -302,3 +302,33 @@ def file_hash(path: str) -> str:
         for chunk in iter(lambda: f.read(1 << 20), b""):
             h.update(chunk)
     return h.hexdigest()
+
+
+class _ShapeOnly:
+    """Layer placeholder of a device-only store (codes live on the GPU)."""
+
+    def __init__(self, shape, n_bits, b_min):
+        self.shape = tuple(shape)
+        self.n_bits, self.b_min = n_bits, b_min
+
+
+class DeviceBitPlaneStore:
+    """A BitPlaneStore whose codes exist only as device bitplanes (models too
+    large to hold as host uint16 codes). Quacks like BitPlaneStore for the
+    decode engine: config_hash, layers (shapes), param_counts, ordered_ids,
+    device_store."""
+
+    def __init__(self, config_hash, n_bits, b_min, shapes: dict, dstore: DeviceStore):
+        self.config_hash = config_hash
+        self.n_bits, self.b_min = n_bits, b_min
+        self.layers = {lid: _ShapeOnly(s, n_bits, b_min) for lid, s in shapes.items()}
+        self._dev = dstore
+
+    def param_counts(self) -> dict:
+        return {lid: int(np.prod(q.shape)) for lid, q in self.layers.items()}
+
+    def ordered_ids(self):
+        return sorted(self.layers, key=lambda l: (l.block, KINDS.index(l.kind)))
+
+    def device_store(self) -> DeviceStore:
+        return self._dev
