@@ -144,6 +144,9 @@ int dpq_session_position(dpq_session* ss, int* pos);
 int dpq_session_profile_ops(dpq_session* ss, int token, int dynamic, float* op_ms, int max_ops,
                             int* n_ops);
 int dpq_session_logits_dev(dpq_session* ss, float** logits_dev);
+/* Diagnostics (env DPQ_DEBUG_TIMES=1 at session creation): per-CTA phase
+ * timestamps (globaltimer ns) of every op of the last step, [op][per_op]. */
+int dpq_session_debug_times(dpq_session* ss, uint64_t* out, int64_t n, int* per_op);
 
 /* Host-side reference of the device plane layout (test infrastructure for the
  * repack; the product path repacks on the device). */

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <utility>
 #include <algorithm>
@@ -222,6 +223,8 @@ struct dpq_session {
   cudaGraphExec_t gexec = nullptr;
   int pos_host = 0;
   int steps_host = 0;
+  unsigned long long* dbg = nullptr;
+  int dbg_per_op = 0;
 };
 
 // ---------------------------------------------------------------------------

@@ -124,6 +124,7 @@ struct OpDesc {
   float* tr_exact;          // [max_steps][n_trace]
   int n_trace;
   int max_steps;
+  unsigned long long* dbg;  // optional per-CTA phase timestamps [grid][8] (globaltimer ns)
   OpLayer layer[kMaxOpLayers];
 };
 

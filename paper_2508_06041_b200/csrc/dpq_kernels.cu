@@ -31,6 +31,13 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
 __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define DPQ_STAMP(i) \
+  do { if (D.dbg && threadIdx.x == 0) D.dbg[blockIdx.x * 8 + (i)] = gtimer(); } while (0)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -61,6 +68,62 @@ __device__ double block_sum_d(double v, double* red) {
   for (int i = 0; i < nw; ++i) t += red[i];   // fixed order: deterministic
   __syncthreads();
   return t;
+}
+
+// Three block-wide double sums with one barrier round (all threads get them).
+__device__ void block_sum3(double& a, double& b, double& c, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  a = warp_sum(a); b = warp_sum(b); c = warp_sum(c);
+  __syncthreads();
+  if (lane == 0) { red[warp] = a; red[32 + warp] = b; red[64 + warp] = c; }
+  __syncthreads();
+  double ta = 0.0, tb = 0.0, tc = 0.0;
+  for (int i = 0; i < nw; ++i) { ta += red[i]; tb += red[32 + i]; tc += red[64 + i]; }
+  a = ta; b = tb; c = tc;
+}
+
+// Dot of one 512-column G row slice (window) with xin[512] (smem), one warp,
+// vector loads: f32 4x float4 / f16 2x 8 halves / e4m3 1x 16 bytes per lane.
+__device__ __forceinline__ float g_dot(const void* Grow, int g_dtype, const float* xin, int lane) {
+  float acc = 0.f;
+  if (g_dtype == G_F16) {
+    const uint4* g = reinterpret_cast<const uint4*>(Grow);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint4 v = __ldg(g + j * 32 + lane);
+      const int c0 = (j * 32 + lane) * 8;
+      const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __half22float2(h[q]);
+        acc += f.x * xin[c0 + 2 * q] + f.y * xin[c0 + 2 * q + 1];
+      }
+    }
+  } else if (g_dtype == G_E4M3) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(Grow) + lane);
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(&v);
+    const int c0 = lane * 16;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      __nv_fp8_e4m3 e;
+      e.__x = b[q];
+      acc += float(e) * xin[c0 + q];
+    }
+  } else {
+    const float4* g = reinterpret_cast<const float4*>(Grow);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 v = __ldg(g + j * 32 + lane);
+      const int c0 = (j * 32 + lane) * 4;
+      acc += v.x * xin[c0] + v.y * xin[c0 + 1] + v.z * xin[c0 + 2] + v.w * xin[c0 + 3];
+    }
+  }
+  return warp_sum(acc);
+}
+
+__device__ __forceinline__ long long g_row_bytes(int g_dtype) {
+  return g_dtype == G_F16 ? 2 * kWinCols : (g_dtype == G_E4M3 ? kWinCols : 4 * kWinCols);
 }
 
 __device__ __forceinline__ float load_g(const void* G, int g_dtype, long long idx) {
@@ -142,18 +205,17 @@ __device__ __forceinline__ void build_lut(float* lut, const float* xw) {
 struct OpSmem {
   float xw[kWinCols];        // current input window (pre-scale)
   float xp[kWinCols];        // estimator input window when it is not xw
-  double red[32];
-  int bits[kMaxOpLayers];    // known bits per layer (-1 = pending decision)
+  double red[96];
+  double lay_q[kMaxOpLayers * 4];
+  int la[kMaxOpLayers];      // planes streamed before a decision
+  int lb[kMaxOpLayers];      // final plane count (-1 = pending decision)
   int is_last;
   unsigned my_gen;
   double xp_scale;           // scale turning xp into the estimator input
   const float* xp_src;       // source vector of xp (nullptr: estimator uses xw)
-  int tasks;                 // number of tasks in the current batch
-  short task_tile[32 * 8];
-  signed char task_plane[32 * 8];
 };
 
-constexpr int kBatchTiles = 32;
+constexpr int kWarpTiles = 8;                 // owned tiles per warp per chunk
 constexpr uint32_t kLutShared = 0x10000;     // shared address of the LUT
 constexpr int kOpSmemBytes = (int)((sizeof(OpSmem) + 127) / 128 * 128);
 
@@ -178,8 +240,8 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
   float* lut = reinterpret_cast<float*>(smem_raw + (kLutShared - sbase));
   OpSmem& sm = *reinterpret_cast<OpSmem*>(smem_raw);
-  float* Psm = reinterpret_cast<float*>(smem_raw + kOpSmemBytes);  // [kBatchTiles][8][32]
-  if (kOpSmemBytes + kBatchTiles * 8 * 32 * 4 > kLutShared - sbase) __trap();
+  // below the LUT: OpSmem, then S / S_l per warp-owned tile [2][16 warps][kWarpTiles][32]
+  if (kOpSmemBytes + 2 * kThreads * kWarpTiles * 4 > kLutShared - sbase) __trap();
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
@@ -217,7 +279,9 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
       }
     }
   }
+  DPQ_STAMP(0);
   pdl_wait();
+  DPQ_STAMP(1);
   if (tid == 0) sm.my_gen = *reinterpret_cast<volatile unsigned*>(&D.sync->gen);
 
   // ---- prologue: input window, estimator-input window, window stats --------
@@ -271,15 +335,14 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
     if (D.need_snap && j == 0 && c < D.cols)
       D.snap[((size_t)ctl->snap_w * D.n_snap + D.snap_idx) * D.snap_stride + c] = v;
   }
-  s1 = block_sum_d(s1, sm.red);
-  s2 = block_sum_d(s2, sm.red);
-  s3 = block_sum_d(s3, sm.red);
+  __syncthreads();
+  build_lut(lut, sm.xw);
+  block_sum3(s1, s2, s3, sm.red);
   if (tid == 0) {
     double* ws = D.win_stats + 4 * w;
     ws[0] = s1; ws[1] = s2; ws[2] = s3; ws[3] = 0.0;
   }
-  build_lut(lut, sm.xw);
-  __syncthreads();
+  DPQ_STAMP(2);
 
   // ---- P1: projection-estimator partial dot products (window slice) ------
   if (mode == MODE_DYNAMIC) {
@@ -301,11 +364,8 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
         }
         const DevSel& S = D.layer[li].S;
         const bool use_p = sm.xp_src && (S.prev_residual || D.est_in);
-        const float* xin = use_p ? sm.xp : sm.xw;
-        const long long base = ((long long)w * S.k + i) * kWinCols;
-        float acc = 0.f;
-        for (int c = lane; c < kWinCols; c += 32) acc += load_g(S.G, S.g_dtype, base + c) * xin[c];
-        acc = warp_sum(acc);
+        const char* grow = reinterpret_cast<const char*>(S.G) + ((long long)w * S.k + i) * g_row_bytes(S.g_dtype);
+        const float acc = g_dot(grow, S.g_dtype, use_p ? sm.xp : sm.xw, lane);
         if (lane == 0) D.gx_part[((size_t)li * n_win + w) * kMaxK + i] = acc;
       }
     }
@@ -319,6 +379,7 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
     sm.is_last = (old == (unsigned)G - 1);
   }
   __syncthreads();
+  DPQ_STAMP(3);
   if (sm.is_last) {
     __threadfence();
     // op input statistics
@@ -328,9 +389,7 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
       t2 += __ldcg(D.win_stats + 4 * i + 1);
       t3 += __ldcg(D.win_stats + 4 * i + 2);
     }
-    t1 = block_sum_d(t1, sm.red);
-    t2 = block_sum_d(t2, sm.red);
-    t3 = block_sum_d(t3, sm.red);
+    block_sum3(t1, t2, t3, sm.red);
     const double inv = 1.0 / sqrt(t2 / (double)D.cols + (double)D.eps);
     if (tid == 0) {
       D.op_stats[0] = (float)t1;
@@ -341,7 +400,27 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
         st[0] = (float)t1; st[1] = (float)t2; st[2] = (float)inv; st[3] = 0.f;
       }
     }
-    // estimates and decisions
+    // projection norms: thread (li, i) sums its window partials; 4 warps per layer
+    if (mode == MODE_DYNAMIC) {
+      const int li = tid / kMaxK, i = tid % kMaxK;
+      double q = 0.0;
+      if (li < D.n_layers) {
+        const DevSel& S = D.layer[li].S;
+        if (S.sentinel == 0 && S.est_kind == EST_PROJECTION && i < S.k) {
+          const float* gp = D.gx_part + (size_t)li * n_win * kMaxK + i;
+          float g0 = 0.f, g1 = 0.f;
+          int ww = 0;
+          for (; ww + 1 < n_win; ww += 2) { g0 += __ldcg(gp + (size_t)ww * kMaxK); g1 += __ldcg(gp + (size_t)(ww + 1) * kMaxK); }
+          if (ww < n_win) g0 += __ldcg(gp + (size_t)ww * kMaxK);
+          float g = g0 + g1;
+          if (S.g_scale) g *= S.g_scale[i];
+          q = (double)g * (double)g;
+        }
+      }
+      q = warp_sum(q);
+      if (lane == 0 && warp < kMaxOpLayers * 4) sm.lay_q[warp] = q;
+      __syncthreads();
+    }
     for (int li = 0; li < D.n_layers; ++li) {
       const OpLayer& Ly = D.layer[li];
       const DevSel& S = Ly.S;
@@ -351,14 +430,7 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
       const bool prev = sm.xp_src && (S.prev_residual || D.est_in);
       const double in_scale = prev ? sm.xp_scale : (D.in_mode == IN_RMS ? inv : 1.0);
       if (S.sentinel == 0 && S.est_kind == EST_PROJECTION) {
-        double q = 0.0;
-        for (int i = tid; i < S.k; i += kThreads) {
-          float g = 0.f;
-          for (int ww = 0; ww < n_win; ++ww) g += __ldcg(D.gx_part + ((size_t)li * n_win + ww) * kMaxK + i);
-          if (S.g_scale) g *= S.g_scale[i];
-          q += (double)g * (double)g;
-        }
-        q = block_sum_d(q, sm.red);
+        const double q = sm.lay_q[4 * li] + sm.lay_q[4 * li + 1] + sm.lay_q[4 * li + 2] + sm.lay_q[4 * li + 3];
         est = in_scale * sqrt(q);
         have_est = true;
       } else if (S.sentinel == 0 && S.est_kind == EST_LINEAR) {
@@ -391,164 +463,213 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
     }
   }
 
+  DPQ_STAMP(4);
   // ---- per-layer plane counts known to this CTA ----------------------------
   if (tid < D.n_layers) {
     int a, b, pend;
     layer_planes(D.layer[tid], mode, ctl, a, b, pend);
-    sm.bits[tid] = pend ? -1 : b;
+    sm.la[tid] = (pend == 2) ? 0 : a;        // planes streamed before any decision
+    sm.lb[tid] = pend ? -1 : b;              // final plane count, -1 = pending
   }
   __syncthreads();
-
   // Let the next kernel's CTAs start (their L2 prefetch overlaps our stream).
   pdl_launch();
 
-  // ---- tiles, in batches ---------------------------------------------------
+  // ---- warp-owned tiles: tiles t_begin + warp + kW*i, all planes per warp --
+  constexpr int kW = kThreads / 32;
   const uint32_t lanereg = kLutShared | ((uint32_t)lane * 4u);
-  bool waited = false;
-  for (int bt0 = t_begin; bt0 < t_end; bt0 += kBatchTiles) {
-    const int bt1 = min(t_end, bt0 + kBatchTiles);
+  float* Ssm = reinterpret_cast<float*>(smem_raw + kOpSmemBytes) + warp * (kWarpTiles * 32);
+  float* Slsm = reinterpret_cast<float*>(smem_raw + kOpSmemBytes) + (kW + warp) * (kWarpTiles * 32);
+  const int n_ct = t_end - t_begin;
+  const int n_my = n_ct > warp ? (n_ct - warp + kW - 1) / kW : 0;
+  int fb0 = sm.lb[0], fb1 = D.n_layers > 1 ? sm.lb[1] : 0, fb2 = D.n_layers > 2 ? sm.lb[2] : 0;
+  bool decided = (fb0 >= 0) && (fb1 >= 0) && (fb2 >= 0);
+  auto final_bits = [&](int li) { return li == 0 ? fb0 : (li == 1 ? fb1 : fb2); };
+  auto layer_of = [&](int t) {
+    int li = 0;
+    while (li + 1 < D.n_layers && t >= D.layer[li + 1].tile_off) ++li;
+    return li;
+  };
+
+  for (int c0 = 0; c0 < n_my; c0 += kWarpTiles) {
+    const int nc = min(kWarpTiles, n_my - c0);
+    // lane i < nc describes owned tile i of this chunk
+    const int my_t = lane < nc ? t_begin + warp + kW * (c0 + lane) : -1;
+    const int my_li = lane < nc ? layer_of(my_t) : 0;
+    for (int i = 0; i < nc; ++i) Ssm[i * 32 + lane] = 0.f;
+    __syncwarp();
+
     for (int phase = 0; phase < 2; ++phase) {
       if (phase == 1) {
-        // decisions needed for pending layers with tiles in this batch?
-        bool need = false;
-        for (int li = 0; li < D.n_layers; ++li) {
-          const OpLayer& Ly = D.layer[li];
-          if (sm.bits[li] >= 0) continue;
-          if (max(bt0, Ly.tile_off) < min(bt1, Ly.tile_off + Ly.L.n_tiles)) need = true;
-        }
-        if (need && !waited) {
-          if (tid == 0) {
-            while (ld_acquire(&D.sync->gen) == sm.my_gen) __nanosleep(64);
+        // decisions of pending layers (one spin per warp, lane 0)
+        if (!decided) {
+          bool need = false;
+          for (int i = 0; i < nc; ++i) {
+            const int li = __shfl_sync(0xffffffffu, my_li, i);
+            if (final_bits(li) < 0) need = true;
           }
-          __syncthreads();
-          if (tid < D.n_layers && sm.bits[tid] < 0) sm.bits[tid] = __ldcg(D.decision + tid);
-          __syncthreads();
-          waited = true;
+          if (!need) break;
+          DPQ_STAMP(5);
+          if (lane == 0) {
+            while (ld_acquire(&D.sync->gen) == sm.my_gen) __nanosleep(32);
+          }
+          __syncwarp();
+          if (fb0 < 0) fb0 = __ldcg(D.decision + 0);
+          if (fb1 < 0) fb1 = __ldcg(D.decision + 1);
+          if (fb2 < 0) fb2 = __ldcg(D.decision + 2);
+          decided = true;
+          DPQ_STAMP(6);
         }
-        if (!need) break;
       }
-      // task list for this batch/phase
-      if (tid == 0) {
-        int n = 0;
-        for (int t = bt0; t < bt1; ++t) {
-          int li = 0;
-          while (t >= D.layer[li].tile_off + D.layer[li].L.n_tiles) ++li;
-          int a, b, pend;
-          layer_planes(D.layer[li], mode, ctl, a, b, pend);
-          int p0, p1;
-          if (phase == 0) {
-            p0 = 0;
-            p1 = pend == 2 ? 0 : a;
-          } else {
-            p0 = pend == 2 ? 0 : a;
-            p1 = sm.bits[li];
-          }
-          for (int p = p0; p < p1; ++p) {
-            sm.task_tile[n] = (short)(t - bt0);
-            sm.task_plane[n] = (signed char)p;
-            ++n;
-          }
+      // per-tile plane range of this phase
+      int p0 = 0, p1 = 0;
+      if (lane < nc) {
+        const int la = sm.la[my_li];
+        if (phase == 0) { p0 = 0; p1 = la; }
+        else {
+          const int fb = final_bits(my_li);
+          const bool was_pending = sm.lb[my_li] < 0;
+          p0 = la;
+          p1 = was_pending ? fb : la;
         }
-        sm.tasks = n;
       }
-      __syncthreads();
-      const int ntask = sm.tasks;
-      // warp-strided tasks with one-task-ahead register prefetch
-      int tk = warp;
-      uint4 n0, n1, n2, n3;
-      auto task_src = [&](int k) -> const uint4* {
-        const int t = bt0 + sm.task_tile[k];
-        int li = 0;
-        while (t >= D.layer[li].tile_off + D.layer[li].L.n_tiles) ++li;
+      // exclusive prefix of task counts across the owned tiles
+      const int cnt = p1 > p0 ? p1 - p0 : 0;
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int start = lane < nc ? incl - cnt : 0x7fffffff;
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      if (total == 0) continue;
+      auto task_tile = [&](int k) { return __popc(__ballot_sync(0xffffffffu, start <= k)) - 1; };
+      auto task_src = [&](int k, int& ti, int& pl) -> const uint4* {
+        ti = task_tile(k);
+        const int t = __shfl_sync(0xffffffffu, my_t, ti);
+        const int li = __shfl_sync(0xffffffffu, my_li, ti);
+        pl = __shfl_sync(0xffffffffu, p0, ti) + (k - __shfl_sync(0xffffffffu, start, ti));
         const DevLayer& L = D.layer[li].L;
-        return L.planes + sm.task_plane[k] * L.plane_stride16 +
-               ((long long)w * L.n_tiles + (t - D.layer[li].tile_off)) * (kTileBytes / 16);
+        return L.planes + pl * L.plane_stride16 +
+               ((long long)w * L.n_tiles + (t - D.layer[li].tile_off)) * (kTileBytes / 16) + lane;
       };
-      if (tk < ntask) {
-        const uint4* s = task_src(tk);
-        n0 = ldg_stream(s + lane); n1 = ldg_stream(s + 32 + lane);
-        n2 = ldg_stream(s + 64 + lane); n3 = ldg_stream(s + 96 + lane);
+      // 3-deep register pipeline over this warp's tasks (tile-major, plane
+      // ascending) with Horner accumulation S = 2 S + P_p per owned tile.
+      uint4 qa0, qa1, qa2, qa3, qb0, qb1, qb2, qb3, qc0, qc1, qc2, qc3;
+      int ta = 0, tb = 0, tc = 0, pa = 0, pb = 0, pc = 0;
+      float S = 0.f;
+      int cur = -1;
+      auto flush_to = [&](int ti) {
+        if (cur >= 0) Ssm[cur * 32 + lane] = S;
+        cur = ti;
+        S = (phase == 1) ? Ssm[ti * 32 + lane] : 0.f;
+      };
+#define DPQ_LOAD(X, T, PL, k)                                                         \
+  {                                                                                   \
+    const uint4* s_ = task_src(k, T, PL);                                             \
+    X##0 = ldg_stream(s_); X##1 = ldg_stream(s_ + 32);                                \
+    X##2 = ldg_stream(s_ + 64); X##3 = ldg_stream(s_ + 96);                           \
+  }
+#define DPQ_RUN(X, T, PL, k)                                                          \
+  {                                                                                   \
+    const float P_ = plane_task(X##0, X##1, X##2, X##3, lanereg);                     \
+    if ((T) != cur) flush_to(T);                                                      \
+    S = 2.f * S + P_;                                                                 \
+    {                                                                                 \
+      const int lsel_ = D.layer[__shfl_sync(0xffffffffu, my_li, T)].S.l;              \
+      const bool dual_ = D.layer[__shfl_sync(0xffffffffu, my_li, T)].dual && mode == MODE_DYNAMIC; \
+      if (dual_ && (PL) == lsel_ - 1) Slsm[(T) * 32 + lane] = S;                      \
+    }                                                                                 \
+    if ((k) + 3 < total) DPQ_LOAD(X, T, PL, (k) + 3);                                 \
+  }
+      DPQ_LOAD(qa, ta, pa, 0);
+      if (1 < total) DPQ_LOAD(qb, tb, pb, 1);
+      if (2 < total) DPQ_LOAD(qc, tc, pc, 2);
+      for (int k = 0; k < total; k += 3) {
+        DPQ_RUN(qa, ta, pa, k);
+        if (k + 1 >= total) break;
+        DPQ_RUN(qb, tb, pb, k + 1);
+        if (k + 2 >= total) break;
+        DPQ_RUN(qc, tc, pc, k + 2);
       }
-      while (tk < ntask) {
-        const uint4 c0 = n0, c1 = n1, c2 = n2, c3 = n3;
-        const int cur = tk;
-        tk += kThreads / 32;
-        if (tk < ntask) {
-          const uint4* s = task_src(tk);
-          n0 = ldg_stream(s + lane); n1 = ldg_stream(s + 32 + lane);
-          n2 = ldg_stream(s + 64 + lane); n3 = ldg_stream(s + 96 + lane);
-        }
-        const float P = plane_task(c0, c1, c2, c3, lanereg);
-        Psm[((int)sm.task_tile[cur] * 8 + sm.task_plane[cur]) * 32 + lane] = P;
-      }
-      __syncthreads();
+#undef DPQ_RUN
+#undef DPQ_LOAD
+      if (cur >= 0) Ssm[cur * 32 + lane] = S;
+      __syncwarp();
     }
 
-    // ---- combine planes per tile, publish partial sums, tile epilogue ------
-    for (int t = bt0 + warp; t < bt1; t += kThreads / 32) {
-      int li = 0;
-      while (t >= D.layer[li].tile_off + D.layer[li].L.n_tiles) ++li;
-      const OpLayer& Ly = D.layer[li];
-      const bool dual = Ly.dual && mode == MODE_DYNAMIC;
-      const int bsel = sm.bits[li];
-      const float* Pt = Psm + (t - bt0) * 8 * 32;
-      const int row_g = t * 32 + lane;                 // op-global padded row
-      float S = 0.f;
-      for (int p = 0; p < bsel; ++p) S = 2.f * S + Pt[p * 32 + lane];
-      D.part[(size_t)w * D.rows_total_pad + row_g] = S;
-      if (dual) {
-        float Sl = 0.f;
-        for (int p = 0; p < Ly.S.l; ++p) Sl = 2.f * Sl + Pt[p * 32 + lane];
-        D.part_lo[(size_t)w * D.rows_total_pad + row_g] = Sl;
-      }
+    // ---- publish partial sums of the owned tiles; per-tile last arriver ----
+    // reduces over windows and applies the affine epilogue.
+    int bsel_i = lane < nc ? final_bits(my_li) : 0;
+    for (int i = 0; i < nc; ++i) {
+      const int t = __shfl_sync(0xffffffffu, my_t, i);
+      const int li = __shfl_sync(0xffffffffu, my_li, i);
+      const bool dual = D.layer[li].dual && mode == MODE_DYNAMIC;
+      const int row_g = t * 32 + lane;
+      D.part[(size_t)w * D.rows_total_pad + row_g] = Ssm[i * 32 + lane];
+      if (dual) D.part_lo[(size_t)w * D.rows_total_pad + row_g] = Slsm[i * 32 + lane];
+    }
+    __threadfence();
+    __syncwarp();
+    unsigned old = 0;
+    if (lane < nc) old = atomicAdd(D.tile_cnt + my_t, 1u);
+    const unsigned lastmask = __ballot_sync(0xffffffffu, lane < nc && old == (unsigned)n_win - 1);
+    if (lastmask) {
       __threadfence();
-      __syncwarp();
-      unsigned old = 0;
-      if (lane == 0) old = atomicAdd(D.tile_cnt + t, 1u);
-      old = __shfl_sync(0xffffffffu, old, 0);
-      if (old != (unsigned)n_win - 1) continue;
-      // last window for this tile: reduce over windows and apply the epilogue
-      __threadfence();
-      if (lane == 0) D.tile_cnt[t] = 0u;
+      if (lane < nc && ((lastmask >> lane) & 1u)) D.tile_cnt[my_t] = 0u;
       double sx = 0.0, sq = 0.0;
-      for (int i = lane; i < n_win; i += 32) {
-        sx += __ldcg(D.win_stats + 4 * i);
-        sq += __ldcg(D.win_stats + 4 * i + 1);
+      for (int ii = lane; ii < n_win; ii += 32) {
+        sx += __ldcg(D.win_stats + 4 * ii);
+        sq += __ldcg(D.win_stats + 4 * ii + 1);
       }
       sx = warp_sum(sx);
       sq = warp_sum(sq);
       const float scale = D.in_mode == IN_RMS ? (float)(1.0 / sqrt(sq / (double)D.cols + (double)D.eps)) : 1.f;
       const float sxf = (float)sx;
-      float St = 0.f, Stl = 0.f;
-      for (int ww = 0; ww < n_win; ++ww) {
-        St += __ldcg(D.part + (size_t)ww * D.rows_total_pad + row_g);
-        if (dual) Stl += __ldcg(D.part_lo + (size_t)ww * D.rows_total_pad + row_g);
-      }
-      const int r = row_g - Ly.tile_off * 32;          // row inside the layer
-      if (r < Ly.L.rows) {
-        const float lo = __ldg(Ly.L.lo + r), span = __ldg(Ly.L.span + r);
-        const int out_row = Ly.out_off + r;
-        if (!dual) {
-          const float sb = ldexpf(span, -bsel);
-          const float y = scale * (lo * sxf + sb * (St + 0.5f * sxf));
-          if (D.out_mode == OUT_ADD) D.out[out_row] += y;
-          else D.out[out_row] = y;
-        } else {
-          const float yh = scale * (lo * sxf + ldexpf(span, -Ly.S.h) * (St + 0.5f * sxf));
-          const float yl = scale * (lo * sxf + ldexpf(span, -Ly.S.l) * (Stl + 0.5f * sxf));
-          D.out_hi[out_row] = yh;
-          D.out_lo[out_row] = yl;
-          const float dd = yh - yl;
-          const double q = warp_sum((double)dd * (double)dd);
+      for (unsigned mk = lastmask; mk; mk &= mk - 1) {
+        const int i = __ffs(mk) - 1;
+        const int t = __shfl_sync(0xffffffffu, my_t, i);
+        const int li = __shfl_sync(0xffffffffu, my_li, i);
+        const int bsel = __shfl_sync(0xffffffffu, bsel_i, i);
+        const OpLayer& Ly = D.layer[li];
+        const bool dual = Ly.dual && mode == MODE_DYNAMIC;
+        const int row_g = t * 32 + lane;
+        float St0 = 0.f, St1 = 0.f, Stl = 0.f;
+        int ww = 0;
+        for (; ww + 1 < n_win; ww += 2) {
+          St0 += __ldcg(D.part + (size_t)ww * D.rows_total_pad + row_g);
+          St1 += __ldcg(D.part + (size_t)(ww + 1) * D.rows_total_pad + row_g);
+        }
+        if (ww < n_win) St0 += __ldcg(D.part + (size_t)ww * D.rows_total_pad + row_g);
+        const float St = St0 + St1;
+        if (dual)
+          for (int w2 = 0; w2 < n_win; ++w2) Stl += __ldcg(D.part_lo + (size_t)w2 * D.rows_total_pad + row_g);
+        const int r = row_g - Ly.tile_off * 32;
+        if (r < Ly.L.rows) {
+          const float lo = __ldg(Ly.L.lo + r), span = __ldg(Ly.L.span + r);
+          const int out_row = Ly.out_off + r;
+          if (!dual) {
+            const float y = scale * (lo * sxf + ldexpf(span, -bsel) * (St + 0.5f * sxf));
+            if (D.out_mode == OUT_ADD) D.out[out_row] += y;
+            else D.out[out_row] = y;
+          } else {
+            const float yh = scale * (lo * sxf + ldexpf(span, -Ly.S.h) * (St + 0.5f * sxf));
+            const float yl = scale * (lo * sxf + ldexpf(span, -Ly.S.l) * (Stl + 0.5f * sxf));
+            D.out_hi[out_row] = yh;
+            D.out_lo[out_row] = yl;
+            const float dd = yh - yl;
+            const double q = warp_sum((double)dd * (double)dd);
+            if (lane == 0) D.dual_sq[t] = (float)q;
+          }
+        } else if (dual) {
+          const double q = warp_sum(0.0);
           if (lane == 0) D.dual_sq[t] = (float)q;
         }
-      } else if (dual) {
-        const double q = warp_sum(0.0);
-        if (lane == 0) D.dual_sq[t] = (float)q;
       }
     }
-    __syncthreads();
   }
+  DPQ_STAMP(7);
 }
 
 // ---------------------------------------------------------------------------
