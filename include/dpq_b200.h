@@ -70,7 +70,7 @@ typedef struct {
   int32_t prime_from_prefill;
   int32_t use_graph;      /* capture the step into a CUDA graph               */
   int32_t use_pdl;        /* programmatic dependent launch between kernels    */
-  int32_t pad_;
+  int32_t use_persistent; /* one persistent step kernel (flag-linked stages)  */
 } dpq_model_desc;
 
 const char* dpq_last_error(void);
@@ -138,6 +138,8 @@ int dpq_session_launch_steps(dpq_session* ss, int n, void* stream);
  * exact errors f32, each [n_steps][n_layers]. */
 int dpq_session_trace(dpq_session* ss, int* n_steps, int8_t* bits, float* est, float* exact);
 int dpq_session_position(dpq_session* ss, int* pos);
+/* 1 if the session runs the persistent step kernel, 0 for the multi-kernel graph. */
+int dpq_session_is_persistent(dpq_session* ss);
 /* Diagnostics: run one step eagerly (no graph) with CUDA events around every
  * fused selector+GEMV op launch; op_ms receives the per-launch device time
  * in schedule order (4 ops per block: qkv, o, up|gate, down). */

@@ -37,7 +37,7 @@ class ModelDesc(C.Structure):
                 ("seq_cap", C.c_int32), ("norm_eps", C.c_float), ("embed", C.c_void_p),
                 ("lm_head", C.c_void_p), ("track_exact", C.c_int32),
                 ("async_prev_block", C.c_int32), ("prime_from_prefill", C.c_int32),
-                ("use_graph", C.c_int32), ("use_pdl", C.c_int32), ("pad_", C.c_int32)]
+                ("use_graph", C.c_int32), ("use_pdl", C.c_int32), ("use_persistent", C.c_int32)]
 
 
 P = C.c_void_p
@@ -67,6 +67,7 @@ _SIGS = {
     "dpq_session_launch_steps": ([P, C.c_int, P], C.c_int),
     "dpq_session_trace": ([P, C.POINTER(C.c_int), P, P, P], C.c_int),
     "dpq_session_position": ([P, C.POINTER(C.c_int)], C.c_int),
+    "dpq_session_is_persistent": ([P], C.c_int),
     "dpq_session_logits_dev": ([P, C.POINTER(P)], C.c_int),
     "dpq_session_profile_ops": ([P, C.c_int, C.c_int, P, C.c_int, C.POINTER(C.c_int)], C.c_int),
     "dpq_session_debug_times": ([P, P, C.c_int64, C.POINTER(C.c_int)], C.c_int),
@@ -104,7 +105,7 @@ def check(rc: int, what: str = "") -> None:
 def call(name, *args):
     fn = getattr(load(), name)
     rc = fn(*args)
-    if name not in ("dpq_planes_bytes", "dpq_version", "dpq_last_error"):
+    if name not in ("dpq_planes_bytes", "dpq_version", "dpq_last_error", "dpq_session_is_persistent"):
         check(rc, name)
     return rc
 

@@ -147,9 +147,10 @@ int launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStrea
 
 // Grid of an op: every window needs >= 1 CTA, never more CTAs than SMs
 // (the decision barrier needs all CTAs co-resident: 1 CTA/SM by smem).
+// Tile CTAs of an op (one SM is reserved for the op's decider CTA).
 int op_grid(const OpDesc& D, int n_sm) {
   long long units = (long long)D.n_win * D.total_tiles;
-  int g = (int)std::min<long long>(units, n_sm);
+  int g = (int)std::min<long long>(units, n_sm - 1);
   return std::max(g, D.n_win);
 }
 
@@ -169,6 +170,8 @@ struct dpq_store {
   Scratch scratch;
   Control* ctl = nullptr;
   OpSync* sync = nullptr;
+  unsigned* ctr = nullptr;
+  long long* gxa = nullptr;
   int* decision = nullptr;
   signed char* tr_bits = nullptr;
   float* tr_est = nullptr;
@@ -211,6 +214,8 @@ struct dpq_session {
   float* est_x = nullptr;            // exact-with-previous-input estimator input
   Scratch scratch;
   OpSync* syncs = nullptr;
+  unsigned* ctrs = nullptr;
+  long long* gxas = nullptr;
   int* decisions = nullptr;
   float *snap = nullptr, *snap_stats = nullptr;
   signed char* tr_bits = nullptr;
@@ -225,6 +230,13 @@ struct dpq_session {
   int steps_host = 0;
   unsigned long long* dbg = nullptr;
   int dbg_per_op = 0;
+  // persistent step kernel
+  bool persistent = false;
+  Scratch scratch2;                  // ping-pong scratch (ops alternate)
+  unsigned* flags = nullptr;
+  size_t n_flags = 0;
+  StepDesc step{};
+  std::vector<OpDesc> ops;           // main ops in execution order
 };
 
 // ---------------------------------------------------------------------------
@@ -369,6 +381,7 @@ extern "C" int dpq_store_create(int device, int n_layers, const dpq_layer_desc* 
   }
   if (s->scratch.make(s->arena, s->max_win, s->max_rows_pad, s->max_tiles) ||
       s->arena.alloc_t(&s->ctl, 1) || s->arena.alloc_t(&s->sync, 2) || s->arena.alloc_t(&s->decision, 4) ||
+      s->arena.alloc_t(&s->ctr, 128) || s->arena.alloc_t(&s->gxa, kMaxOpLayers * kMaxK) ||
       s->arena.alloc_t(&s->tr_bits, 4) || s->arena.alloc_t(&s->tr_est, 4) ||
       s->arena.alloc_t(&s->tr_exact, 4) || s->arena.alloc_t(&s->est_buf, s->max_cols))
     return fail(DPQ_ERR_CUDA);
@@ -417,6 +430,8 @@ OpDesc single_op(dpq_store* s, int layer, const DevSel& S, const float* x, float
   D.decision = s->decision;
   D.main_decision = s->decision;
   D.sync = s->sync;
+  D.ctr = s->ctr;
+  D.gxa = s->gxa;
   D.tr_bits = s->tr_bits;
   D.tr_est = s->tr_est;
   D.tr_exact = s->tr_exact;
@@ -447,7 +462,7 @@ __global__ void reset_trace1(signed char* bits, float* est, float* exact) {
 }
 
 int run_op(const OpDesc& D, Control* ctl, int n_sm, cudaStream_t st, bool pdl) {
-  const int g = op_grid(D, n_sm);
+  const int g = op_grid(D, n_sm) + 1;      // + the decider CTA
   return launch(op_kernel, dim3(g), dim3(kThreads), (size_t)kOpSmemAlloc, st, pdl, D, ctl);
 }
 

@@ -113,6 +113,8 @@ struct OpDesc {
   int* main_decision;       // estimation ops: the main op's decision array
   const float* est_in;      // standalone select_gemv: explicit estimator input
   OpSync* sync;
+  unsigned* ctr;            // per-op counters [128]: gdone, opdone, warr[n_win], tgrab[n_win]
+  long long* gxa;           // per-op projection accumulators [kMaxOpLayers][kMaxK], fixed point 2^-40
   // snapshots (async estimator inputs), each [2 slots][n_snap][snap_stride]
   float* snap;              // raw inputs
   float* snap_stats;        // [2][n_snap][4] = (sum, sumsq, inv, -)

@@ -16,6 +16,7 @@
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
 #include <math_constants.h>
+#include <cstdio>
 
 namespace dpq {
 
@@ -36,8 +37,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// Spin-wait watchdog: a wait that exceeds 2 s reports where it stalled and
+// traps, turning a would-be hang into a launch error.
+__device__ __noinline__ void dpq_hang(const char* what, int a, int b, unsigned v) {
+  printf("dpq watchdog: %s stalled (block %d thread %d, arg %d/%d, value %u)\n", what, blockIdx.x, threadIdx.x,
+         a, b, v);
+  __trap();
+}
+#define DPQ_SPIN_UNTIL(cond, what, a, b, v)                                   \
+  do {                                                                        \
+    const unsigned long long t0_ = gtimer();                                  \
+    while (!(cond)) {                                                         \
+      __nanosleep(20);                                                        \
+      if (gtimer() - t0_ > 2000000000ull) dpq_hang(what, (a), (b), (v));      \
+    }                                                                         \
+  } while (0)
 #define DPQ_STAMP(i) \
-  do { if (D.dbg && threadIdx.x == 0) D.dbg[blockIdx.x * 8 + (i)] = gtimer(); } while (0)
+  do { if (D.dbg && threadIdx.x == 0) D.dbg[X.cta * 8 + (i)] = gtimer(); } while (0)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -206,7 +222,7 @@ struct OpSmem {
   float xw[kWinCols];        // current input window (pre-scale)
   float xp[kWinCols];        // estimator input window when it is not xw
   double red[96];
-  double lay_q[kMaxOpLayers * 4];
+  int rank;                  // arrival rank of this CTA in its window
   int la[kMaxOpLayers];      // planes streamed before a decision
   int lb[kMaxOpLayers];      // final plane count (-1 = pending decision)
   int is_last;
@@ -233,106 +249,279 @@ __device__ __forceinline__ void layer_planes(const OpLayer& Ly, int mode, const 
   a = S.l; b = S.h; pending = 1;
 }
 
-extern "C" __global__ void __launch_bounds__(kThreads, 1)
-op_kernel(const OpDesc D, Control* __restrict__ ctl) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // Shared layout: [sbase, 0x10000): OpSmem + plane sums; [0x10000, +kLutBytes): LUT.
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
-  float* lut = reinterpret_cast<float*>(smem_raw + (kLutShared - sbase));
-  OpSmem& sm = *reinterpret_cast<OpSmem*>(smem_raw);
-  // below the LUT: OpSmem, then S / S_l per warp-owned tile [2][16 warps][kWarpTiles][32]
-  if (kOpSmemBytes + 2 * kThreads * kWarpTiles * 4 > kLutShared - sbase) __trap();
+// Per-call context of a fused op: which CTA of how many, readiness flags of
+// the producers of the input (persistent step kernel) and of our outputs.
+struct StageCtx {
+  int cta, G;
+  unsigned epoch;
+  const unsigned* dep0;     // producer flags covering the input (nullptr: none)
+  int dep0_off, dep0_rpf;   // flag index = off + column / rows_per_flag
+  const unsigned* dep1;     // second producer (IN_SILU gate half)
+  int dep1_off;
+  unsigned* out_flags;      // per output tile, set to epoch by the tile reducer
+  const OpDesc* next;       // next op: its always-planes are prefetched to L2
+};
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x;
+// Wait until flags f[i0, i1) all equal epoch. Call with a full warp: the
+// flags are polled lane-parallel (one L2 round trip per poll, not per flag).
+__device__ __forceinline__ void wait_flags_warp(const unsigned* f, int i0, int i1, unsigned epoch) {
+  const int lane = threadIdx.x & 31;
+  for (int base = i0; base < i1; base += 32) {
+    const int i = base + lane;
+    const unsigned long long t0 = gtimer();
+    while (!__all_sync(0xffffffffu, i >= i1 || ld_acquire(f + i) == epoch)) {
+      __nanosleep(20);
+      if (gtimer() - t0 > 2000000000ull) dpq_hang("readiness flags", i0, i1, epoch);
+    }
+  }
+}
+
+__device__ __forceinline__ void cta_window(const OpDesc& D, int cta, int G, int& w, int& j, int& m,
+                                           int& t_begin, int& t_end) {
+  w = cta % D.n_win;
+  j = cta / D.n_win;
+  m = (G - w + D.n_win - 1) / D.n_win;
+  t_begin = (int)((long long)D.total_tiles * j / m);
+  t_end = (int)((long long)D.total_tiles * (j + 1) / m);
+}
+
+// L2 prefetch of the always-streamed planes of this CTA's share of op D.
+__device__ void prefetch_op(const OpDesc& D, const Control* ctl, int cta, int G) {
+  if (cta >= G) return;
+  int w, j, m, t_begin, t_end;
+  cta_window(D, cta, G, w, j, m, t_begin, t_end);
+  const int mode = ctl->mode;
+  for (int li = 0; li < D.n_layers; ++li) {
+    const OpLayer& Ly = D.layer[li];
+    int a, b, pend;
+    layer_planes(Ly, mode, ctl, a, b, pend);
+    if (a <= 0) continue;
+    const int lt0 = max(t_begin, Ly.tile_off), lt1 = min(t_end, Ly.tile_off + Ly.L.n_tiles);
+    if (lt0 >= lt1) continue;
+    for (int p = 0; p < a; ++p) {
+      const char* base = reinterpret_cast<const char*>(
+          Ly.L.planes + p * Ly.L.plane_stride16 +
+          ((long long)w * Ly.L.n_tiles + (lt0 - Ly.tile_off)) * (kTileBytes / 16));
+      long long bytes = (long long)(lt1 - lt0) * kTileBytes;
+      while (bytes > 0) {
+        const unsigned chunk = (unsigned)min(bytes, (long long)65536);
+        prefetch_l2_bulk(base, chunk);
+        base += chunk;
+        bytes -= chunk;
+      }
+    }
+  }
+}
+
+constexpr int kGShares = 2;      // CTAs per window computing estimator partials
+constexpr int kChunk = 2;        // tiles a warp grabs at a time
+
+// Estimator input of an op (runtime.py:300-309): explicit est_in, the
+// previous-step / previous-block snapshot, or nullptr (= the op input).
+__device__ __forceinline__ const float* est_input(const OpDesc& D, const Control* ctl, int mode, double& scale) {
+  scale = 1.0;
+  if (D.est_in) return D.est_in;
+  if (mode != MODE_DYNAMIC) return nullptr;
+  int need = 0;
+  for (int li = 0; li < D.n_layers; ++li) {
+    const DevSel& S = D.layer[li].S;
+    if (S.prev_residual && S.sentinel == 0 && (S.est_kind == EST_LINEAR || S.est_kind == EST_PROJECTION)) need = 1;
+  }
+  if (!need) return nullptr;
+  int slot = -1, idx = -1;
+  if (ctl->async_prev_block) { slot = ctl->snap_w; idx = D.layer[0].snap_in; }
+  else if (ctl->has_prev) { slot = ctl->snap_r; idx = D.snap_idx; }
+  if (slot < 0 || idx < 0) return nullptr;
+  const size_t loc = (size_t)slot * D.n_snap + idx;
+  if (D.in_mode == IN_RMS) scale = (double)D.snap_stats[loc * 4 + 2];
+  return D.snap + loc * D.snap_stride;
+}
+
+// G tile CTAs + the decider finish an op; the last resets the op's counters
+// and accumulators for its next execution (nobody can still be using them).
+__device__ __forceinline__ void op_done(const OpDesc& D, int G) {
+  __threadfence();
+  if (atomicAdd(D.ctr + 1, 1u) == (unsigned)G) {
+    for (int i = 0; i < 3 + D.n_win; ++i) D.ctr[i] = 0u;
+    for (int i = 0; i < kMaxOpLayers * kMaxK; ++i) D.gxa[i] = 0;
+    __threadfence();
+  }
+}
+
+__device__ __forceinline__ int estimator_shares(int G, int n_win) {
+  int total = 0;
+  for (int ww = 0; ww < n_win; ++ww) total += min(kGShares, (G - ww + n_win - 1) / n_win);
+  return total;
+}
+
+// Decider of an op, run by warp 0 of the dedicated decider CTA (it owns no
+// tiles, so its latency never delays a tile): waits for the estimator shares,
+// then op input statistics, estimates, decisions (runtime.py:184-193), trace,
+// and the decision-ready release. All loads are issued before any use.
+__device__ void decide_warp(const OpDesc& D, const Control* __restrict__ ctl, int G) {
+  const int lane = threadIdx.x & 31;
   const int n_win = D.n_win;
   const int mode = ctl->mode;
-
-  // ---- CTA -> (window, tile range) --------------------------------------
-  // CTAs c = w, w + n_win, w + 2 n_win, ... share window w.
-  const int w = blockIdx.x % n_win;
-  const int j = blockIdx.x / n_win;
-  const int m = (G - w + n_win - 1) / n_win;
-  const int t_begin = (int)((long long)D.total_tiles * j / m);
-  const int t_end = (int)((long long)D.total_tiles * (j + 1) / m);
-
-  // ---- L2 prefetch of the always-streamed planes (independent of inputs) --
-  if (tid == 0) {
-    for (int li = 0; li < D.n_layers; ++li) {
+  const unsigned total = (unsigned)estimator_shares(G, n_win);
+  if (lane == 0) DPQ_SPIN_UNTIL(ld_acquire(D.ctr) >= total, "decider shares", (int)total, D.n_win, ld_acquire(D.ctr));
+  __syncwarp();
+  double xp_scale;
+  const float* xp_src = est_input(D, ctl, mode, xp_scale);
+  // loads: window stats (2 windows per lane) and projection accumulators
+  double a1[2], a2[2], a3[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int i = lane + 32 * u;
+    const bool ok = i < n_win;
+    a1[u] = ok ? __ldcg(D.win_stats + 4 * i) : 0.0;
+    a2[u] = ok ? __ldcg(D.win_stats + 4 * i + 1) : 0.0;
+    a3[u] = ok ? __ldcg(D.win_stats + 4 * i + 2) : 0.0;
+  }
+  long long gv[kMaxOpLayers][kMaxK / 32];
+#pragma unroll
+  for (int li = 0; li < kMaxOpLayers; ++li)
+#pragma unroll
+    for (int u = 0; u < kMaxK / 32; ++u) {
+      const int i = lane + 32 * u;
+      const bool ok = mode == MODE_DYNAMIC && li < D.n_layers && D.layer[li].S.sentinel == 0 &&
+                      D.layer[li].S.est_kind == EST_PROJECTION && i < D.layer[li].S.k;
+      gv[li][u] = ok ? __ldcg(D.gxa + li * kMaxK + i) : 0;
+    }
+  const double t1 = warp_sum(a1[0] + a1[1]);
+  const double t2 = warp_sum(a2[0] + a2[1]);
+  const double t3 = warp_sum(a3[0] + a3[1]);
+  const double inv = 1.0 / sqrt(t2 / (double)D.cols + (double)D.eps);
+  const int force = ctl->force, trace_step = ctl->trace_step;
+  if (lane == 0) {
+    D.op_stats[0] = (float)t1;
+    D.op_stats[1] = (float)t2;
+    D.op_stats[2] = (float)inv;
+    if (D.need_snap) {
+      float* st = D.snap_stats + ((size_t)ctl->snap_w * D.n_snap + D.snap_idx) * 4;
+      st[0] = (float)t1; st[1] = (float)t2; st[2] = (float)inv; st[3] = 0.f;
+    }
+  }
+  if (mode == MODE_DYNAMIC) {
+#pragma unroll
+    for (int li = 0; li < kMaxOpLayers; ++li) {
+      if (li >= D.n_layers) break;
       const OpLayer& Ly = D.layer[li];
-      int a, b, pend;
-      layer_planes(Ly, mode, ctl, a, b, pend);
-      if (a <= 0) continue;
-      const int lt0 = max(t_begin, Ly.tile_off), lt1 = min(t_end, Ly.tile_off + Ly.L.n_tiles);
-      if (lt0 >= lt1) continue;
-      for (int p = 0; p < a; ++p) {
-        const char* base = reinterpret_cast<const char*>(
-            Ly.L.planes + p * Ly.L.plane_stride16 +
-            ((long long)w * Ly.L.n_tiles + (lt0 - Ly.tile_off)) * (kTileBytes / 16));
-        long long bytes = (long long)(lt1 - lt0) * kTileBytes;
-        while (bytes > 0) {
-          const unsigned chunk = (unsigned)min(bytes, (long long)65536);
-          prefetch_l2_bulk(base, chunk);
-          base += chunk;
-          bytes -= chunk;
+      const DevSel& S = Ly.S;
+      double est = CUDART_NAN;
+      bool have_est = false;
+      const bool prev = xp_src && (S.prev_residual || D.est_in);
+      const double in_scale = prev ? xp_scale : (D.in_mode == IN_RMS ? inv : 1.0);
+      if (S.sentinel == 0 && S.est_kind == EST_PROJECTION) {
+        double q = 0.0;
+#pragma unroll
+        for (int u = 0; u < kMaxK / 32; ++u) {
+          const int i = lane + 32 * u;
+          double g = (double)gv[li][u] * 0x1p-40;
+          if (S.g_scale && i < S.k) g *= (double)S.g_scale[i];
+          q += g * g;
+        }
+        q = warp_sum(q);
+        est = in_scale * sqrt(q);
+        have_est = true;
+      } else if (S.sentinel == 0 && S.est_kind == EST_LINEAR) {
+        const double sq = prev ? t3 : t2;
+        est = S.slope * (in_scale * sqrt(sq)) + S.intercept;
+        have_est = true;
+      }
+      if (lane == 0) {
+        int bit;
+        if (S.sentinel == 3 || (Ly.dual && S.est_kind == EST_EXACT && S.sentinel == 0))
+          bit = -1;                                   // finalize / prior kernel decides
+        else if (force && Ly.trace_idx >= 0) bit = ctl->forced_bits[Ly.trace_idx];
+        else if (S.sentinel == 1) bit = S.l;
+        else if (S.sentinel == 2) bit = S.h;
+        else if (have_est) bit = (est > S.T) ? S.h : S.l;
+        else bit = S.l;
+        if (bit >= 0) D.decision[li] = bit;
+        if (Ly.trace_idx >= 0 && D.n_trace > 0) {
+          const size_t o = (size_t)trace_step * D.n_trace + Ly.trace_idx;
+          if (bit >= 0) D.tr_bits[o] = (signed char)bit;
+          if (S.sentinel != 3) D.tr_est[o] = have_est ? (float)est : CUDART_NAN_F;
         }
       }
     }
   }
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    st_release(D.ctr + 2, 1u);                // decision ready (reset when the op completes)
+    op_done(D, G);
+  }
+}
+
+__device__ __forceinline__ void op_stage(const OpDesc& D, const Control* __restrict__ ctl, const StageCtx& X,
+                                         unsigned char* smem_raw) {
+  // Shared layout: [sbase, 0x10000): OpSmem + per-warp S / S_l; [0x10000, +kLutBytes): LUT.
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  float* lut = reinterpret_cast<float*>(smem_raw + (kLutShared - sbase));
+  OpSmem& sm = *reinterpret_cast<OpSmem*>(smem_raw);
+  if (kOpSmemBytes + 2 * kThreads * kWarpTiles * 4 > kLutShared - sbase) __trap();
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kW = kThreads / 32;
+  const int G = X.G;
+  const int n_win = D.n_win;
+  const int mode = ctl->mode;
+  // static window assignment: CTAs w, w + n_win, ... share window w
+  int w, j, m, t_begin, t_end;
+  cta_window(D, X.cta, G, w, j, m, t_begin, t_end);
+  // op counters: [0] estimator shares done, [1] CTAs done, [2] decision ready, [3 + w] window arrivals
+  unsigned* warr = D.ctr + 3;
+
+  // ---- L2 prefetch of our static share of the planes, and of the next op --
+  if (tid == 0) {
+    prefetch_op(D, ctl, X.cta, G);
+    if (X.next) prefetch_op(*X.next, ctl, X.cta, X.G);
+  }
   DPQ_STAMP(0);
   pdl_wait();
+  unsigned my_rank = 0;
+  if (tid == 0) my_rank = atomicAdd(warr + w, 1u);   // arrival rank in the window (used below)
+  if (warp == 0 && X.dep0) {
+    const int c0 = w * kWinCols, c1 = min(D.cols, c0 + kWinCols);
+    wait_flags_warp(X.dep0, X.dep0_off + c0 / X.dep0_rpf, X.dep0_off + (c1 + X.dep0_rpf - 1) / X.dep0_rpf,
+                    X.epoch);
+    if (X.dep1)
+      wait_flags_warp(X.dep1, X.dep1_off + c0 / X.dep0_rpf, X.dep1_off + (c1 + X.dep0_rpf - 1) / X.dep0_rpf,
+                      X.epoch);
+  }
   DPQ_STAMP(1);
-  if (tid == 0) sm.my_gen = *reinterpret_cast<volatile unsigned*>(&D.sync->gen);
 
-  // ---- prologue: input window, estimator-input window, window stats --------
-  const int col0 = w * kWinCols;
+  // ---- estimator-input source ----------------------------------------------
   if (tid == 0) {
-    // estimator input for previous-residual estimators (runtime.py:300-309)
-    const float* src = nullptr;
-    double scale = 1.0;
-    if (D.est_in) {
-      src = D.est_in;
-    } else if (mode == MODE_DYNAMIC) {
-      int need = 0;
-      for (int li = 0; li < D.n_layers; ++li) {
-        const DevSel& S = D.layer[li].S;
-        if (S.prev_residual && S.sentinel == 0 && (S.est_kind == EST_LINEAR || S.est_kind == EST_PROJECTION))
-          need = 1;
-      }
-      int slot = -1, idx = -1;
-      if (need) {
-        if (ctl->async_prev_block) { slot = ctl->snap_w; idx = D.layer[0].snap_in; }
-        else if (ctl->has_prev) { slot = ctl->snap_r; idx = D.snap_idx; }
-      }
-      if (slot >= 0 && idx >= 0) {
-        const size_t loc = (size_t)slot * D.n_snap + idx;
-        src = D.snap + loc * D.snap_stride;
-        if (D.in_mode == IN_RMS) scale = (double)D.snap_stats[loc * 4 + 2];
-      }
-    }
-    sm.xp_src = src;
+    sm.rank = (int)my_rank;
+    double scale;
+    sm.xp_src = est_input(D, ctl, mode, scale);
     sm.xp_scale = scale;
   }
   __syncthreads();
+
+  // ---- prologue: input window (+ estimator-input window), stats, LUT -------
+  const int col0 = w * kWinCols;
   double s1 = 0.0, s2 = 0.0, s3 = 0.0;
   {
     const int c = col0 + tid;
     float v = 0.f, vp = 0.f;
     if (c < D.cols) {
       if (D.in_mode == IN_SILU) {
-        const float up = D.in0[c], gt = D.in1[c];
+        const float up = __ldcg(D.in0 + c), gt = __ldcg(D.in1 + c);
         v = up * (gt / (1.0f + expf(-gt)));
       } else {
-        v = D.in0[c];
+        v = __ldcg(D.in0 + c);
       }
-      if (sm.xp_src) vp = sm.xp_src[c];
+      if (sm.xp_src) vp = __ldcg(sm.xp_src + c);
     }
     sm.xw[tid] = v;
     sm.xp[tid] = vp;
     s1 = v;
     s2 = (double)v * (double)v;
     s3 = (double)vp * (double)vp;
-    if (D.need_snap && j == 0 && c < D.cols)
+    if (D.need_snap && sm.rank == 0 && c < D.cols)
       D.snap[((size_t)ctl->snap_w * D.n_snap + D.snap_idx) * D.snap_stride + c] = v;
   }
   __syncthreads();
@@ -342,18 +531,27 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
     double* ws = D.win_stats + 4 * w;
     ws[0] = s1; ws[1] = s2; ws[2] = s3; ws[3] = 0.0;
   }
+  if (tid < D.n_layers) {
+    int a, b, pend;
+    layer_planes(D.layer[tid], mode, ctl, a, b, pend);
+    sm.la[tid] = (pend == 2) ? 0 : a;        // planes streamed before any decision
+    sm.lb[tid] = pend ? -1 : b;              // final plane count, -1 = pending
+  }
+  __syncthreads();
   DPQ_STAMP(2);
 
-  // ---- P1: projection-estimator partial dot products (window slice) ------
-  if (mode == MODE_DYNAMIC) {
-    int ng_total = 0;
-    for (int li = 0; li < D.n_layers; ++li) {
-      const DevSel& S = D.layer[li].S;
-      if (S.est_kind == EST_PROJECTION && S.sentinel == 0) ng_total += S.k;
-    }
-    if (ng_total > 0) {
-      const int r0 = (int)((long long)ng_total * j / m), r1 = (int)((long long)ng_total * (j + 1) / m);
-      for (int r = r0 + warp; r < r1; r += kThreads / 32) {
+  // ---- estimator share: the first min(kGShares, m) CTAs of each window -----
+  const int rank = sm.rank;
+  const int n_sh = min(kGShares, m);
+  if (rank < n_sh) {
+    if (mode == MODE_DYNAMIC) {
+      int ng_total = 0;
+      for (int li = 0; li < D.n_layers; ++li) {
+        const DevSel& S = D.layer[li].S;
+        if (S.est_kind == EST_PROJECTION && S.sentinel == 0) ng_total += S.k;
+      }
+      const int r0 = ng_total * rank / n_sh, r1 = ng_total * (rank + 1) / n_sh;
+      for (int r = r0 + warp; r < r1; r += kW) {
         int li = 0, i = r;
         while (true) {
           const DevSel& S = D.layer[li].S;
@@ -366,122 +564,26 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
         const bool use_p = sm.xp_src && (S.prev_residual || D.est_in);
         const char* grow = reinterpret_cast<const char*>(S.G) + ((long long)w * S.k + i) * g_row_bytes(S.g_dtype);
         const float acc = g_dot(grow, S.g_dtype, use_p ? sm.xp : sm.xw, lane);
-        if (lane == 0) D.gx_part[((size_t)li * n_win + w) * kMaxK + i] = acc;
+        if (lane == 0)
+          atomicAdd(reinterpret_cast<unsigned long long*>(D.gxa + li * kMaxK + i),
+                    (unsigned long long)llrint((double)acc * 0x1p40));
       }
     }
-  }
-
-  // ---- op barrier arrive; the last CTA decides -----------------------------
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const unsigned old = atomicAdd(&D.sync->arrive, 1u);
-    sm.is_last = (old == (unsigned)G - 1);
-  }
-  __syncthreads();
-  DPQ_STAMP(3);
-  if (sm.is_last) {
-    __threadfence();
-    // op input statistics
-    double t1 = 0.0, t2 = 0.0, t3 = 0.0;
-    for (int i = tid; i < n_win; i += kThreads) {
-      t1 += __ldcg(D.win_stats + 4 * i);
-      t2 += __ldcg(D.win_stats + 4 * i + 1);
-      t3 += __ldcg(D.win_stats + 4 * i + 2);
-    }
-    block_sum3(t1, t2, t3, sm.red);
-    const double inv = 1.0 / sqrt(t2 / (double)D.cols + (double)D.eps);
-    if (tid == 0) {
-      D.op_stats[0] = (float)t1;
-      D.op_stats[1] = (float)t2;
-      D.op_stats[2] = (float)inv;
-      if (D.need_snap) {
-        float* st = D.snap_stats + ((size_t)ctl->snap_w * D.n_snap + D.snap_idx) * 4;
-        st[0] = (float)t1; st[1] = (float)t2; st[2] = (float)inv; st[3] = 0.f;
-      }
-    }
-    // projection norms: thread (li, i) sums its window partials; 4 warps per layer
-    if (mode == MODE_DYNAMIC) {
-      const int li = tid / kMaxK, i = tid % kMaxK;
-      double q = 0.0;
-      if (li < D.n_layers) {
-        const DevSel& S = D.layer[li].S;
-        if (S.sentinel == 0 && S.est_kind == EST_PROJECTION && i < S.k) {
-          const float* gp = D.gx_part + (size_t)li * n_win * kMaxK + i;
-          float g0 = 0.f, g1 = 0.f;
-          int ww = 0;
-          for (; ww + 1 < n_win; ww += 2) { g0 += __ldcg(gp + (size_t)ww * kMaxK); g1 += __ldcg(gp + (size_t)(ww + 1) * kMaxK); }
-          if (ww < n_win) g0 += __ldcg(gp + (size_t)ww * kMaxK);
-          float g = g0 + g1;
-          if (S.g_scale) g *= S.g_scale[i];
-          q = (double)g * (double)g;
-        }
-      }
-      q = warp_sum(q);
-      if (lane == 0 && warp < kMaxOpLayers * 4) sm.lay_q[warp] = q;
-      __syncthreads();
-    }
-    for (int li = 0; li < D.n_layers; ++li) {
-      const OpLayer& Ly = D.layer[li];
-      const DevSel& S = Ly.S;
-      if (mode != MODE_DYNAMIC) continue;
-      double est = CUDART_NAN;
-      bool have_est = false;
-      const bool prev = sm.xp_src && (S.prev_residual || D.est_in);
-      const double in_scale = prev ? sm.xp_scale : (D.in_mode == IN_RMS ? inv : 1.0);
-      if (S.sentinel == 0 && S.est_kind == EST_PROJECTION) {
-        const double q = sm.lay_q[4 * li] + sm.lay_q[4 * li + 1] + sm.lay_q[4 * li + 2] + sm.lay_q[4 * li + 3];
-        est = in_scale * sqrt(q);
-        have_est = true;
-      } else if (S.sentinel == 0 && S.est_kind == EST_LINEAR) {
-        const double sq = prev ? t3 : t2;
-        est = S.slope * (in_scale * sqrt(sq)) + S.intercept;
-        have_est = true;
-      }
-      if (tid == 0) {
-        int bit;
-        if (S.sentinel == 3 || (Ly.dual && S.est_kind == EST_EXACT && S.sentinel == 0))
-          bit = -1;                                         // finalize / prior kernel decides
-        else if (ctl->force && Ly.trace_idx >= 0) bit = ctl->forced_bits[Ly.trace_idx];
-        else if (S.sentinel == 1) bit = S.l;
-        else if (S.sentinel == 2) bit = S.h;
-        else if (have_est) bit = (est > S.T) ? S.h : S.l;
-        else bit = S.l;
-        if (bit >= 0) D.decision[li] = bit;
-        if (Ly.trace_idx >= 0 && D.n_trace > 0) {
-          const size_t o = (size_t)ctl->trace_step * D.n_trace + Ly.trace_idx;
-          if (bit >= 0) D.tr_bits[o] = (signed char)bit;
-          if (S.sentinel != 3) D.tr_est[o] = have_est ? (float)est : CUDART_NAN_F;
-        }
-      }
-    }
+    __threadfence();                          // every issuing thread orders its accumulations
     __syncthreads();
     if (tid == 0) {
-      D.sync->arrive = 0u;
       __threadfence();
-      st_release(&D.sync->gen, sm.my_gen + 1u);
+      atomicAdd(D.ctr, 1u);                   // estimator share done (the decider CTA waits for all)
     }
   }
-
+  DPQ_STAMP(3);
   DPQ_STAMP(4);
-  // ---- per-layer plane counts known to this CTA ----------------------------
-  if (tid < D.n_layers) {
-    int a, b, pend;
-    layer_planes(D.layer[tid], mode, ctl, a, b, pend);
-    sm.la[tid] = (pend == 2) ? 0 : a;        // planes streamed before any decision
-    sm.lb[tid] = pend ? -1 : b;              // final plane count, -1 = pending
-  }
-  __syncthreads();
-  // Let the next kernel's CTAs start (their L2 prefetch overlaps our stream).
-  pdl_launch();
+  if (!X.out_flags) pdl_launch();
 
-  // ---- warp-owned tiles: tiles t_begin + warp + kW*i, all planes per warp --
-  constexpr int kW = kThreads / 32;
+  // ---- dynamic tiles: warps grab kChunk tiles of this window at a time -----
   const uint32_t lanereg = kLutShared | ((uint32_t)lane * 4u);
   float* Ssm = reinterpret_cast<float*>(smem_raw + kOpSmemBytes) + warp * (kWarpTiles * 32);
   float* Slsm = reinterpret_cast<float*>(smem_raw + kOpSmemBytes) + (kW + warp) * (kWarpTiles * 32);
-  const int n_ct = t_end - t_begin;
-  const int n_my = n_ct > warp ? (n_ct - warp + kW - 1) / kW : 0;
   int fb0 = sm.lb[0], fb1 = D.n_layers > 1 ? sm.lb[1] : 0, fb2 = D.n_layers > 2 ? sm.lb[2] : 0;
   bool decided = (fb0 >= 0) && (fb1 >= 0) && (fb2 >= 0);
   auto final_bits = [&](int li) { return li == 0 ? fb0 : (li == 1 ? fb1 : fb2); };
@@ -490,121 +592,120 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
     while (li + 1 < D.n_layers && t >= D.layer[li + 1].tile_off) ++li;
     return li;
   };
+  // lane-distributed description of one (chunk, phase) task list over this
+  // warp's owned tiles t_begin + warp + kW*(c0 + i), i < nc
+  int my_t = -1, my_li = 0, p0 = 0, start = 0x7fffffff, total = 0;
+  const int n_ct = t_end - t_begin;
+  const int n_my = n_ct > warp ? (n_ct - warp + kW - 1) / kW : 0;
+  auto describe = [&](int c0, int phase) {
+    const int nc = max(0, min(kWarpTiles, n_my - c0));
+    my_t = lane < nc ? t_begin + warp + kW * (c0 + lane) : -1;
+    my_li = lane < nc ? layer_of(my_t) : 0;
+    int q0 = 0, q1 = 0;
+    if (lane < nc) {
+      const int la = sm.la[my_li];
+      if (phase == 0) { q0 = 0; q1 = la; }
+      else { q0 = la; q1 = sm.lb[my_li] < 0 ? final_bits(my_li) : la; }
+    }
+    p0 = q0;
+    const int cnt = q1 > q0 ? q1 - q0 : 0;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    start = lane < nc ? incl - cnt : 0x7fffffff;
+    total = __shfl_sync(0xffffffffu, incl, 31);
+  };
+  auto task_src = [&](int k, int& ti, int& pl) -> const uint4* {
+    ti = __popc(__ballot_sync(0xffffffffu, start <= k)) - 1;
+    const int t = __shfl_sync(0xffffffffu, my_t, ti);
+    const int li = __shfl_sync(0xffffffffu, my_li, ti);
+    pl = __shfl_sync(0xffffffffu, p0, ti) + (k - __shfl_sync(0xffffffffu, start, ti));
+    const DevLayer& L = D.layer[li].L;
+    return L.planes + pl * L.plane_stride16 +
+           ((long long)w * L.n_tiles + (t - D.layer[li].tile_off)) * (kTileBytes / 16) + lane;
+  };
+  uint4 qa0, qa1, qa2, qa3, qb0, qb1, qb2, qb3, qc0, qc1, qc2, qc3;
+  int ta = 0, tb = 0, tc = 0, pa = 0, pb = 0, pc = 0;
+#define DPQ_LOAD(X_, T, PL, k)                                                        \
+  {                                                                                   \
+    const uint4* s_ = task_src(k, T, PL);                                             \
+    X_##0 = ldg_stream(s_); X_##1 = ldg_stream(s_ + 32);                              \
+    X_##2 = ldg_stream(s_ + 64); X_##3 = ldg_stream(s_ + 96);                         \
+  }
+  auto prime = [&]() {
+    if (0 < total) DPQ_LOAD(qa, ta, pa, 0);
+    if (1 < total) DPQ_LOAD(qb, tb, pb, 1);
+    if (2 < total) DPQ_LOAD(qc, tc, pc, 2);
+  };
+  // 3-deep register pipeline over the described tasks (tile-major, plane
+  // ascending) with Horner accumulation S = 2 S + P_p per tile.
+  auto run = [&](int phase) {
+    float S = 0.f;
+    int cur = -1;
+#define DPQ_RUN(X_, T, PL, k)                                                         \
+  {                                                                                   \
+    const float P_ = plane_task(X_##0, X_##1, X_##2, X_##3, lanereg);                 \
+    if ((T) != cur) {                                                                 \
+      if (cur >= 0) Ssm[cur * 32 + lane] = S;                                         \
+      cur = (T);                                                                      \
+      S = (phase == 1) ? Ssm[cur * 32 + lane] : 0.f;                                  \
+    }                                                                                 \
+    S = 2.f * S + P_;                                                                 \
+    {                                                                                 \
+      const OpLayer& Ly_ = D.layer[__shfl_sync(0xffffffffu, my_li, T)];              \
+      if (Ly_.dual && mode == MODE_DYNAMIC && (PL) == Ly_.S.l - 1) Slsm[(T) * 32 + lane] = S; \
+    }                                                                                 \
+    if ((k) + 3 < total) DPQ_LOAD(X_, T, PL, (k) + 3);                                \
+  }
+    for (int k = 0; k < total; k += 3) {
+      DPQ_RUN(qa, ta, pa, k);
+      if (k + 1 >= total) break;
+      DPQ_RUN(qb, tb, pb, k + 1);
+      if (k + 2 >= total) break;
+      DPQ_RUN(qc, tc, pc, k + 2);
+    }
+#undef DPQ_RUN
+    if (cur >= 0) Ssm[cur * 32 + lane] = S;
+    __syncwarp();
+  };
 
   for (int c0 = 0; c0 < n_my; c0 += kWarpTiles) {
     const int nc = min(kWarpTiles, n_my - c0);
-    // lane i < nc describes owned tile i of this chunk
-    const int my_t = lane < nc ? t_begin + warp + kW * (c0 + lane) : -1;
-    const int my_li = lane < nc ? layer_of(my_t) : 0;
+    const int c_t = lane < nc ? t_begin + warp + kW * (c0 + lane) : -1;
+    const int c_li = lane < nc ? layer_of(c_t) : 0;
     for (int i = 0; i < nc; ++i) Ssm[i * 32 + lane] = 0.f;
     __syncwarp();
-
-    for (int phase = 0; phase < 2; ++phase) {
-      if (phase == 1) {
-        // decisions of pending layers (one spin per warp, lane 0)
-        if (!decided) {
-          bool need = false;
-          for (int i = 0; i < nc; ++i) {
-            const int li = __shfl_sync(0xffffffffu, my_li, i);
-            if (final_bits(li) < 0) need = true;
-          }
-          if (!need) break;
-          DPQ_STAMP(5);
-          if (lane == 0) {
-            while (ld_acquire(&D.sync->gen) == sm.my_gen) __nanosleep(32);
-          }
-          __syncwarp();
-          if (fb0 < 0) fb0 = __ldcg(D.decision + 0);
-          if (fb1 < 0) fb1 = __ldcg(D.decision + 1);
-          if (fb2 < 0) fb2 = __ldcg(D.decision + 2);
-          decided = true;
-          DPQ_STAMP(6);
-        }
+    describe(c0, 0);
+    prime();
+    run(0);
+    // planes gated by a pending decision
+    bool need = false;
+    for (int i = 0; i < nc; ++i)
+      if (sm.lb[__shfl_sync(0xffffffffu, c_li, i)] < 0) need = true;
+    if (need) {
+      if (!decided) {
+        DPQ_STAMP(5);
+        if (lane == 0) DPQ_SPIN_UNTIL(ld_acquire(D.ctr + 2) != 0u, "decision", D.n_layers, D.n_win, 0u);
+        __syncwarp();
+        if (fb0 < 0) fb0 = __ldcg(D.decision + 0);
+        if (fb1 < 0) fb1 = __ldcg(D.decision + 1);
+        if (fb2 < 0) fb2 = __ldcg(D.decision + 2);
+        decided = true;
+        DPQ_STAMP(6);
       }
-      // per-tile plane range of this phase
-      int p0 = 0, p1 = 0;
-      if (lane < nc) {
-        const int la = sm.la[my_li];
-        if (phase == 0) { p0 = 0; p1 = la; }
-        else {
-          const int fb = final_bits(my_li);
-          const bool was_pending = sm.lb[my_li] < 0;
-          p0 = la;
-          p1 = was_pending ? fb : la;
-        }
-      }
-      // exclusive prefix of task counts across the owned tiles
-      const int cnt = p1 > p0 ? p1 - p0 : 0;
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int start = lane < nc ? incl - cnt : 0x7fffffff;
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      if (total == 0) continue;
-      auto task_tile = [&](int k) { return __popc(__ballot_sync(0xffffffffu, start <= k)) - 1; };
-      auto task_src = [&](int k, int& ti, int& pl) -> const uint4* {
-        ti = task_tile(k);
-        const int t = __shfl_sync(0xffffffffu, my_t, ti);
-        const int li = __shfl_sync(0xffffffffu, my_li, ti);
-        pl = __shfl_sync(0xffffffffu, p0, ti) + (k - __shfl_sync(0xffffffffu, start, ti));
-        const DevLayer& L = D.layer[li].L;
-        return L.planes + pl * L.plane_stride16 +
-               ((long long)w * L.n_tiles + (t - D.layer[li].tile_off)) * (kTileBytes / 16) + lane;
-      };
-      // 3-deep register pipeline over this warp's tasks (tile-major, plane
-      // ascending) with Horner accumulation S = 2 S + P_p per owned tile.
-      uint4 qa0, qa1, qa2, qa3, qb0, qb1, qb2, qb3, qc0, qc1, qc2, qc3;
-      int ta = 0, tb = 0, tc = 0, pa = 0, pb = 0, pc = 0;
-      float S = 0.f;
-      int cur = -1;
-      auto flush_to = [&](int ti) {
-        if (cur >= 0) Ssm[cur * 32 + lane] = S;
-        cur = ti;
-        S = (phase == 1) ? Ssm[ti * 32 + lane] : 0.f;
-      };
-#define DPQ_LOAD(X, T, PL, k)                                                         \
-  {                                                                                   \
-    const uint4* s_ = task_src(k, T, PL);                                             \
-    X##0 = ldg_stream(s_); X##1 = ldg_stream(s_ + 32);                                \
-    X##2 = ldg_stream(s_ + 64); X##3 = ldg_stream(s_ + 96);                           \
-  }
-#define DPQ_RUN(X, T, PL, k)                                                          \
-  {                                                                                   \
-    const float P_ = plane_task(X##0, X##1, X##2, X##3, lanereg);                     \
-    if ((T) != cur) flush_to(T);                                                      \
-    S = 2.f * S + P_;                                                                 \
-    {                                                                                 \
-      const int lsel_ = D.layer[__shfl_sync(0xffffffffu, my_li, T)].S.l;              \
-      const bool dual_ = D.layer[__shfl_sync(0xffffffffu, my_li, T)].dual && mode == MODE_DYNAMIC; \
-      if (dual_ && (PL) == lsel_ - 1) Slsm[(T) * 32 + lane] = S;                      \
-    }                                                                                 \
-    if ((k) + 3 < total) DPQ_LOAD(X, T, PL, (k) + 3);                                 \
-  }
-      DPQ_LOAD(qa, ta, pa, 0);
-      if (1 < total) DPQ_LOAD(qb, tb, pb, 1);
-      if (2 < total) DPQ_LOAD(qc, tc, pc, 2);
-      for (int k = 0; k < total; k += 3) {
-        DPQ_RUN(qa, ta, pa, k);
-        if (k + 1 >= total) break;
-        DPQ_RUN(qb, tb, pb, k + 1);
-        if (k + 2 >= total) break;
-        DPQ_RUN(qc, tc, pc, k + 2);
-      }
-#undef DPQ_RUN
-#undef DPQ_LOAD
-      if (cur >= 0) Ssm[cur * 32 + lane] = S;
-      __syncwarp();
+      describe(c0, 1);
+      prime();
+      run(1);
     }
 
-    // ---- publish partial sums of the owned tiles; per-tile last arriver ----
-    // reduces over windows and applies the affine epilogue.
-    int bsel_i = lane < nc ? final_bits(my_li) : 0;
+    // ---- publish partial sums; per-tile last arriver reduces over windows --
+    const int bsel_i = lane < nc ? final_bits(c_li) : 0;
     for (int i = 0; i < nc; ++i) {
-      const int t = __shfl_sync(0xffffffffu, my_t, i);
-      const int li = __shfl_sync(0xffffffffu, my_li, i);
+      const int t = __shfl_sync(0xffffffffu, c_t, i);
+      const int li = __shfl_sync(0xffffffffu, c_li, i);
       const bool dual = D.layer[li].dual && mode == MODE_DYNAMIC;
       const int row_g = t * 32 + lane;
       D.part[(size_t)w * D.rows_total_pad + row_g] = Ssm[i * 32 + lane];
@@ -613,11 +714,11 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
     __threadfence();
     __syncwarp();
     unsigned old = 0;
-    if (lane < nc) old = atomicAdd(D.tile_cnt + my_t, 1u);
+    if (lane < nc) old = atomicAdd(D.tile_cnt + c_t, 1u);
     const unsigned lastmask = __ballot_sync(0xffffffffu, lane < nc && old == (unsigned)n_win - 1);
     if (lastmask) {
       __threadfence();
-      if (lane < nc && ((lastmask >> lane) & 1u)) D.tile_cnt[my_t] = 0u;
+      if (lane < nc && ((lastmask >> lane) & 1u)) D.tile_cnt[c_t] = 0u;
       double sx = 0.0, sq = 0.0;
       for (int ii = lane; ii < n_win; ii += 32) {
         sx += __ldcg(D.win_stats + 4 * ii);
@@ -629,8 +730,8 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
       const float sxf = (float)sx;
       for (unsigned mk = lastmask; mk; mk &= mk - 1) {
         const int i = __ffs(mk) - 1;
-        const int t = __shfl_sync(0xffffffffu, my_t, i);
-        const int li = __shfl_sync(0xffffffffu, my_li, i);
+        const int t = __shfl_sync(0xffffffffu, c_t, i);
+        const int li = __shfl_sync(0xffffffffu, c_li, i);
         const int bsel = __shfl_sync(0xffffffffu, bsel_i, i);
         const OpLayer& Ly = D.layer[li];
         const bool dual = Ly.dual && mode == MODE_DYNAMIC;
@@ -651,7 +752,7 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
           const int out_row = Ly.out_off + r;
           if (!dual) {
             const float y = scale * (lo * sxf + ldexpf(span, -bsel) * (St + 0.5f * sxf));
-            if (D.out_mode == OUT_ADD) D.out[out_row] += y;
+            if (D.out_mode == OUT_ADD) D.out[out_row] = __ldcg(D.out + out_row) + y;
             else D.out[out_row] = y;
           } else {
             const float yh = scale * (lo * sxf + ldexpf(span, -Ly.S.h) * (St + 0.5f * sxf));
@@ -666,10 +767,37 @@ op_kernel(const OpDesc D, Control* __restrict__ ctl) {
           const double q = warp_sum(0.0);
           if (lane == 0) D.dual_sq[t] = (float)q;
         }
+        if (X.out_flags) {
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) st_release(X.out_flags + t, X.epoch);
+        }
       }
     }
   }
+#undef DPQ_LOAD
+  // ---- op done: the last CTA resets the op's counters for the next use -----
+  __syncthreads();
+  if (tid == 0) op_done(D, G);
   DPQ_STAMP(7);
+}
+
+extern "C" __global__ void __launch_bounds__(kThreads, 1)
+op_kernel(const OpDesc D, Control* __restrict__ ctl) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ Control cs;          // the control block, read once
+  pdl_wait();
+  if (threadIdx.x == 0) cs = *ctl;
+  __syncthreads();
+  // the last CTA is the op's decider; the others own the tiles
+  if (blockIdx.x == gridDim.x - 1) {
+    if (threadIdx.x < 32) decide_warp(D, &cs, gridDim.x - 1);
+    return;
+  }
+  StageCtx X{};
+  X.cta = blockIdx.x;
+  X.G = gridDim.x - 1;
+  op_stage(D, &cs, X, smem_raw);
 }
 
 // ---------------------------------------------------------------------------
@@ -761,33 +889,29 @@ struct AttnDesc {
   unsigned* cnt;         // [H]
   float* out;            // [d]
   int H, KV, hd, d, dkv, n_chunks;
+  const unsigned* qkv_flags;   // persistent: per 32-row tile of the qkv op output
+  unsigned* head_flags;        // persistent: per head, set when attn[h] is final
 };
 
 constexpr int kAttnChunk = 64;
 
 __device__ __forceinline__ float rope_elem(const float* v, int i, int hd, const float* c, const float* s) {
   const int half = hd / 2;
-  if (i < half) return v[i] * c[i] - v[i + half] * s[i];
-  if (i < 2 * half) return v[i - half] * s[i - half] + v[i] * c[i - half];
-  return v[i];
+  if (i < half) return __ldcg(v + i) * c[i] - __ldcg(v + i + half) * s[i];
+  if (i < 2 * half) return __ldcg(v + i - half) * s[i - half] + __ldcg(v + i) * c[i - half];
+  return __ldcg(v + i);
 }
 
-// grid (H, n_chunks), 128 threads. Scores for chunk positions, chunk-local
-// softmax stats + weighted V; the last chunk CTA of a head merges.
-extern "C" __global__ void __launch_bounds__(128)
-attention_kernel(const AttnDesc A, Control* __restrict__ ctl) {
-  extern __shared__ float ash[];
-  float* q = ash;                        // [hd]
-  float* kt = q + A.hd;                  // [hd] rotated k at position t
-  float* vt = kt + A.hd;                 // [hd]
-  float* sc = vt + A.hd;                 // [kAttnChunk]
-  __shared__ float red[4];
-  __shared__ int last;
-  pdl_wait();
-  const int h = blockIdx.x, ch = blockIdx.y;
-  const int t = ctl->pos;
+// One (head, 64-position chunk) unit: RoPE on q and the new k, scores, chunk
+// softmax stats and weighted V; the last chunk of a head merges the chunks
+// (runtime.py:351-362). smem: (3 hd + kAttnChunk) floats + 1 int.
+__device__ void attn_unit(const AttnDesc& A, int h, int ch, int t, float* ash, float* kvs, unsigned epoch) {
+  float* q = ash;
+  float* kt = q + A.hd;
+  float* vt = kt + A.hd;
+  float* sc = vt + A.hd;
+  int* last = reinterpret_cast<int*>(sc + kAttnChunk);
   const int n_used = t / kAttnChunk + 1;
-  if (ch >= n_used) return;
   const int grp = A.H / A.KV, kvh = h / grp;
   const int half = A.hd / 2;
   const float* cs = A.cosv + (size_t)t * half;
@@ -796,10 +920,17 @@ attention_kernel(const AttnDesc A, Control* __restrict__ ctl) {
   const float* kraw = A.qkv + A.d + kvh * A.hd;
   const float* vraw = A.qkv + A.d + A.dkv + kvh * A.hd;
   const float scale = 1.0f / sqrtf((float)A.hd);
+  if (A.qkv_flags && threadIdx.x < 32) {
+    wait_flags_warp(A.qkv_flags, (h * A.hd) / 32, (h * A.hd + A.hd + 31) / 32, epoch);
+    wait_flags_warp(A.qkv_flags, (A.d + kvh * A.hd) / 32, (A.d + kvh * A.hd + A.hd + 31) / 32, epoch);
+    wait_flags_warp(A.qkv_flags, (A.d + A.dkv + kvh * A.hd) / 32, (A.d + A.dkv + kvh * A.hd + A.hd + 31) / 32,
+                    epoch);
+  }
+  __syncthreads();
   for (int i = threadIdx.x; i < A.hd; i += blockDim.x) {
-    q[i] = half ? rope_elem(qraw, i, A.hd, cs, sn) : qraw[i];
-    kt[i] = half ? rope_elem(kraw, i, A.hd, cs, sn) : kraw[i];
-    vt[i] = vraw[i];
+    q[i] = half ? rope_elem(qraw, i, A.hd, cs, sn) : __ldcg(qraw + i);
+    kt[i] = half ? rope_elem(kraw, i, A.hd, cs, sn) : __ldcg(kraw + i);
+    vt[i] = __ldcg(vraw + i);
   }
   __syncthreads();
   // the first query head of each kv group appends position t to the cache
@@ -810,9 +941,23 @@ attention_kernel(const AttnDesc A, Control* __restrict__ ctl) {
     }
   }
   const int s0 = ch * kAttnChunk, s1 = min(t + 1, s0 + kAttnChunk);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int s = s0 + warp; s < s1; s += 4) {
-    const float* kr = (s == t) ? kt : A.kc + (size_t)s * A.dkv + kvh * A.hd;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // stage this chunk's K and V rows in shared memory (one coalesced pass)
+  float* Ks = kvs;
+  float* Vs = kvs + kAttnChunk * A.hd;
+  const int npos = s1 - s0;
+  for (int idx = threadIdx.x; idx < npos * A.hd; idx += blockDim.x) {
+    const int sp = idx / A.hd, i = idx - sp * A.hd;
+    const int s = s0 + sp;
+    if (s == t) { Ks[idx] = kt[i]; Vs[idx] = vt[i]; }
+    else {
+      Ks[idx] = __ldcg(A.kc + (size_t)s * A.dkv + kvh * A.hd + i);
+      Vs[idx] = __ldcg(A.vc + (size_t)s * A.dkv + kvh * A.hd + i);
+    }
+  }
+  __syncthreads();
+  for (int s = s0 + warp; s < s1; s += nw) {
+    const float* kr = Ks + (s - s0) * A.hd;
     float acc = 0.f;
     for (int i = lane; i < A.hd; i += 32) acc += q[i] * kr[i];
     acc = warp_sum(acc);
@@ -826,13 +971,23 @@ attention_kernel(const AttnDesc A, Control* __restrict__ ctl) {
   __syncthreads();
   float l = 0.f;
   for (int s = s0; s < s1; ++s) l += sc[s - s0];
+  if (n_used == 1) {
+    for (int i = threadIdx.x; i < A.hd; i += blockDim.x) {
+      float o = 0.f;
+      for (int s = 0; s < npos; ++s) o += sc[s] * Vs[s * A.hd + i];
+      A.out[h * A.hd + i] = o / l;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && A.head_flags) {
+      __threadfence();
+      st_release(A.head_flags + h, epoch);
+    }
+    return;
+  }
   float* P = A.part + ((size_t)h * A.n_chunks + ch) * (A.hd + 2);
   for (int i = threadIdx.x; i < A.hd; i += blockDim.x) {
     float o = 0.f;
-    for (int s = s0; s < s1; ++s) {
-      const float vv = (s == t) ? vt[i] : A.vc[(size_t)s * A.dkv + kvh * A.hd + i];
-      o += sc[s - s0] * vv;
-    }
+    for (int s = 0; s < npos; ++s) o += sc[s] * Vs[s * A.hd + i];
     P[i] = o;
   }
   if (threadIdx.x == 0) { P[A.hd] = mx; P[A.hd + 1] = l; }
@@ -840,10 +995,10 @@ attention_kernel(const AttnDesc A, Control* __restrict__ ctl) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned old = atomicAdd(A.cnt + h, 1u);
-    last = (old == (unsigned)n_used - 1);
+    *last = (old == (unsigned)n_used - 1);
   }
   __syncthreads();
-  if (!last) return;
+  if (!*last) return;
   __threadfence();
   float M = -CUDART_INF_F;
   for (int c = 0; c < n_used; ++c)
@@ -861,8 +1016,24 @@ attention_kernel(const AttnDesc A, Control* __restrict__ ctl) {
     }
     A.out[h * A.hd + i] = o / Lsum;
   }
-  if (threadIdx.x == 0) A.cnt[h] = 0u;
-  (void)red;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    A.cnt[h] = 0u;
+    if (A.head_flags) {
+      __threadfence();
+      st_release(A.head_flags + h, epoch);
+    }
+  }
+}
+
+// grid (H, n_chunks), 128 threads.
+extern "C" __global__ void __launch_bounds__(128)
+attention_kernel(const AttnDesc A, Control* __restrict__ ctl) {
+  extern __shared__ float ash[];
+  pdl_wait();
+  const int t = ctl->pos;
+  if ((int)blockIdx.y >= t / kAttnChunk + 1) return;
+  attn_unit(A, blockIdx.x, blockIdx.y, t, ash, ash + 3 * A.hd + kAttnChunk + 4, 0u);
 }
 
 struct HeadDesc {
@@ -874,24 +1045,27 @@ struct HeadDesc {
   int vocab, d;
   float eps;
   int max_steps;
+  const unsigned* x_flags;   // persistent: all d/32 tiles of the last down op
 };
 
-// grid: ceil(vocab / 16) CTAs x 512 threads (16 warps = 16 logits per CTA).
-extern "C" __global__ void __launch_bounds__(512)
-lmhead_kernel(const HeadDesc Hd, Control* __restrict__ ctl) {
-  extern __shared__ float xs[];          // [d] normalized final residual
+// Final RMSNorm + lm_head rows [16 cta, 16 cta + 16) + (last CTA) greedy
+// argmax and end-of-step control (runtime.py:372-380). blockDim 512.
+__device__ void head_stage(const HeadDesc& Hd, Control* __restrict__ ctl, int cta, int G, float* xs,
+                           unsigned epoch) {
   __shared__ double red[32];
   __shared__ int last;
-  pdl_wait();
+  __shared__ float bv[512];
+  __shared__ int bx[512];
+  if (Hd.x_flags && threadIdx.x < 32) wait_flags_warp(Hd.x_flags, 0, (Hd.d + 31) / 32, epoch);
+  __syncthreads();
   double sq = 0.0;
-  for (int i = threadIdx.x; i < Hd.d; i += blockDim.x) { const double v = Hd.x[i]; sq += v * v; }
+  for (int i = threadIdx.x; i < Hd.d; i += blockDim.x) { const double v = __ldcg(Hd.x + i); sq += v * v; }
   sq = block_sum_d(sq, red);
   const float inv = (float)(1.0 / sqrt(sq / (double)Hd.d + (double)Hd.eps));
-  for (int i = threadIdx.x; i < Hd.d; i += blockDim.x) xs[i] = Hd.x[i] * inv;
+  for (int i = threadIdx.x; i < Hd.d; i += blockDim.x) xs[i] = __ldcg(Hd.x + i) * inv;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int v = blockIdx.x * 16 + warp;
-  if (v < Hd.vocab) {
+  for (int v = cta * 16 + warp; warp < 16 && v < Hd.vocab; v += G * 16) {
     const float* row = Hd.lm + (size_t)v * Hd.d;
     float acc = 0.f;
     for (int i = lane; i < Hd.d; i += 32) acc += row[i] * xs[i];
@@ -900,24 +1074,22 @@ lmhead_kernel(const HeadDesc Hd, Control* __restrict__ ctl) {
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(Hd.cnt, 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) last = (atomicAdd(Hd.cnt, 1u) == (unsigned)G - 1);
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // greedy argmax (first maximum, like np.argmax) + end-of-step control
+  // greedy argmax (first maximum, like np.argmax)
   float best = -CUDART_INF_F;
   int bi = 0x7fffffff;
   for (int i = threadIdx.x; i < Hd.vocab; i += blockDim.x) {
     const float z = __ldcg(Hd.logits + i);
     if (z > best || (z == best && i < bi)) { best = z; bi = i; }
   }
-  __shared__ float bv[512];
-  __shared__ int bx[512];
   bv[threadIdx.x] = best;
   bx[threadIdx.x] = bi;
   __syncthreads();
-  for (int o = 256; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
       const float zb = bv[threadIdx.x + o];
       const int ib = bx[threadIdx.x + o];
       if (zb > bv[threadIdx.x] || (zb == bv[threadIdx.x] && ib < bx[threadIdx.x])) {
@@ -940,8 +1112,17 @@ lmhead_kernel(const HeadDesc Hd, Control* __restrict__ ctl) {
       ctl->snap_w ^= 1;
       ctl->has_prev = 1;
     }
+    __threadfence();
     ctl->n_steps_done += 1;
   }
+}
+
+// grid: ceil(vocab / 16) CTAs x 512 threads.
+extern "C" __global__ void __launch_bounds__(512)
+lmhead_kernel(const HeadDesc Hd, Control* __restrict__ ctl) {
+  extern __shared__ float xs[];
+  pdl_wait();
+  head_stage(Hd, ctl, blockIdx.x, gridDim.x, xs, 0u);
 }
 
 // x = embed[ctl->token]  (runtime.py:345)
@@ -951,6 +1132,106 @@ extern "C" __global__ void begin_kernel(const float* __restrict__ embed, float* 
   const int tok = ctl->token;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x)
     x[i] = embed[(size_t)tok * d + i];
+}
+
+// ---------------------------------------------------------------------------
+// Persistent decode step: one CTA per SM runs every stage of one token.
+// Stages are linked by epoch-tagged readiness flags (per 32-row output tile of
+// an op, per attention head, per embedding tile) instead of kernel
+// boundaries: a CTA starts its share of op N+1 as soon as the input window it
+// needs is final, and prefetches op N+1's planes into L2 while op N runs.
+// ---------------------------------------------------------------------------
+enum StageKind : int { ST_BEGIN = 0, ST_OP = 1, ST_ATTN = 2, ST_HEAD = 3 };
+
+struct Stage {
+  int kind;
+  int idx;                   // op / attention index
+  int G;                     // participating CTAs
+  int next_op;               // op whose planes to prefetch (-1 none)
+  const unsigned* dep0;
+  const unsigned* dep1;
+  int dep0_off, dep0_rpf, dep1_off, pad_;
+  unsigned* out_flags;
+};
+
+struct StepDesc {
+  int n_stages;
+  const Stage* stages;
+  const OpDesc* ops;
+  const AttnDesc* attn;
+  HeadDesc head;
+  const float* embed;
+  float* x;
+  unsigned* x_flags;         // begin stage output flags [d/32]
+  int d;
+};
+
+extern "C" __global__ void __launch_bounds__(kThreads, 1)
+step_kernel(const StepDesc SD, Control* __restrict__ ctl) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ Control cs;          // the control block, read once (constant during a step)
+  pdl_wait();
+  if (threadIdx.x == 0) cs = *ctl;
+  __syncthreads();
+  const unsigned epoch = (unsigned)cs.n_steps_done + 1u;
+  // scratch region below the LUT: [OpSmem][S arrays 32 KB][OpDesc copy]
+  float* aux = reinterpret_cast<float*>(smem_raw + kOpSmemBytes);
+  OpDesc* dsm = reinterpret_cast<OpDesc*>(smem_raw + kOpSmemBytes + 2 * kThreads * kWarpTiles * 4);
+  const int cta = blockIdx.x;
+  // embedding: CTA c writes x tiles c, c+G, ...
+  {
+    const int tok = cs.token;
+    const int n_t = (SD.d + 31) / 32;
+    for (int tt = cta; tt < n_t; tt += gridDim.x) {
+      const int i = tt * 32 + (threadIdx.x & 31);
+      if (threadIdx.x < 32 && i < SD.d) SD.x[i] = SD.embed[(size_t)tok * SD.d + i];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(SD.x_flags + tt, epoch);
+      }
+    }
+  }
+  for (int si = 0; si < SD.n_stages; ++si) {
+    const Stage st = SD.stages[si];
+    __syncthreads();
+    if (st.kind == ST_OP) {
+      if (cta == (int)gridDim.x - 1) {           // the dedicated decider CTA
+        if (threadIdx.x < 32) decide_warp(SD.ops[st.idx], &cs, st.G);
+        continue;
+      }
+      if (cta >= st.G) continue;
+      const int n = (int)(sizeof(OpDesc) / 4);
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        reinterpret_cast<int*>(dsm)[i] = reinterpret_cast<const int*>(SD.ops + st.idx)[i];
+      __syncthreads();
+      StageCtx X{};
+      X.cta = cta;
+      X.G = st.G;
+      X.epoch = epoch;
+      X.dep0 = st.dep0;
+      X.dep0_off = st.dep0_off;
+      X.dep0_rpf = st.dep0_rpf;
+      X.dep1 = st.dep1;
+      X.dep1_off = st.dep1_off;
+      X.out_flags = st.out_flags;
+      X.next = st.next_op >= 0 ? SD.ops + st.next_op : nullptr;
+      op_stage(*dsm, &cs, X, smem_raw);
+    } else if (st.kind == ST_ATTN) {
+      const AttnDesc& A = SD.attn[st.idx];
+      const int t = cs.pos;
+      const int n_used = t / kAttnChunk + 1;
+      const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
+      float* kvs = reinterpret_cast<float*>(smem_raw + (kLutShared - sbase));   // LUT region is free here
+      for (int u = cta; u < A.H * n_used; u += gridDim.x - 1) {
+        if (cta == (int)gridDim.x - 1) break;
+        attn_unit(A, u / n_used, u % n_used, t, aux, kvs, epoch);
+        __syncthreads();
+      }
+    } else if (st.kind == ST_HEAD) {
+      if (cta < st.G && cta != (int)gridDim.x - 1) head_stage(SD.head, ctl, cta, st.G, aux, epoch);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -318,3 +318,28 @@ def test_async_prev_step_and_prev_block_projection(toy_weights, toy_store):
             _, est_o = trace_arrays(eng_o.records, ids)
             _, est_d = trace_arrays(eng.trace.steps, ids)
             np.testing.assert_allclose(est_d, est_o, rtol=1e-4)
+
+
+@pytest.mark.parametrize("gqa", [False, True])
+def test_persistent_step_kernel_equals_multi_kernel(gqa):
+    """The persistent flag-linked step kernel and the per-op kernel graph run
+    the same arithmetic: logits, decisions and estimates are bit-identical."""
+    cfg = M.ModelConfig(n_blocks=3, d_model=256, n_heads=8, d_ff=768, vocab=256, seq_cap=160,
+                        n_kv_heads=2 if gqa else None)
+    w = M.init_model(1, cfg)
+    store = Q.quantize_model(w, 5, 3)
+    plan = synthetic_projection_plan(store, {l: (3, 4) for l in store.layers}, k=32, seed=4)
+    toks = np.random.default_rng(9).integers(0, 256, 90)
+    calibrate_T(w, store, plan, toks[:12])
+    runs = []
+    for persistent in (True, False):
+        eng = R.DecodeEngine(w, store, plan, use_persistent=persistent)
+        assert eng.persistent == persistent
+        lg = [eng.step(int(toks[0]), dynamic=False)]
+        for t in toks[1:]:
+            lg.append(eng.step(int(t), dynamic=True))
+        runs.append((np.array(lg), [s.bits for s in eng.trace.steps],
+                     [s.estimates for s in eng.trace.steps]))
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert runs[0][1] == runs[1][1]
+    assert runs[0][2] == runs[1][2]

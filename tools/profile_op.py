@@ -61,6 +61,17 @@ def main():
     _lib.call("dpq_session_debug_times", eng._h, C.c_void_p(buf.ctypes.data), buf.size, C.byref(per))
     buf = buf.reshape(-1, per.value // 8, 8).astype(np.int64)
     names = ["qkv", "o", "upgate", "down"]
+    os.makedirs("gpurun_out", exist_ok=True)
+    np.save(f"gpurun_out/stamps_{'static' if args.static else 'dyn'}_{'graph' if args.graph else 'eager'}.npy", buf)
+    valid_all = buf[buf[:, :, 0] > 0]
+    T0 = valid_all[:, 0].min() if len(valid_all) else 0
+    print("timeline (us from first stamp): op first_start last_start median_dep_ready last_end")
+    for i in range(n_ops):
+        t = buf[i][buf[i][:, 0] > 0]
+        if len(t) == 0:
+            continue
+        print(f"  {names[i % 4] + str(i // 4):>10} {(t[:, 0].min() - T0) / 1e3:8.1f} {(t[:, 0].max() - T0) / 1e3:8.1f} "
+              f"{(np.median(t[:, 1]) - T0) / 1e3:8.1f} {(t[:, 7].max() - T0) / 1e3:8.1f}")
     print(f"{'op':>10} {'ev_us':>7} {'grid':>4} {'start_spread':>12} {'wait':>6} {'lut':>6} {'G+arr':>6} "
           f"{'->dec':>6} {'phA':>6} {'dwait':>6} {'rest':>6} {'total':>7}")
     for i in range(n_ops):
