@@ -145,6 +145,10 @@ int dpq_session_is_persistent(dpq_session* ss);
  * in schedule order (4 ops per block: qkv, o, up|gate, down). */
 int dpq_session_profile_ops(dpq_session* ss, int token, int dynamic, float* op_ms, int max_ops,
                             int* n_ops);
+/* Persistent engine stage list (kind: 0 begin, 1 op, 2 attention, 3 head,
+ * 4 emit; idx: op index in schedule order / block). n_stages = 0 when the
+ * session runs the multi-kernel path (exact / track_exact plans). */
+int dpq_session_engine_stages(dpq_session* ss, int* n_stages, int32_t* kinds, int32_t* idx);
 int dpq_session_logits_dev(dpq_session* ss, float** logits_dev);
 /* Diagnostics (env DPQ_DEBUG_TIMES=1 at session creation): per-CTA phase
  * timestamps (globaltimer ns) of every op of the last step, [op][per_op]. */

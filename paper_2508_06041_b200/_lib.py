@@ -69,6 +69,7 @@ _SIGS = {
     "dpq_session_position": ([P, C.POINTER(C.c_int)], C.c_int),
     "dpq_session_is_persistent": ([P], C.c_int),
     "dpq_session_logits_dev": ([P, C.POINTER(P)], C.c_int),
+    "dpq_session_engine_stages": ([P, C.POINTER(C.c_int), P, P], C.c_int),
     "dpq_session_profile_ops": ([P, C.c_int, C.c_int, P, C.c_int, C.POINTER(C.c_int)], C.c_int),
     "dpq_session_debug_times": ([P, P, C.c_int64, C.POINTER(C.c_int)], C.c_int),
     "dpq_repack_host": ([P, C.c_int, C.c_int, C.c_int, P, C.c_int64], C.c_int),

@@ -321,9 +321,10 @@ def test_async_prev_step_and_prev_block_projection(toy_weights, toy_store):
 
 
 @pytest.mark.parametrize("gqa", [False, True])
-def test_persistent_step_kernel_equals_multi_kernel(gqa):
-    """The persistent flag-linked step kernel and the per-op kernel graph run
-    the same arithmetic: logits, decisions and estimates are bit-identical."""
+def test_engine_matches_multi_kernel_and_is_deterministic(gqa):
+    """The persistent engine (producer-fused estimators, fixed-point
+    accumulation) and the per-op kernel graph agree under forced-bits replay;
+    two engine runs are bit-identical (logits, decisions, estimates)."""
     cfg = M.ModelConfig(n_blocks=3, d_model=256, n_heads=8, d_ff=768, vocab=256, seq_cap=160,
                         n_kv_heads=2 if gqa else None)
     w = M.init_model(1, cfg)
@@ -331,10 +332,11 @@ def test_persistent_step_kernel_equals_multi_kernel(gqa):
     plan = synthetic_projection_plan(store, {l: (3, 4) for l in store.layers}, k=32, seed=4)
     toks = np.random.default_rng(9).integers(0, 256, 90)
     calibrate_T(w, store, plan, toks[:12])
+    ids = store.ordered_ids()
     runs = []
-    for persistent in (True, False):
-        eng = R.DecodeEngine(w, store, plan, use_persistent=persistent)
-        assert eng.persistent == persistent
+    for _ in range(2):
+        eng = R.DecodeEngine(w, store, plan)
+        assert eng.persistent
         lg = [eng.step(int(toks[0]), dynamic=False)]
         for t in toks[1:]:
             lg.append(eng.step(int(t), dynamic=True))
@@ -343,3 +345,20 @@ def test_persistent_step_kernel_equals_multi_kernel(gqa):
     assert np.array_equal(runs[0][0], runs[1][0])
     assert runs[0][1] == runs[1][1]
     assert runs[0][2] == runs[1][2]
+    old = R.DecodeEngine(w, store, plan, use_persistent=False)
+    assert not old.persistent
+    lg = [old.step(int(toks[0]), dynamic=False)]
+    for t, bits in zip(toks[1:], runs[0][1]):
+        lg.append(old.step(int(t), dynamic=True, forced_bits=bits))
+    lg = np.array(lg)
+    assert np.max(np.abs(lg - runs[0][0])) <= 1e-4 * np.max(np.abs(lg))
+    est_e = np.array([[e[l] for l in ids] for e in runs[0][2]])
+    est_o = np.array([[s.estimates[l] for l in ids] for s in old.trace.steps])
+    np.testing.assert_allclose(est_e, est_o, rtol=1e-4)
+    T = np.array([plan.layers[l].T for l in ids])
+    hi = np.array([plan.layers[l].pair[1] for l in ids])
+    lo = np.array([plan.layers[l].pair[0] for l in ids])
+    want = np.where(est_o > T, hi, lo)
+    got = np.array([[b[l] for l in ids] for b in runs[0][1]])
+    near = np.abs(est_o - T) <= 1e-3 * np.abs(T)
+    assert np.all((got == want) | near)
