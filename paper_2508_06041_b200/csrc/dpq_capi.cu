@@ -249,6 +249,7 @@ struct dpq_session {
   int eng_smem = 0;
   int eng_grid = 0;
   unsigned long long* eng_dbg = nullptr;
+  unsigned long long* eng_emit = nullptr;
 };
 
 // ---------------------------------------------------------------------------
@@ -291,7 +292,35 @@ extern "C" int dpq_repack_host(const uint16_t* codes, int rows, int cols, int n_
 // ---------------------------------------------------------------------------
 // misc
 // ---------------------------------------------------------------------------
-extern "C" const char* dpq_last_error(void) { return g_err.c_str(); }
+static unsigned long long* g_diag_host = nullptr;   // mapped: engine watchdog record
+static int* g_prog_host = nullptr;                    // mapped: per-CTA progress (DPQ_ENGINE_TRACE)
+
+extern "C" const char* dpq_last_error(void) {
+  if (g_diag_host && g_diag_host[0]) {
+    char buf[512];
+    snprintf(buf, sizeof(buf), " [engine watchdog: dpq_engine.cu line %llu, block %llu, thread %llu, args %lld %lld"
+             " extra %llx %llx %llx %llx %llx %llx]",
+             g_diag_host[1], g_diag_host[2], g_diag_host[3], (long long)g_diag_host[4], (long long)g_diag_host[5],
+             g_diag_host[6], g_diag_host[7], g_diag_host[8], g_diag_host[9], g_diag_host[10], g_diag_host[11]);
+    g_err += buf;
+    g_err += " wstate:";
+    for (int q = 0; q < 16; ++q) {
+      snprintf(buf, sizeof(buf), " %llu/%llu", g_diag_host[12 + q] / 16, g_diag_host[12 + q] % 16);
+      g_err += buf;
+    }
+    g_diag_host[0] = 0;
+    if (g_prog_host) {
+      std::string pr = " progress(cta: step<<16|stage, phase, prod_j, prod_op):";
+      for (int c = 0; c < 148; ++c) {
+        snprintf(buf, sizeof(buf), " %d:%x,%d,%d,%d", c, g_prog_host[4 * c], g_prog_host[4 * c + 1], g_prog_host[4 * c + 2],
+                 g_prog_host[4 * c + 3]);
+        pr += buf;
+      }
+      g_err += pr;
+    }
+  }
+  return g_err.c_str();
+}
 extern "C" int dpq_version(void) { return 1; }
 
 extern "C" int dpq_device_info(int device, int* n_sm, int* cc_major, int* cc_minor) {

@@ -28,14 +28,20 @@
 //    and feeds the next estimators.
 #include "dpq_common.cuh"
 
+// Consumer-only CTA barrier (the producer warp never joins).
+#define CSYNC() asm volatile("bar.sync 1, 512;" ::: "memory")
+
 namespace dpq {
 namespace eng {
 
-constexpr int NT = 384;            // threads per CTA
-constexpr int NW = NT / 32;        // warps per CTA
-constexpr int DEPTH = 4;           // register ring depth (plane items in flight per warp; slots a, b, c, e)
-constexpr int kMaxRuns = 48;
-constexpr int kMaxChunks = 48;
+constexpr int NT = 512;            // consumer threads per CTA (warps 0..15)
+constexpr int NW = NT / 32;        // consumer warps
+constexpr int NTB = NT + 32;       // block: consumers + one TMA producer warp (warp 16)
+constexpr int kSlotTiles = 8;      // tiles per ring slot (one plane of up to 8 consecutive tiles)
+constexpr int kSlotBytes = kSlotTiles * 2048;
+constexpr int kMaxSlots = 8;       // ring slots (power of two: index arithmetic by shifts)
+constexpr int kMaxRuns = 96;       // (layer, window, <= 8 tiles) runs per op per CTA
+constexpr int kMaxTiles = 128;     // tiles (groups) per op per CTA (parked base sums)
 constexpr double kFxSum = 4294967296.0;       // 2^32: sum v
 constexpr double kFxSq = 16777216.0;          // 2^24: sum v^2
 
@@ -102,10 +108,10 @@ struct Prog {
   float* logits;
   float* const* kc;        // [n_blocks] -> [seq_cap][dkv]
   float* const* vc;
-  float* slot_base;        // [max_win][slot_stride]
+  unsigned long long* slot;  // [max_win][slot_stride]: float S | epoch << 32 (single-copy atomic)
   float* slot_extra;
   int slot_stride;
-  unsigned* tile_cnt;
+  int slot_max_win;
   float* attn_part;        // [H][max_chunks][hd + 2]
   unsigned* attn_cnt;      // [KV]
   int attn_max_chunks;
@@ -120,6 +126,8 @@ struct Prog {
   int n_trace, max_steps;
   int* tok_log;
   struct ECtl* ctl;
+  int smem_dyn;             // dynamic shared memory bytes of the launch
+  int upper_slots;          // ring slots above the LUT too
   unsigned long long* dbg; // optional per-stage timestamps [stages][grid][8]
 };
 
@@ -147,6 +155,9 @@ __device__ __forceinline__ uint4 ld_nc(const uint4* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
+__device__ __forceinline__ void l1_prefetch(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" :: "l"(p));
+}
 __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
 }
@@ -166,9 +177,42 @@ __device__ __forceinline__ unsigned long long gclock() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// Spin-wait watchdog: a wait beyond 4 s traps (a launch error instead of a
-// hang). No call, so nothing is spilled around the polling loops.
-#define hang(what, a, b) __trap()
+// Spin-wait watchdog: a wait beyond 4 s records (line, block, thread, a, b)
+// in mapped host memory (dpq_engine_diag) and traps (a launch error instead of
+// a hang). No call, so nothing is spilled around the polling loops.
+__device__ unsigned long long* g_diag = nullptr;
+__device__ volatile int* g_prog = nullptr;     // optional mapped progress words [grid][4] (debug)
+#ifdef DPQ_ENGINE_TRACE
+#define PROGRESS(slot, v) do { if (g_prog) g_prog[blockIdx.x * 4 + (slot)] = (v); } while (0)
+#define WSTATE(v) do { if (lane == 0) sm.wstate[warp] = (v); } while (0)
+#else
+#define PROGRESS(slot, v) do { } while (0)
+#define WSTATE(v) do { } while (0)
+#endif
+#define hang(what, a, b)                                                                   \
+  do {                                                                                     \
+    if (g_diag) {                                                                          \
+      volatile unsigned long long* d_ = g_diag;                                            \
+      d_[1] = (unsigned long long)__LINE__; d_[2] = blockIdx.x; d_[3] = threadIdx.x;       \
+      d_[4] = (unsigned long long)(long long)(a); d_[5] = (unsigned long long)(long long)(b); \
+      __threadfence_system(); d_[0] = 1ull; __threadfence_system();                        \
+    }                                                                                      \
+    __trap();                                                                              \
+  } while (0)
+// Poll cheaply; read the (slow) global timer only every 4096 polls.
+#define SPIN_UNTIL_NS(cond, what, a, b, NS)                                                \
+  do {                                                                                     \
+    unsigned n_ = 0;                                                                       \
+    unsigned long long t0_ = 0;                                                            \
+    while (!(cond)) {                                                                      \
+      if ((++n_ & 4095u) == 0) {                                                           \
+        const unsigned long long t_ = gclock();                                            \
+        if (t0_ == 0) t0_ = t_;                                                            \
+        else if (t_ - t0_ > (NS)) hang(what, a, b);                                         \
+      }                                                                                    \
+    }                                                                                      \
+  } while (0)
+#define SPIN_UNTIL(cond, what, a, b) SPIN_UNTIL_NS(cond, what, a, b, 4000000000ull)
 template <typename T>
 __device__ __forceinline__ T wsum(T v) {
 #pragma unroll
@@ -244,15 +288,16 @@ __device__ __forceinline__ void build_lut(float* lut, const float* xw) {
 // A group is (32-row tile t, 512-column window w), linear index g = w * n_tiles
 // + t (window-major). Groups are split over the grid by their base planes
 // (known before the decision), CTA c owning [ga, gb) starting at the first
-// group at or after item c*N/G. Warp k of a CTA owns groups ga + k + NW*j and
-// streams, in order, the base planes of all its groups, then the extra planes
-// (l..b-1) of those whose layer decided high; S is accumulated per group by
-// Horner over planes (S_{p+1} = 2 S_p + P_p), the base part parked in shared
-// memory between the two passes.
+// group at or after item c*N/G. The range is cut into runs of <= 8 tiles of
+// one layer inside one window. The TMA producer warp streams, per run and
+// plane, one bulk copy of the run's tiles into a 16 KB ring slot: base planes
+// [0, nb) of all runs (window ascending), then - once the decision is
+// published - extra planes [nb, fin) of the runs whose layer decided high
+// (window descending, so the LUT changes at most three times). Consumer task
+// (run, tile) goes to warp k % NW; S is accumulated per tile by Horner over
+// planes (S_{p+1} = 2 S_p + P_p), the base part parked in shared memory.
 // ---------------------------------------------------------------------------
-constexpr int kMaxGroups = 16;     // groups per warp per op
-constexpr int kMaxItems = kMaxGroups * 8;
-constexpr uint32_t kLutA = 0x10000, kLutB = 0x20000;   // two resident window LUTs
+constexpr uint32_t kLut = 0x20000;   // the window LUT (absolute shared address)
 
 struct Work {
   int nb[kMaxOpLayers], fin[kMaxOpLayers];
@@ -260,20 +305,47 @@ struct Work {
   int valid;
 };
 
+struct Run {
+  short li, w;
+  short t0, nt;            // op tiles [t0, t0 + nt)
+  short k0;                // first tile index inside the CTA range (parking slot)
+  short pad;
+};
+
+struct RunList {
+  int n;
+  Run r[kMaxRuns];
+};
+
 struct Smem {
   Prog prog;               // program descriptor (kernel parameter copy)
   ECtl ctl;                // control block of the current step (read at BEGIN)
-  Op op[2];                // shared-memory copies of the current / next op descriptors
-  Work work[2];            // current / next op
-  float xw[2][kWinCols];
+  Op op[2];                // consumer copies of the current / next op descriptors
+  Work work[2];            // consumer work of the current / next op
+  RunList runs;            // consumer run list of the current op
+  Op pop;                  // producer copy of the op it streams
+  Work pw;                 // producer work
+  Op pop2;                 // producer copy of the following op (L2 prefetch)
+  Work pw2;
+  RunList pruns;           // producer run list
+  unsigned long long full[kMaxSlots], empty[kMaxSlots];   // ring mbarriers
+  volatile int seq[kMaxSlots];       // FIFO index armed in each slot (phase disambiguation)
+  unsigned slot_off[kMaxSlots];      // slot byte offset from the dynamic smem base
+  int n_slots;
+  volatile int dec_op;               // op counter whose decision is published
+  volatile int step_ready;           // step whose control block consumers have loaded
+  volatile int cons_op, cons_j;      // consumer progress (watchdog diagnostics)
+  unsigned long long* stamp;         // current stage's timestamps (profiling) or nullptr
+  volatile int wstate[NW];           // per consumer warp: item it waits for * 16 + state
+  int dec_fin[2][kMaxOpLayers];      // published final bits (op counter parity)
+  float xw[kWinCols];
   float scale, sx;         // op input scale (1/rms or 1) and sum of raw input
   int last;
   double red[32];
   float head_v[NW];
   int head_i[NW];
-  float sbuf[NW][kMaxGroups][32];   // base-pass S of groups with extra planes
-  const uint4* ia[NW][kMaxItems];   // per-warp item list: plane address (lane 0)
-  unsigned im[NW][kMaxItems];       // item meta: k | p << 8 | pass << 12 | last << 13 | lutB << 14
+  float sbuf[kMaxTiles][32];         // base-pass S of tiles whose layer has extra planes
+  short fo_bo[kMaxRuns], fo_eo[kMaxRuns], fo_xt[kMaxRuns];
 };
 
 __device__ __forceinline__ int layer_of(const Op& O, int t) {
@@ -321,22 +393,83 @@ __device__ __forceinline__ void build_work_warp(const Op& O, const ECtl& C, int 
     W.nb[lane] = nb[lane];
     W.fin[lane] = nb[lane];
   }
-  if (lane == 0) W.valid = 1;
 }
 
-// Plane address (lane 0) of plane p of group g.
-__device__ __forceinline__ const uint4* group_plane(const Op& O, int g, int p) {
-  const int w = g / O.n_tiles, t = g - w * O.n_tiles;
-  const Layer& L = O.L[layer_of(O, t)];
-  return L.planes + p * L.pstride + ((long long)w * L.n_tiles + (t - L.tile_off)) * (kTileBytes / 16);
+// Run list of work W (one thread; decision independent).
+__device__ void build_runs(const Op& O, const Work& W, RunList& R) {
+  R.n = 0;
+  if (W.ga >= W.gb) return;
+  const int nt = O.n_tiles;
+  const int wa = W.ga / nt, wb = (W.gb - 1) / nt;
+  for (int w = wa; w <= wb; ++w) {
+    const int lo = max(W.ga - w * nt, 0), hi = min(W.gb - w * nt, nt);
+    for (int li = 0; li < O.n_layers; ++li) {
+      const Layer& L = O.L[li];
+      const int t0 = max(lo, L.tile_off), t1 = min(hi, L.tile_off + L.n_tiles);
+      for (int t = t0; t < t1; t += kSlotTiles) {
+        if (R.n >= kMaxRuns) __trap();       // host sizing guarantees this cannot happen
+        Run& r = R.r[R.n++];
+        r.li = (short)li;
+        r.w = (short)w;
+        r.t0 = (short)t;
+        r.nt = (short)min(kSlotTiles, t1 - t);
+        r.k0 = (short)(w * nt + t - W.ga);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA / mbarrier helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_n(unsigned long long* bar, unsigned n) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  const uint32_t a = smem_u32(bar);
+  unsigned ok = 0;
+  auto test = [&]() {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    return ok != 0;
+  };
+  SPIN_UNTIL_NS(test(), "ring slot", (long long)a, (long long)parity, 1000000000ull);
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
 // ---------------------------------------------------------------------------
 // Vector emission: statistics + estimator feeds of one 32-row tile (a warp;
 // lane = row). v = value (0 for padding rows).
 // ---------------------------------------------------------------------------
+// Pull everything emit_tile(inst, tile) will read (feed descriptors, G^T
+// blocks) into L1 ahead of the value it depends on.
+__device__ __forceinline__ void emit_prefetch(const Prog& P, int inst, int tile) {
+  const int lane = threadIdx.x & 31;
+  for (int fi = P.feed_begin[inst]; fi < P.feed_begin[inst + 1]; ++fi) {
+    const Feed* Fp = P.feeds + fi;
+    const uint4* Gt = Fp->Gt;
+    if (!Gt) continue;
+    const int nsub = Fp->kpad / 64, per = Fp->f16 ? 256 : 512;
+    const uint4* blk = Gt + (size_t)tile * nsub * per + lane;
+    for (int i = 0; i < nsub * per / 32; ++i) l1_prefetch(blk + 32 * i);
+  }
+}
+
+__device__ unsigned long long* g_emit_stamp = nullptr;   // profiling: [8] stamps of one emit
 __device__ __noinline__ void emit_tile(const Prog& P, const ECtl& C, int inst, int tile, float v) {
   const int lane = threadIdx.x & 31;
+  unsigned long long* es = (g_emit_stamp && blockIdx.x == 0 && threadIdx.x == 0) ? g_emit_stamp : nullptr;
+  if (es) es[0] = gclock();
   const int cur = C.n_steps_done & 1;
   const double dv = (double)v;
   const double s = wsum(dv), q = wsum(dv * dv);
@@ -355,6 +488,7 @@ __device__ __noinline__ void emit_tile(const Prog& P, const ECtl& C, int inst, i
 #pragma unroll
       for (int q = 0; q < (int)(sizeof(Feed) / 16); ++q) fd[q] = __ldg(fp + q);
     }
+    if (es && fi == P.feed_begin[inst]) es[1] = gclock();
     long long* acc;
     if (F.kind == FEED_PREV) {
       if (!upd) continue;
@@ -375,6 +509,7 @@ __device__ __noinline__ void emit_tile(const Prog& P, const ECtl& C, int inst, i
           uint4 c[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) c[i] = __ldg(blk + 32 * i);
+          if (es && fi == P.feed_begin[inst]) { es[2] = gclock(); es[7] = c[0].x + c[7].w; es[3] = gclock(); }
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const __half2* hh = reinterpret_cast<const __half2*>(&c[i]);
@@ -405,6 +540,7 @@ __device__ __noinline__ void emit_tile(const Prog& P, const ECtl& C, int inst, i
             }
           }
         }
+        if (es && fi == P.feed_begin[inst]) es[4] = gclock();
         const int k0 = sub * 64 + 2 * lane;
         const double sc = ldexp(1.0, F.fb);
         if (k0 < F.k) red_add64(acc + k0, fx((double)g0, sc));
@@ -412,47 +548,45 @@ __device__ __noinline__ void emit_tile(const Prog& P, const ECtl& C, int inst, i
       }
     }
     if (lane == 0) red_add64(acc + F.k, fx(q, kFxSq));
+    if (es && fi == P.feed_begin[inst]) es[5] = gclock();
   }
+  if (es) es[6] = gclock();
 }
 
 // ---------------------------------------------------------------------------
 // Grid barrier (monotonic 64-bit arrival counter)
 // ---------------------------------------------------------------------------
-// bar[0]: arrival counter (G per stage, monotonic); bar[16 * (1 + i)], i < 8:
-// release flags (the stage epoch), written by the last arriver; CTA c polls
-// flag c % 8 (separate lines: polling never contends with the arrivals).
+// Grid barrier: monotonic arrival counter bar[0] (G arrivals per stage);
+// waiters poll it relaxed and fence after (cheapest variant measured by
+// tools/ubench_barrier.cu on B200: ~1.3 us for 148 CTAs).
 __device__ __forceinline__ void bar_arrive(const Prog& P, unsigned long long epoch, int G) {
-  __syncthreads();
+  CSYNC();
   if (threadIdx.x == 0) {
     __threadfence();
-    const unsigned long long old = atomicAdd(P.bar, 1ull);
-    if (old + 1 == epoch * (unsigned long long)G) {
-      __threadfence();
-#pragma unroll
-      for (int i = 0; i < 8; ++i) asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(P.bar + 16 * (1 + i)), "l"(epoch) : "memory");
-    }
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" :: "l"(P.bar) : "memory");
   }
 }
 __device__ __forceinline__ void bar_wait(const Prog& P, unsigned long long epoch) {
   if (threadIdx.x == 0) {
-    const unsigned long long* f = P.bar + 16 * (1 + (blockIdx.x & 7));
-    if (ld_acq64(f) < epoch) {
-      const unsigned long long t0 = gclock();
-      while (ld_acq64(f) < epoch) {
-        if (gclock() - t0 > 4000000000ull) hang("grid barrier", 0, (long long)epoch);
-      }
-    }
+    const unsigned long long target = epoch * (unsigned long long)gridDim.x;
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(P.bar) : "memory");
+    auto poll = [&]() {
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(P.bar) : "memory");
+      return v >= target;
+    };
+    if (v < target) SPIN_UNTIL_NS(poll(), "grid barrier", 0, (long long)epoch, 3000000000ull);
     __threadfence();
   }
-  __syncthreads();
+  CSYNC();
 }
 
 __device__ __forceinline__ void read_ctl(const Prog& P, ECtl& C) {
   const int* src = reinterpret_cast<const int*>(P.ctl);
   int* dst = reinterpret_cast<int*>(&C);
-  __syncthreads();
+  CSYNC();
   if (threadIdx.x < (int)(sizeof(ECtl) / 4)) dst[threadIdx.x] = __ldcg(src + threadIdx.x);
-  __syncthreads();
+  CSYNC();
 }
 
 // ---------------------------------------------------------------------------
@@ -465,28 +599,30 @@ __device__ __forceinline__ void load4(uint4* dst, const uint4* a) {
   dst[3] = ld_nc(a + 96);
 }
 
-// L2 prefetch of this CTA's base planes of op O: one (window, layer, plane)
-// contiguous stripe per thread.
-__device__ __noinline__ void prefetch_work_l2(const Op& O, const Work& W) {
+// L2 prefetch of this CTA's planes [p_lo, p_hi(layer)) of op O (one warp;
+// lane = (window of the CTA range, layer, plane) stripe of contiguous tiles).
+// hi_fin: 0 -> base planes [0, nb), 1 -> extra planes [nb, fin).
+__device__ __forceinline__ void prefetch_work_l2(const Op& O, const Work& W, int extra) {
   if (W.ga >= W.gb) return;
-  int idx = 0;
-  for (int w = W.ga / O.n_tiles; w <= (W.gb - 1) / O.n_tiles; ++w) {
+  const int lane = threadIdx.x & 31;
+  const int w_first = W.ga / O.n_tiles, w_last = (W.gb - 1) / O.n_tiles;
+  const int nwin = min(2, w_last - w_first + 1);
+  for (int idx = lane; idx < nwin * O.n_layers * 8; idx += 32) {
+    const int wi = idx / (O.n_layers * 8), rem = idx - wi * O.n_layers * 8, li = rem >> 3, p = rem & 7;
+    const int p0 = extra ? W.nb[li] : 0, p1 = extra ? W.fin[li] : W.nb[li];
+    if (p < p0 || p >= p1) continue;
+    const int w = w_first + wi;
     const int t_lo = max(W.ga - w * O.n_tiles, 0), t_hi = min(W.gb - w * O.n_tiles, O.n_tiles);
-    for (int li = 0; li < O.n_layers; ++li) {
-      const Layer& L = O.L[li];
-      const int t0 = max(t_lo, L.tile_off), t1 = min(t_hi, L.tile_off + L.n_tiles);
-      if (t0 >= t1) continue;
-      for (int p = 0; p < W.nb[li]; ++p, ++idx) {
-        if ((idx % NT) != (int)threadIdx.x) continue;
-        const char* a = reinterpret_cast<const char*>(L.planes + p * L.pstride + ((long long)w * L.n_tiles + (t0 - L.tile_off)) * 128);
-        long long bytes = (long long)(t1 - t0) * kTileBytes;
-        while (bytes > 0) {
-          const unsigned c = (unsigned)min(bytes, 65536LL);
-          l2_prefetch(a, c);
-          a += c;
-          bytes -= c;
-        }
-      }
+    const Layer& L = O.L[li];
+    const int t0 = max(t_lo, L.tile_off), t1 = min(t_hi, L.tile_off + L.n_tiles);
+    if (t0 >= t1) continue;
+    const char* a = reinterpret_cast<const char*>(L.planes + p * L.pstride + ((long long)w * L.n_tiles + (t0 - L.tile_off)) * 128);
+    long long bytes = (long long)(t1 - t0) * kTileBytes;
+    while (bytes > 0) {
+      const unsigned c = (unsigned)min(bytes, 65536LL);
+      l2_prefetch(a, c);
+      a += c;
+      bytes -= c;
     }
   }
 }
@@ -514,30 +650,48 @@ __device__ __noinline__ void prefetch_feeds_l2(const Prog& P, const ECtl& C, int
 // ---------------------------------------------------------------------------
 // Tile reduction + epilogue (one warp, lane = row of the tile)
 // ---------------------------------------------------------------------------
-// S of op tile t: sum of the window slots in fixed order.
-__device__ __forceinline__ float tile_S(const Prog& P, const Op& O, int t) {
+// S of op tile t: sum of the window slots in fixed window order, each slot
+// awaited until it carries this op's epoch (no fence / counter needed: the
+// 64-bit slot store is single-copy atomic).
+__device__ __forceinline__ float tile_S(const Prog& P, const Op& O, int t, unsigned epoch) {
   const int lane = threadIdx.x & 31;
-  const size_t row = (size_t)t * 32 + lane;
-  float b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f;
-  int w = 0;
-  for (; w + 3 < O.n_win; w += 4) {
-    b0 += __ldcg(P.slot_base + (size_t)w * P.slot_stride + row);
-    b1 += __ldcg(P.slot_base + (size_t)(w + 1) * P.slot_stride + row);
-    b2 += __ldcg(P.slot_base + (size_t)(w + 2) * P.slot_stride + row);
-    b3 += __ldcg(P.slot_base + (size_t)(w + 3) * P.slot_stride + row);
+  const unsigned long long* base = P.slot + (size_t)t * 32 + lane;
+  float acc = 0.f;
+  for (int w0 = 0; w0 < O.n_win; w0 += 8) {
+    const int nw = min(8, O.n_win - w0);
+    unsigned long long v[8];
+    bool ok;
+    unsigned n_ = 0;
+    unsigned long long t0 = 0;
+    do {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < nw) v[j] = __ldcg(base + (size_t)(w0 + j) * P.slot_stride);
+      ok = true;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < nw) ok &= (unsigned)(v[j] >> 32) == epoch;
+      if ((++n_ & 1023u) == 0) {
+        const unsigned long long t_ = gclock();
+        if (t0 == 0) t0 = t_;
+        else if (t_ - t0 > 4000000000ull) hang("window slots", t, 0);
+      }
+    } while (!__all_sync(0xffffffffu, ok));
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < nw) acc += __uint_as_float((unsigned)v[j]);
   }
-  for (; w < O.n_win; ++w) b0 += __ldcg(P.slot_base + (size_t)w * P.slot_stride + row);
-  return (b0 + b1) + (b2 + b3);
+  return acc;
 }
 
 // y of op tile t (layer li) at the final plane count; valid = row exists.
 __device__ __forceinline__ float tile_y(const Prog& P, const Op& O, const Work& W, const Smem& sm, int t,
-                                        int& li, int& r, bool& valid) {
+                                        unsigned epoch, int& li, int& r, bool& valid) {
   const int lane = threadIdx.x & 31;
   li = layer_of(O, t);
   const Layer& L = O.L[li];
   const int fin = W.fin[li];
-  const float S = tile_S(P, O, t);
+  const float S = tile_S(P, O, t, epoch);
   r = (t - L.tile_off) * 32 + lane;
   valid = r < L.rows;
   if (!valid) return 0.f;
@@ -545,139 +699,111 @@ __device__ __forceinline__ float tile_y(const Prog& P, const Op& O, const Work& 
   return sm.scale * (lo * sm.sx + ldexpf(span, -fin) * (S + 0.5f * sm.sx));
 }
 
-__device__ __noinline__ void reduce_unit(const Prog& P, const ECtl& C, const Op& O, const Work& W, const Smem& sm, int u) {
+__device__ __noinline__ void reduce_unit(const Prog& P, const ECtl& C, const Op& O, const Work& W, const Smem& sm, int u,
+                                         unsigned epoch) {
+  const int lane = threadIdx.x & 31;
+  // independent operands first (they do not wait for the window slots)
+  {
+    const int t = u, li = layer_of(O, t);
+    const Layer& L = O.L[li];
+    const int r = (t - L.tile_off) * 32 + lane;
+    if (r < L.rows) { l1_prefetch(L.lo + r); l1_prefetch(L.span + r); }
+    if (O.pair) {
+      const int t2 = u + O.L[0].n_tiles, li2 = layer_of(O, t2);
+      const Layer& L2 = O.L[li2];
+      const int r2 = (t2 - L2.tile_off) * 32 + lane;
+      if (r2 < L2.rows) { l1_prefetch(L2.lo + r2); l1_prefetch(L2.span + r2); }
+    } else if (O.add && r < L.rows) {
+      l1_prefetch(O.out + L.out_off + r);
+    }
+    if (O.out_inst >= 0)
+      emit_prefetch(P, O.out_inst, O.pair ? u : (O.L[li].out_off >> 5) + (u - O.L[li].tile_off));
+  }
+  unsigned long long* stp = (threadIdx.x == 0 && u == blockIdx.x * NW) ? sm.stamp : nullptr;
+  if (stp) stp[2] = gclock();
   if (O.pair) {
     const int half = O.L[0].n_tiles;
     int li, r, li2, r2;
     bool ok, ok2;
-    const float up = tile_y(P, O, W, sm, u, li, r, ok);
-    const float gt = tile_y(P, O, W, sm, u + half, li2, r2, ok2);
+    const float up = tile_y(P, O, W, sm, u, epoch, li, r, ok);
+    const float gt = tile_y(P, O, W, sm, u + half, epoch, li2, r2, ok2);
     const float hv = ok ? up * (gt / (1.0f + expf(-gt))) : 0.f;   // runtime.py:368
     if (ok) O.out[r] = hv;
+    if (stp) stp[3] = gclock();
     if (O.out_inst >= 0) emit_tile(P, C, O.out_inst, u, hv);
+    if (stp) stp[4] = gclock();
   } else {
     int li, r;
     bool ok;
-    const float y = tile_y(P, O, W, sm, u, li, r, ok);
+    const float y = tile_y(P, O, W, sm, u, epoch, li, r, ok);
     const int o = O.L[li].out_off + r;
     float v = 0.f;
     if (O.add) {
       if (ok) {
-        v = __ldcg(O.out + o) + y;                                   // runtime.py:364, 370
+        v = O.out[o] + y;                                            // runtime.py:364, 370
         O.out[o] = v;
       }
     } else if (ok) {
       O.out[o] = y;
     }
+    if (stp) stp[3] = gclock();
     if (O.out_inst >= 0) emit_tile(P, C, O.out_inst, (O.L[li].out_off >> 5) + (u - O.L[li].tile_off), v);
+    if (stp) stp[4] = gclock();
   }
 }
 
 // Contributions a tile (or pair) receives: one per window.
-__device__ __forceinline__ unsigned unit_target(const Op& O, const Work& W, int u) {
-  return (unsigned)O.n_win * (O.pair ? 2u : 1u);
-}
+
 
 // ---------------------------------------------------------------------------
-// The op stage
+// The op stage (consumer warps 0..NW-1)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int my_groups(const Work& W, int warp) {
-  const int n = W.gb - W.ga;
-  return n > warp ? (n - warp + NW - 1) / NW : 0;
-}
-
-// Append the items of one pass (0: planes [0, nb), 1: planes [nb, fin)) of
-// this warp's groups to its shared-memory item list; returns the new length.
-// Lane k < mine handles group k (prefix sums by shuffles).
-__device__ __forceinline__ int list_pass(const Op& O, const Work& W, Smem& sm, int warp, int mine, int pass,
-                                         int n0, int w_first) {
-  const int lane = threadIdx.x & 31;
-  int cnt = 0, p0 = 0, g = 0, li = 0;
-  if (lane < mine) {
-    g = W.ga + warp + NW * lane;
-    li = layer_of(O, g % O.n_tiles);
-    p0 = pass ? W.nb[li] : 0;
-    cnt = (pass ? W.fin[li] : W.nb[li]) - p0;
-  }
-  int incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  if (lane < mine) {
-    const int w = g / O.n_tiles;
-    const unsigned lb = (w != w_first) ? 1u : 0u;
-    for (int q = 0; q < cnt; ++q) {
-      const int idx = n0 + incl - cnt + q;
-      sm.ia[warp][idx] = group_plane(O, g, p0 + q);
-      sm.im[warp][idx] = (unsigned)lane | (unsigned)(p0 + q) << 8 | (unsigned)pass << 12 |
-                         (unsigned)(q + 1 == cnt) << 13 | lb << 14;
-    }
-  }
-  __syncwarp();
-  return n0 + total;
-}
-
-// Reduction duty of this warp: units u = cta * NW + warp (+ G * NW ...);
-// wait until all window contributions arrived, then reduce (fixed order).
+// Reduction duty of this warp: units u = cta * NW + warp (+ G * NW ...),
+// each reduced as soon as its window slots carry this op's epoch.
 __device__ __noinline__ void reduce_duty(const Prog& P, const ECtl& C, const Op& O, const Work& W, const Smem& sm,
-                                          int cta, int G) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                          int cta, int G, unsigned epoch) {
+  const int warp = threadIdx.x >> 5;
   const int n_units = O.pair ? O.L[0].n_tiles : O.n_tiles;
-  for (int u = cta * NW + warp; u < n_units; u += G * NW) {
-    const unsigned target = unit_target(O, W, u);
-    if (lane == 0) {
-      const unsigned* c = P.tile_cnt + u;
-      unsigned v;
-      const unsigned long long t0 = gclock();
-      while (true) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
-        if (v >= target) break;
-        if (gclock() - t0 > 4000000000ull) hang("tile contributions", u, (long long)v);
-      }
-      P.tile_cnt[u] = 0u;
-    }
-    __syncwarp();
-    __threadfence();
-    reduce_unit(P, C, O, W, sm, u);
-  }
+  for (int u = cta * NW + warp; u < n_units; u += G * NW) reduce_unit(P, C, O, W, sm, u, epoch);
 }
 
-__device__ __noinline__ void op_stage(const Prog& P, const ECtl& C, const Op& O, Work& W, const Op* On, Work* Wn,
-                                         Smem& sm, int cta, int G, unsigned long long wait_target, bool do_wait,
-                                         unsigned long long* stamp) {
+// FIFO layout of an op (relative to its first FIFO index): base items run by
+// run, planes [0, nb); then extra items for runs in reverse order, planes
+// [nb, fin). Returns the total and fills per-run offsets (lane-parallel).
+// Returns the number of ring items the op consumed (FIFO advance).
+__device__ __noinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, Work& W, Op* On, Work* Wn,
+                                     const Op* On_global, Smem& sm, int cta, int G,
+                                     unsigned long long wait_target, bool do_wait, unsigned long long* stamp,
+                                     int op_no, int j_op) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned epoch = (unsigned)(wait_target + 1);     // this stage's epoch: tags the window slots
   const int cur = C.n_steps_done & 1;
-  // ---- base work (decision independent) and first loads, before the barrier
-  if (!W.valid) {
+  // ---- base work and run list (decision independent), before the barrier
+  // every thread reads W.valid before anyone can change it: the decision to
+  // join the CSYNC below must be uniform (a named-barrier count mismatch
+  // would silently misalign all later consumer barriers)
+  const bool built = W.valid != 0;
+  CSYNC();
+  if (!built) {
     if (warp == 0) build_work_warp(O, C, cta, G, W);
-    __syncthreads();
+    CSYNC();
   }
-  const int mine = my_groups(W, warp);
-  if (mine > kMaxGroups) __trap();        // host sizing guarantees this cannot happen
-  const int w_first = W.ga < W.gb ? W.ga / O.n_tiles : 0;
-  const int w_last = W.ga < W.gb ? (W.gb - 1) / O.n_tiles : -1;
-  int n_items = list_pass(O, W, sm, warp, mine, 0, 0, w_first);   // base planes: decision independent
-  // register ring: slot d holds item i + d while item i is consumed (named
-  // registers only, so nothing is ever addressed through local memory)
-  uint4 a0, a1, a2, a3, b0, b1, b2, b3, c0, c1, c2, c3, e0, e1, e2, e3;
-#define ENG_LD(X, IDX)                                    \
-  {                                                       \
-    const uint4* a_ = sm.ia[warp][IDX] + lane;            \
-    X##0 = ld_nc(a_); X##1 = ld_nc(a_ + 32);              \
-    X##2 = ld_nc(a_ + 64); X##3 = ld_nc(a_ + 96);         \
+  if (tid == 0) {
+    sm.stamp = stamp;
+    build_runs(O, W, sm.runs);
+    sm.cons_op = op_no;
+    sm.cons_j = j_op;
   }
-  if (0 < n_items) ENG_LD(a, 0)
-  if (1 < n_items) ENG_LD(b, 1)
-  if (2 < n_items) ENG_LD(c, 2)
-  if (3 < n_items) ENG_LD(e, 3)
-  const int n_pre = min(n_items, DEPTH);
   if (do_wait) bar_wait(P, wait_target);
   if (stamp && tid == 0) stamp[0] = gclock();
 
-  // ---- prologue: decisions (runtime.py:184-193), input statistics, x windows
+  // ---- prologue: the first window's input (LUT source) in flight first, then
+  // decisions (runtime.py:184-193), input statistics, the next op's descriptor
+  const int w_first = sm.runs.n > 0 ? sm.runs.r[0].w : -1;
+  if (w_first >= 0) {
+    const int col = w_first * kWinCols + tid;
+    sm.xw[tid] = col < O.cols ? __ldcg(O.in + col) : 0.f;
+  }
   if (warp < O.n_layers) {
     const int li = warp;
     const Layer& L = O.L[li];
@@ -701,6 +827,7 @@ __device__ __noinline__ void op_stage(const Prog& P, const ECtl& C, const Op& O,
     }
     if (lane == 0) {
       W.fin[li] = bit;
+      sm.dec_fin[op_no & 1][li] = bit;
       if (C.mode == MODE_DYNAMIC && cta == 0 && L.trace >= 0 && P.n_trace > 0 && C.trace_step < P.max_steps) {
         const size_t o = (size_t)C.trace_step * P.n_trace + L.trace;
         P.tr_bits[o] = (signed char)bit;
@@ -716,81 +843,251 @@ __device__ __noinline__ void op_stage(const Prog& P, const ECtl& C, const Op& O,
       sm.scale = O.rms ? (float)rsqrt_d(s2 / (double)O.cols + (double)P.eps) : 1.f;
     }
   } else if (warp == kMaxOpLayers + 1 && On && !Wn->valid) {
+    const int nw4 = (int)(sizeof(Op) / 16);
+    const int4* src = reinterpret_cast<const int4*>(On_global);
+    int4* dst = reinterpret_cast<int4*>(On);
+    for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
+    __syncwarp();
     build_work_warp(*On, C, cta, G, *Wn);
+    __syncwarp();
+    if (lane == 0) Wn->valid = 1;
+  } else if (warp == kMaxOpLayers + 2) {
+    prefetch_feeds_l2(P, C, O.out_inst, O.n_tiles * 32, cta, G);
   }
-  // input windows of this CTA (at most two) -> LUT A / B
-  if (w_last > w_first + 1) __trap();     // host sizing guarantees at most two windows per CTA
-  for (int q = tid; q < 2 * kWinCols; q += NT) {
-    const int which = q / kWinCols, w = w_first + which;
-    const int col = w * kWinCols + (q - which * kWinCols);
-    sm.xw[which][q - which * kWinCols] = (w <= w_last && col < O.cols) ? __ldcg(O.in + col) : 0.f;
+  CSYNC();
+  if (tid == 0) {
+    __threadfence_block();
+    sm.dec_op = op_no + 1;            // the producer may now stream the extra planes
   }
-  __syncthreads();
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(&sm);
-  build_lut(reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLutA - sbase)), sm.xw[0]);
-  if (w_last > w_first)
-    build_lut(reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLutB - sbase)), sm.xw[1]);
-  // zero row 256 of each LUT (= row 0 of LUT B for LUT A)
-  if (tid < 64) {
-    reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLutB + 256 * 256 - sbase))[tid] = 0.f;
-    if (w_last == w_first) reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLutB - sbase))[tid] = 0.f;
+  float* lut = reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLut - smem_u32(&sm)));
+  int lut_w = -1;
+  if (w_first >= 0) {                 // LUT of the first window (its input loaded above)
+    build_lut(lut, sm.xw);
+    if (tid < 64) lut[256 * kGroups + tid] = 0.f;
+    lut_w = w_first;
   }
-  __syncthreads();
-  if (stamp && tid == 0) stamp[1] = gclock();
-  // extra planes of groups whose layer decided high; refill the ring to DEPTH
-  n_items = list_pass(O, W, sm, warp, mine, 1, n_items, w_first);
-  if (0 >= n_pre && 0 < n_items) ENG_LD(a, 0)
-  if (1 >= n_pre && 1 < n_items) ENG_LD(b, 1)
-  if (2 >= n_pre && 2 < n_items) ENG_LD(c, 2)
-  if (3 >= n_pre && 3 < n_items) ENG_LD(e, 3)
-  // ---- stream: item i lives in slot i % 4 (a, b, c, e); after use the slot
-  // is refilled with item i + 4. Unrolled by 4 so every slot index is static.
-  float S = 0.f;
-  auto post = [&](int i, float Pv) {
-    const unsigned m = sm.im[warp][i];
-    const int k = m & 0xff, p = (m >> 8) & 0xf, pass = (m >> 12) & 1;
-    const int g = W.ga + warp + NW * k;
-    const int w = g / O.n_tiles, t = g - w * O.n_tiles;
-    const int li = layer_of(O, t);
-    if (pass == 1 && p == W.nb[li]) S = sm.sbuf[warp][k][lane];
-    S = 2.f * S + Pv;                                    // Horner over planes
-    if ((m >> 13) & 1u) {                                // end of this group's pass
-      if (pass == 0 && W.fin[li] > W.nb[li]) sm.sbuf[warp][k][lane] = S;      // park the base part
-      else P.slot_base[(size_t)w * P.slot_stride + (size_t)t * 32 + lane] = S;
-      S = 0.f;
+  // FIFO offsets of the runs (thread 0; a few dozen runs at most)
+  const RunList& R = sm.runs;
+  int n_base = 0, n_ext = 0, t_ext = 0;
+  if (tid == 0) {
+    int o = 0;
+    for (int r = 0; r < R.n; ++r) { sm.fo_bo[r] = (short)o; o += W.nb[R.r[r].li]; }
+    n_base = o;
+    int xt = 0;
+    for (int r = R.n - 1; r >= 0; --r) {
+      const int ex = W.fin[R.r[r].li] - W.nb[R.r[r].li];
+      sm.fo_eo[r] = (short)o;
+      sm.fo_xt[r] = (short)xt;
+      if (ex > 0) { o += ex; xt += R.r[r].nt; }
     }
-  };
-#define ENG_STEP(X, J)                                                                    \
-  if ((J) < n_items) {                                                                    \
-    const unsigned m_ = sm.im[warp][J];                                                   \
-    const uint32_t lr_ = ((m_ >> 14) & 1u ? kLutB : kLutA) | ((uint32_t)lane * 4u);       \
-    const float Pv_ = plane_sum(X##0, X##1, X##2, X##3, lr_);                             \
-    if ((J) + 4 < n_items) ENG_LD(X, (J) + 4)                                             \
-    post((J), Pv_);                                                                       \
+    n_ext = o - n_base;
+    t_ext = xt;
+    sm.last = n_base | (n_ext << 16);
+    reinterpret_cast<int*>(sm.red)[0] = t_ext;
   }
-  for (int i = 0; i < n_items; i += 4) {
-    ENG_STEP(a, i)
-    ENG_STEP(b, i + 1)
-    ENG_STEP(c, i + 2)
-    ENG_STEP(e, i + 3)
+  CSYNC();
+  n_base = sm.last & 0xffff;
+  n_ext = sm.last >> 16;
+  t_ext = reinterpret_cast<int*>(sm.red)[0];
+  if (stamp && tid == 0) stamp[1] = gclock();
+  if (tid == 0) PROGRESS(1, 1);
+  const int n_tasks_base = W.gb - W.ga;
+  // ---- stream: tasks (run, tile) in FIFO order, LUT rebuilt per window segment
+  const unsigned char* dyn0 = reinterpret_cast<const unsigned char*>(&sm);
+  for (int kind = 0; kind < 2; ++kind) {
+    const int n_tasks = kind ? t_ext : n_tasks_base;
+    int k = 0;                          // task index at the segment start
+    int rr = kind ? R.n - 1 : 0;        // run index at the segment start
+    while (k < n_tasks) {
+      // segment: consecutive runs (task order) of one window
+      while (kind && W.fin[R.r[rr].li] == W.nb[R.r[rr].li]) --rr;
+      const int w = R.r[rr].w;
+      int k_end = k, re = rr;
+      while (kind ? re >= 0 : re < R.n) {
+        const Run& q = R.r[re];
+        if (q.w != w) break;
+        if (!kind || W.fin[q.li] > W.nb[q.li]) k_end += q.nt;
+        re += kind ? -1 : 1;
+      }
+      if (w != lut_w) {
+        CSYNC();                          // previous LUT users done
+        const int col = w * kWinCols + tid;
+        sm.xw[tid] = col < O.cols ? __ldcg(O.in + col) : 0.f;
+        CSYNC();
+        build_lut(lut, sm.xw);
+        if (tid < 64) lut[256 * kGroups + tid] = 0.f;
+        CSYNC();
+        lut_w = w;
+      }
+      const uint32_t lanereg = kLut | ((uint32_t)lane * 4u);
+      for (int kt = k + warp; kt < k_end; kt += NW) {
+        // task kt -> run and tile
+        int r = rr, base_k = k;
+        while (true) {
+          const Run& q = R.r[r];
+          const bool has = !kind || W.fin[q.li] > W.nb[q.li];
+          if (has && kt < base_k + q.nt) break;
+          if (has) base_k += q.nt;
+          r += kind ? -1 : 1;
+        }
+        const Run& q = R.r[r];
+        const int i = kt - base_k;
+        const int nb = W.nb[q.li], fin = W.fin[q.li];
+        const int p0 = kind ? nb : 0, p1 = kind ? fin : nb;
+        const int jr = j_op + (kind ? sm.fo_eo[r] : sm.fo_bo[r]);
+        float S = kind ? sm.sbuf[q.k0 + i][lane] : 0.f;
+        for (int p = p0; p < p1; ++p) {
+          const int j = jr + (p - p0);
+          const int slot = j & (kMaxSlots - 1);
+          WSTATE(j * 16 + 1);
+          if (lane == 0) {
+            if (sm.seq[slot] > j) hang("ring overtaken", ((long long)j << 32) | (unsigned)sm.seq[slot], ((long long)r << 32) | (unsigned)kt);
+            if (!(sm.seq[slot] == j)) {
+              unsigned n_ = 0;
+              unsigned long long t0_ = 0;
+              while (!(sm.seq[slot] == j)) {
+                if ((++n_ & 4095u) == 0) {
+                  const unsigned long long t_ = gclock();
+                  if (t0_ == 0) t0_ = t_;
+                  else if (t_ - t0_ > 1000000000ull) {
+                    if (g_diag) {
+                      volatile unsigned long long* d_ = g_diag;
+                      d_[6] = ((unsigned long long)W.ga << 32) | (unsigned)W.gb;
+                      d_[7] = ((unsigned long long)sm.pw.ga << 32) | (unsigned)sm.pw.gb;
+                      d_[8] = (unsigned long long)(W.nb[0] | W.nb[1] << 8 | W.nb[2] << 16 | W.fin[0] << 24) |
+                              ((unsigned long long)(sm.pw.nb[0] | sm.pw.nb[1] << 8 | sm.pw.nb[2] << 16) << 32);
+                      d_[9] = ((unsigned long long)R.n << 32) | (unsigned)sm.pruns.n;
+                      d_[10] = ((unsigned long long)(unsigned)sm.fo_bo[1] << 32) | (unsigned)(j_op);
+                      d_[11] = ((unsigned long long)C.mode << 32) | (unsigned)C.force;
+                      for (int q2 = 0; q2 < NW; ++q2) d_[12 + q2] = (unsigned long long)sm.wstate[q2];
+                    }
+                    hang("ring sequence", ((long long)j << 32) | (unsigned)sm.seq[slot],
+                         ((long long)(kind * 1000 + r) << 32) | (unsigned)kt);
+                  }
+                }
+              }
+            }
+          }
+          __syncwarp();
+          WSTATE(j * 16 + 2);
+          mbar_wait(&sm.full[slot], (unsigned)((j / kMaxSlots) & 1));
+          WSTATE(j * 16 + 3);
+          const uint4* d = reinterpret_cast<const uint4*>(dyn0 + sm.slot_off[slot] + i * kTileBytes) + lane;
+          const uint4 d0 = d[0], d1 = d[32], d2 = d[64], d3 = d[96];
+          S = 2.f * S + plane_sum(d0, d1, d2, d3, lanereg);       // Horner over planes
+          __syncwarp();                                            // every lane has used its slot data
+          if (lane == 0) mbar_arrive_n(&sm.empty[slot], i == q.nt - 1 ? (unsigned)(kSlotTiles + 1 - q.nt) : 1u);
+          WSTATE(j * 16 + 4);
+        }
+        const int t = q.t0 + i;
+        if (!kind && fin > nb) {
+          sm.sbuf[q.k0 + i][lane] = S;                              // park the base part
+        } else {
+          __stcg(P.slot + (size_t)q.w * P.slot_stride + (size_t)t * 32 + lane,
+                 (unsigned long long)epoch << 32 | __float_as_uint(S));
+        }
+      }
+      k = k_end;
+      rr = re;
+    }
+    if (!kind) CSYNC();                   // parked base sums visible before the extra pass
   }
-#undef ENG_STEP
-#undef ENG_LD
+  if (tid == 0) PROGRESS(1, 2);
   if (stamp && tid == 0) stamp[5] = gclock();
-  if (On) prefetch_work_l2(*On, *Wn);
-  if (warp == NW - 1) prefetch_feeds_l2(P, C, O.out_inst, O.n_tiles * 32, cta, G);
-  // ---- publish: one fence per warp, then one arrival per owned group
-  __threadfence();
-  __syncwarp();
-  for (int k = lane; k < mine; k += 32) {
-    const int g = W.ga + warp + NW * k;
-    const int t = g % O.n_tiles;
-    atomicAdd(P.tile_cnt + (O.pair ? (t % O.L[0].n_tiles) : t), 1u);
-  }
-  reduce_duty(P, C, O, W, sm, cta, G);
+  reduce_duty(P, C, O, W, sm, cta, G, epoch);
+  if (tid == 0) PROGRESS(1, 3);
   if (stamp && tid == 0) stamp[6] = gclock();
-  __syncthreads();
+  CSYNC();
   if (tid == 0) W.valid = 0;
+  return n_base + n_ext;
+}
+
+// ---------------------------------------------------------------------------
+// The TMA producer warp: streams every op's planes into the ring, running
+// ahead of the consumers across stage barriers (bounded by ring space, and by
+// each op's decision for its extra planes).
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void producer(const Prog& P, Smem& sm, int cta, int G, int n_steps) {
+  const int lane = threadIdx.x & 31;
+  int j = 0, op_no = 0;
+  const unsigned char* dyn0 = reinterpret_cast<const unsigned char*>(&sm);
+  auto issue = [&](const Op& O, const Run& r, int p) {
+    const int slot = j & (kMaxSlots - 1);
+    if (j >= kMaxSlots) {
+      const uint32_t a = smem_u32(&sm.empty[slot]);
+      const unsigned par = (unsigned)(((j / kMaxSlots) - 1) & 1);
+      unsigned ok = 0;
+      auto test = [&]() {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok) : "r"(a), "r"(par) : "memory");
+        return ok != 0;
+      };
+      SPIN_UNTIL_NS(test(), "producer slot", ((long long)j << 32) | (unsigned)op_no,
+                    ((long long)sm.cons_op << 32) | (unsigned)sm.cons_j, 12000000000ull);
+      // the consumers' generic reads of the slot precede this async-proxy write
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    sm.seq[slot] = j;
+    PROGRESS(2, j);
+    PROGRESS(3, op_no);
+    const Layer& L = O.L[r.li];
+    const uint4* src = L.planes + p * L.pstride + ((long long)r.w * L.n_tiles + (r.t0 - L.tile_off)) * (kTileBytes / 16);
+    mbar_expect_tx(&sm.full[slot], (unsigned)r.nt * kTileBytes);
+    tma_load_1d(const_cast<unsigned char*>(dyn0) + sm.slot_off[slot], src, (unsigned)r.nt * kTileBytes, &sm.full[slot]);
+    ++j;
+  };
+  for (int step = 0; step < n_steps; ++step) {
+    if (lane == 0) SPIN_UNTIL_NS(sm.step_ready >= step + 1, "producer step", step, 0, 12000000000ull);
+    __syncwarp();
+    __threadfence_block();
+    const ECtl& C = sm.ctl;
+    for (int si = 0; si < P.n_stages; ++si) {
+      const int2 st = P.stages[si];
+      if (st.x != ST_OP) continue;
+      const int nw4 = (int)(sizeof(Op) / 16);
+      const int4* src = reinterpret_cast<const int4*>(P.ops + st.y);
+      int4* dst = reinterpret_cast<int4*>(&sm.pop);
+      for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
+      __syncwarp();
+      build_work_warp(sm.pop, C, cta, G, sm.pw);
+      __syncwarp();
+      // the next op's base planes -> L2 while this op streams through the ring
+      {
+        int nsi = si + 1;
+        while (nsi < P.n_stages && P.stages[nsi].x != ST_OP) ++nsi;
+        if (nsi < P.n_stages) {
+          const int4* src2 = reinterpret_cast<const int4*>(P.ops + P.stages[nsi].y);
+          int4* dst2 = reinterpret_cast<int4*>(&sm.pop2);
+          for (int q = lane; q < nw4; q += 32) dst2[q] = __ldg(src2 + q);
+          __syncwarp();
+          build_work_warp(sm.pop2, C, cta, G, sm.pw2);
+          __syncwarp();
+          prefetch_work_l2(sm.pop2, sm.pw2, 0);
+        }
+      }
+      if (lane == 0) {
+        const Op& O = sm.pop;
+        build_runs(O, sm.pw, sm.pruns);
+        const RunList& R = sm.pruns;
+        for (int r = 0; r < R.n; ++r)
+          for (int p = 0; p < sm.pw.nb[R.r[r].li]; ++p) issue(O, R.r[r], p);
+        bool may_extra = false;
+        if (C.mode == MODE_DYNAMIC && !C.force)
+          for (int li = 0; li < O.n_layers; ++li) may_extra |= O.L[li].sentinel == 0 && O.L[li].l < O.L[li].h;
+        if (may_extra && R.n > 0) {
+          SPIN_UNTIL_NS(sm.dec_op >= op_no + 1, "producer decision", op_no, 0, 12000000000ull);
+          __threadfence_block();
+          for (int r = R.n - 1; r >= 0; --r) {
+            const int li = R.r[r].li;
+            const int fin = sm.dec_fin[op_no & 1][li];
+            for (int p = sm.pw.nb[li]; p < fin; ++p) issue(O, R.r[r], p);
+          }
+        }
+      }
+      __syncwarp();
+      ++op_no;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -817,126 +1114,117 @@ __device__ __noinline__ void attn_emit_head(const Prog& P, const ECtl& C, int in
   }
 }
 
+// Unit = (query head h, chunk of <= kAttnChunkE positions). K/V rows of the
+// chunk are staged in shared memory (the LUT region is free here); chunk
+// partials (m, l, o) are merged by the last unit of the head. The unit that
+// holds position t of the first head of each KV group appends k_t / v_t.
+constexpr int kAttnChunkE = 32;   // K/V staging stays inside the LUT region
+
 __device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, float* sh, int cta, int G, int* s_last) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t = C.pos, n = t + 1;
-  const int hd = P.hd, KV = P.KV, qh = P.H / P.KV, half = hd / 2;
-  int nch = min((n + 15) / 16, max(1, G / KV));
-  nch = min(nch, P.attn_max_chunks);
-  const int clen = (n + nch - 1) / nch;
-  nch = (n + clen - 1) / clen;
-  const int units = KV * nch;
+  const int hd = P.hd, H = P.H, qh = P.H / P.KV, half = hd / 2;
+  const int nch = (n + kAttnChunkE - 1) / kAttnChunkE;
+  const int units = H * nch;
   const float scale = 1.0f / sqrtf((float)hd);
   const float* cs = P.cosv + (size_t)t * half;
   const float* sn = P.sinv + (size_t)t * half;
   float* kc = P.kc[b];
   float* vc = P.vc[b];
-  // smem: q[qh][hd] kt[hd] vt[hd] K[32][hd] V[32][hd] sc[qh][32] o[qh][hd] m[qh] l[qh] al[qh]
-  float* q = sh;
-  float* kt = q + qh * hd;
-  float* vt = kt + hd;
-  float* Ks = vt + hd;
-  float* Vs = Ks + 32 * hd;
-  float* sc = Vs + 32 * hd;
-  float* o = sc + qh * 32;
-  float* mm = o + qh * hd;
-  float* ll = mm + qh;
-  float* al = ll + qh;
   const int inst = 4 * b + 1;
+  // G^T blocks the attention output feeds (o-proj estimators) -> L2
+  if (warp == NW - 1) prefetch_feeds_l2(P, C, inst, P.d, cta, G);
+  // smem: Ks[64][hd] Vs[64][hd] q[hd] kt[hd] vt[hd] sc[64] o[hd] red[NW][hd]
+  float* Ks = sh;
+  float* Vs = Ks + kAttnChunkE * hd;
+  float* q = Vs + kAttnChunkE * hd;
+  float* kt = q + hd;
+  float* vt = kt + hd;
+  float* sc = vt + hd;
+  float* stat = sc + kAttnChunkE;          // [0] m, [1] l
   for (int u = cta; u < units; u += G) {
-    const int g = u / nch, ch = u % nch;
-    const int s0 = ch * clen, s1 = min(n, s0 + clen);
-    __syncthreads();
-    for (int idx = tid; idx < qh * hd; idx += NT) {
-      const int hq = idx / hd, i = idx - hq * hd;
-      q[idx] = rope_at(P.qkv + (g * qh + hq) * hd, i, hd, cs, sn);
-      o[idx] = 0.f;
-    }
+    const int h = u / nch, ch = u - h * nch;
+    const int g = h / qh;
+    const int s0 = ch * kAttnChunkE, s1 = min(n, s0 + kAttnChunkE), ns = s1 - s0;
+    const bool has_t = s1 == n;
+    CSYNC();
+    // q (RoPE), and the new k / v when this chunk holds position t
     for (int i = tid; i < hd; i += NT) {
-      kt[i] = rope_at(P.qkv + P.d + g * hd, i, hd, cs, sn);
-      vt[i] = __ldcg(P.qkv + P.d + P.dkv + g * hd + i);
+      q[i] = rope_at(P.qkv + h * hd, i, hd, cs, sn);
+      if (has_t) {
+        kt[i] = rope_at(P.qkv + P.d + g * hd, i, hd, cs, sn);
+        vt[i] = __ldcg(P.qkv + P.d + P.dkv + g * hd + i);
+      }
     }
-    if (tid < qh) { mm[tid] = -CUDART_INF_F; ll[tid] = 0.f; }
-    __syncthreads();
-    if (s1 == n) {       // the unit holding position t appends it to the cache (runtime.py:355-356)
+    // K / V rows of the chunk (positions < t from the cache), 16-byte loads
+    const int nv = hd / 4;
+    for (int idx = tid; idx < (ns - (has_t ? 1 : 0)) * nv; idx += NT) {
+      const int sp = idx / nv, c4 = idx - sp * nv;
+      const size_t off = (size_t)(s0 + sp) * P.dkv + g * hd + 4 * c4;
+      reinterpret_cast<float4*>(Ks + sp * hd)[c4] = __ldcg(reinterpret_cast<const float4*>(kc + off));
+      reinterpret_cast<float4*>(Vs + sp * hd)[c4] = __ldcg(reinterpret_cast<const float4*>(vc + off));
+    }
+    CSYNC();
+    if (has_t) {
       for (int i = tid; i < hd; i += NT) {
-        kc[(size_t)t * P.dkv + g * hd + i] = kt[i];
-        vc[(size_t)t * P.dkv + g * hd + i] = vt[i];
+        Ks[(ns - 1) * hd + i] = kt[i];
+        Vs[(ns - 1) * hd + i] = vt[i];
+        if (h % qh == 0) {                         // runtime.py:355-356 (KV append)
+          kc[(size_t)t * P.dkv + g * hd + i] = kt[i];
+          vc[(size_t)t * P.dkv + g * hd + i] = vt[i];
+        }
       }
+      CSYNC();
     }
-    for (int sb = s0; sb < s1; sb += 32) {
-      const int ns = min(32, s1 - sb);
-      for (int idx = tid; idx < ns * hd; idx += NT) {
-        const int sp = idx / hd, i = idx - sp * hd;
-        const int s = sb + sp;
-        if (s == t) { Ks[idx] = kt[i]; Vs[idx] = vt[i]; }
-        else {
-          Ks[idx] = __ldcg(kc + (size_t)s * P.dkv + g * hd + i);
-          Vs[idx] = __ldcg(vc + (size_t)s * P.dkv + g * hd + i);
-        }
-      }
-      __syncthreads();
-      for (int pr = warp; pr < qh * ns; pr += NW) {
-        const int hq = pr / ns, sp = pr - hq * ns;
-        float a = 0.f;
-        for (int i = lane; i < hd; i += 32) a += q[hq * hd + i] * Ks[sp * hd + i];
-        a = wsum(a);
-        if (lane == 0) sc[hq * 32 + sp] = a * scale;
-      }
-      __syncthreads();
-      if (warp < qh) {
-        const int hq = warp;
-        const float v = lane < ns ? sc[hq * 32 + lane] : -CUDART_INF_F;
-        float mx = v;
+    // scores (runtime.py:358): one warp per position
+    for (int sp = warp; sp < ns; sp += NW) {
+      float a = 0.f;
+      for (int i = lane; i < hd; i += 32) a += q[i] * Ks[sp * hd + i];
+      a = wsum(a);
+      if (lane == 0) sc[sp] = a * scale;
+    }
+    CSYNC();
+    // softmax over the chunk (runtime.py:359-361), warp 0
+    if (warp == 0) {
+      float mx = -CUDART_INF_F;
+      for (int sp = lane; sp < ns; sp += 32) mx = fmaxf(mx, sc[sp]);
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-        const float mnew = fmaxf(mm[hq], mx);
-        const float p = lane < ns ? expf(v - mnew) : 0.f;
-        const float ps = wsum(p);
-        if (lane < ns) sc[hq * 32 + lane] = p;
-        if (lane == 0) {
-          const float a = expf(mm[hq] - mnew);
-          al[hq] = a;
-          ll[hq] = ll[hq] * a + ps;
-          mm[hq] = mnew;
-        }
+      for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      float l = 0.f;
+      for (int sp = lane; sp < ns; sp += 32) {
+        const float e = expf(sc[sp] - mx);
+        sc[sp] = e;
+        l += e;
       }
-      __syncthreads();
-      for (int idx = tid; idx < qh * hd; idx += NT) {
-        const int hq = idx / hd, i = idx - hq * hd;
-        float acc = o[idx] * al[hq];
-        for (int sp = 0; sp < ns; ++sp) acc += sc[hq * 32 + sp] * Vs[sp * hd + i];
-        o[idx] = acc;
-      }
-      __syncthreads();
+      l = wsum(l);
+      if (lane == 0) { stat[0] = mx; stat[1] = l; }
+    }
+    CSYNC();
+    // o = sum_s p_s v_s (runtime.py:362)
+    for (int i = tid; i < hd; i += NT) {
+      float acc = 0.f;
+      for (int sp = 0; sp < ns; ++sp) acc += sc[sp] * Vs[sp * hd + i];
+      if (nch == 1) P.attn[h * hd + i] = acc / stat[1];
+      else P.attn_part[((size_t)h * P.attn_max_chunks + ch) * (hd + 2) + i] = acc;
     }
     if (nch == 1) {
-      for (int idx = tid; idx < qh * hd; idx += NT) {
-        const int hq = idx / hd;
-        P.attn[g * qh * hd + idx] = o[idx] / ll[hq];
-      }
-      __syncthreads();
-      if (P.attn_emit) for (int hq = 0; hq < qh; ++hq) attn_emit_head(P, C, inst, g * qh + hq);
+      CSYNC();
+      if (P.attn_emit) attn_emit_head(P, C, inst, h);
       continue;
     }
-    for (int idx = tid; idx < qh * hd; idx += NT) {
-      const int hq = idx / hd, i = idx - hq * hd;
-      P.attn_part[((size_t)(g * qh + hq) * P.attn_max_chunks + ch) * (hd + 2) + i] = o[idx];
-    }
-    if (tid < qh) {
-      float* pp = P.attn_part + ((size_t)(g * qh + tid) * P.attn_max_chunks + ch) * (hd + 2);
-      pp[hd] = mm[tid];
-      pp[hd + 1] = ll[tid];
+    if (tid == 0) {
+      float* pp = P.attn_part + ((size_t)h * P.attn_max_chunks + ch) * (hd + 2);
+      pp[hd] = stat[0];
+      pp[hd + 1] = stat[1];
     }
     __threadfence();
-    __syncthreads();
-    if (tid == 0) *s_last = atomicAdd(P.attn_cnt + g, 1u) == (unsigned)nch - 1;
-    __syncthreads();
+    CSYNC();
+    if (tid == 0) *s_last = atomicAdd(P.attn_cnt + h, 1u) == (unsigned)nch - 1;
+    CSYNC();
     if (!*s_last) continue;
     __threadfence();
-    for (int idx = tid; idx < qh * hd; idx += NT) {
-      const int hq = idx / hd, i = idx - hq * hd;
-      const float* base = P.attn_part + (size_t)(g * qh + hq) * P.attn_max_chunks * (hd + 2);
+    const float* base = P.attn_part + (size_t)h * P.attn_max_chunks * (hd + 2);
+    for (int i = tid; i < hd; i += NT) {
       float M = -CUDART_INF_F;
       for (int c = 0; c < nch; ++c) M = fmaxf(M, __ldcg(base + c * (hd + 2) + hd));
       float Ls = 0.f, acc = 0.f;
@@ -945,11 +1233,11 @@ __device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, flo
         Ls += __ldcg(base + c * (hd + 2) + hd + 1) * e;
         acc += __ldcg(base + c * (hd + 2) + i) * e;
       }
-      P.attn[g * qh * hd + idx] = acc / Ls;
+      P.attn[h * hd + i] = acc / Ls;
     }
-    if (tid == 0) P.attn_cnt[g] = 0u;
-    __syncthreads();
-    if (P.attn_emit) for (int hq = 0; hq < qh; ++hq) attn_emit_head(P, C, inst, g * qh + hq);
+    if (tid == 0) P.attn_cnt[h] = 0u;
+    CSYNC();
+    if (P.attn_emit) attn_emit_head(P, C, inst, h);
   }
 }
 
@@ -1001,9 +1289,9 @@ __device__ __noinline__ void head_stage(const Prog& P, const ECtl& C, Smem& sm, 
     if (lane == 0) P.logits[v] = a * inv;
   }
   __threadfence();
-  __syncthreads();
+  CSYNC();
   if (tid == 0) sm.last = atomicAdd(P.head_cnt, 1u) == (unsigned)G - 1;
-  __syncthreads();
+  CSYNC();
   if (!sm.last) return;
   __threadfence();
   float best = -CUDART_INF_F;
@@ -1019,7 +1307,7 @@ __device__ __noinline__ void head_stage(const Prog& P, const ECtl& C, Smem& sm, 
     if (zb > best || (zb == best && ib < bi)) { best = zb; bi = ib; }
   }
   if (lane == 0) { sm.head_v[warp] = best; sm.head_i[warp] = bi; }
-  __syncthreads();
+  CSYNC();
   if (tid == 0) {
     for (int w = 1; w < NW; ++w)
       if (sm.head_v[w] > best || (sm.head_v[w] == best && sm.head_i[w] < bi)) { best = sm.head_v[w]; bi = sm.head_i[w]; }
@@ -1067,55 +1355,80 @@ __device__ __noinline__ void begin_stage(const Prog& P, const ECtl& C, int cta, 
 // The kernel: n_steps decode steps (greedy token feedback on the device when
 // n_steps > 1; the host writes the token / mode of a single step).
 // ---------------------------------------------------------------------------
-extern "C" __global__ void __launch_bounds__(NT, 1) engine_kernel(const Prog Pk, int n_steps) {
+extern "C" __global__ void __launch_bounds__(NTB, 1) engine_kernel(const Prog Pk, int n_steps) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-  if (threadIdx.x == 0) sm.prog = Pk;
+  const int cta = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
+  if (tid == 0) {
+    sm.prog = Pk;
+    sm.work[0].valid = 0;
+    sm.work[1].valid = 0;
+    sm.dec_op = 0;
+    sm.step_ready = 0;
+    // ring slots: below the LUT (after Smem) and above its zero row
+    const uint32_t base = smem_u32(smem_raw);
+    uint32_t lo = (base + (uint32_t)sizeof(Smem) + 1023u) & ~1023u;
+    int n = 0;
+    while (lo + kSlotBytes <= kLut && n < kMaxSlots) { sm.slot_off[n++] = lo - base; lo += kSlotBytes; }
+    uint32_t hi = kLut + 256 * 256 + 256;
+    while (Pk.upper_slots && hi + kSlotBytes <= base + (uint32_t)Pk.smem_dyn && n < kMaxSlots) {
+      sm.slot_off[n++] = hi - base;
+      hi += kSlotBytes;
+    }
+    if (n < kMaxSlots) __trap();        // host sizing guarantees kMaxSlots ring slots
+    sm.n_slots = n;
+    for (int q = 0; q < n; ++q) {
+      mbar_init(&sm.full[q], 1);
+      mbar_init(&sm.empty[q], kSlotTiles);
+      sm.seq[q] = -1;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
   const Prog& P = sm.prog;
-  float* lut = reinterpret_cast<float*>(smem_raw + (kLutA - sbase));
+  if (tid >= NT) {                        // TMA producer warp
+    producer(P, sm, cta, G, n_steps);
+    return;
+  }
+  float* lut = reinterpret_cast<float*>(smem_raw + (kLut - smem_u32(smem_raw)));
   __shared__ int s_last;
-  const int cta = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
-  if (tid == 0) { sm.work[0].valid = 0; sm.work[1].valid = 0; }
-  int wi = 0;
+  int wi = 0, op_no = 0, j_op = 0;
   // barrier epochs continue from previous launches (counter = G x stages so far)
   const unsigned long long e0 = ld_acq64(P.bar) / (unsigned long long)G;   // stages completed before
   unsigned long long k = 0;     // stages completed in this launch
   ECtl& C = sm.ctl;
-  __syncthreads();
   for (int step = 0; step < n_steps; ++step) {
     for (int si = 0; si < P.n_stages; ++si) {
       const int2 st = P.stages[si];
       const bool wait = k > 0;
       const unsigned long long target = e0 + k;        // epoch of the previous stage
+      if (tid == 0) PROGRESS(0, (step << 16) | si);
       if (st.x == ST_OP) {
-        // next op stage of this step (ring run-ahead target)
         int nsi = si + 1;
         while (nsi < P.n_stages && P.stages[nsi].x != ST_OP) ++nsi;
         const bool has_next = nsi < P.n_stages;
-        // descriptors to shared memory (the current one may already be there)
-        {
+        const bool have_desc = sm.work[wi].valid != 0;
+        if (!have_desc) {
           const int nw4 = (int)(sizeof(Op) / 16);
           const int4* src = reinterpret_cast<const int4*>(P.ops + st.y);
           int4* dst = reinterpret_cast<int4*>(&sm.op[wi]);
-          if (!sm.work[wi].valid)
-            for (int q = tid; q < nw4; q += NT) dst[q] = __ldg(src + q);
-          if (has_next) {
-            const int4* src2 = reinterpret_cast<const int4*>(P.ops + P.stages[nsi].y);
-            int4* dst2 = reinterpret_cast<int4*>(&sm.op[wi ^ 1]);
-            for (int q = tid; q < nw4; q += NT) dst2[q] = __ldg(src2 + q);
-          }
-          __syncthreads();
+          for (int q = tid; q < nw4; q += NT) dst[q] = __ldg(src + q);
+          CSYNC();
         }
-        op_stage(P, C, sm.op[wi], sm.work[wi], has_next ? &sm.op[wi ^ 1] : nullptr, &sm.work[wi ^ 1], sm, cta, G,
-                 target, wait, P.dbg ? P.dbg + ((size_t)si * G + cta) * 8 : nullptr);
+        j_op += op_stage(P, C, sm.op[wi], sm.work[wi], has_next ? &sm.op[wi ^ 1] : nullptr, &sm.work[wi ^ 1],
+                         has_next ? P.ops + P.stages[nsi].y : nullptr, sm, cta, G, target, wait,
+                         P.dbg ? P.dbg + ((size_t)si * G + cta) * 8 : nullptr, op_no, j_op);
+        ++op_no;
         wi ^= 1;
       } else {
         if (wait) bar_wait(P, target);
         if (P.dbg && tid == 0) P.dbg[((size_t)si * G + cta) * 8] = gclock();
         if (st.x == ST_BEGIN) {
           read_ctl(P, C);
+          if (tid == 0) {
+            __threadfence_block();
+            sm.step_ready = step + 1;                   // the producer may stream this step
+          }
           begin_stage(P, C, cta, G);
         } else if (st.x == ST_ATTN) {
           attn_stage(P, C, st.y, lut, cta, G, &s_last);

@@ -27,7 +27,8 @@ def line_map(lib: str, kernel: str) -> dict:
     m, cur, inside = {}, None, False
     for ln in out.splitlines():
         if ln.startswith(".text."):
-            inside = ln.strip() == f".text.{kernel}:"
+            name = ln.strip()[6:-1]
+            inside = name == kernel or (kernel in name and not name.startswith("$"))
             continue
         if not inside:
             continue
@@ -45,7 +46,7 @@ def main():
     rep, lib, kernel = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
     txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
-                          "-k", kernel], capture_output=True, text=True).stdout
+                          "-k", "regex:" + kernel], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hi = next(i for i, r in enumerate(rows) if "Address" in r)
     hdr = rows[hi]
