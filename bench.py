@@ -38,7 +38,7 @@ PROMPT = 16
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=256)
+    ap.add_argument("--steps", type=int, default=128)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llama3_8b", choices=["llama3_8b", "llama2_7b", "cfg1", "llama2_70b_slice"])
@@ -230,9 +230,56 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def step_bytes(cfg, store, plan, bits_row, ids, g_bytes_per_el, pos):
+    """Algorithmic HBM bytes of one decode step at the realized bits (SURVEY
+    8d): selected planes rows*cols*b/8 + (lo, span) 8*rows + the estimator's
+    G (g_bytes * k * cols per dynamic layer) + KV cache read/append
+    (2 * n_blocks * (pos+1) * d_kv * 4) + lm_head (vocab * d * 4) + embedding
+    row. Activations (x, y: a few KB per layer) are counted as 4*(rows+cols)."""
+    by = 0.0
+    for i, lid in enumerate(ids):
+        rows, cols = store.layers[lid].shape
+        b = int(bits_row[i])
+        by += rows * cols * b / 8 + 8 * rows + 4 * (rows + cols)
+        pl = plan.layers[lid]
+        if pl.estimator is not None and np.isfinite(pl.T):
+            by += g_bytes_per_el * pl.estimator.kind.k * cols
+    d_kv = cfg.kv_heads * (cfg.d_model // cfg.n_heads)
+    by += 2 * cfg.n_blocks * (pos + 1) * d_kv * 4
+    by += cfg.vocab * cfg.d_model * 4 + cfg.d_model * 4
+    return by
+
+
+def op_stage_times(eng, store, plan, ids, g_bytes):
+    """Per-op critical-path times (us) and GB/s of the last step, from the
+    engine's per-stage %globaltimer stamps (session built with DPQ_DEBUG_TIMES)."""
+    import ctypes as C
+    from paper_2508_06041_b200 import _lib
+    n = C.c_int()
+    _lib.call("dpq_session_engine_stages", eng._h, C.byref(n), None, None)
+    kinds = np.zeros(n.value, dtype=np.int32)
+    idx = np.zeros(n.value, dtype=np.int32)
+    _lib.call("dpq_session_engine_stages", eng._h, C.byref(n), C.c_void_p(kinds.ctypes.data),
+              C.c_void_p(idx.ctypes.data))
+    per = C.c_int()
+    _lib.call("dpq_session_debug_times", eng._h, None, 0, C.byref(per))
+    G = per.value // 8
+    buf = np.zeros(n.value * G * 8, dtype=np.uint64)
+    _lib.call("dpq_session_debug_times", eng._h, C.c_void_p(buf.ctypes.data), buf.size, C.byref(per))
+    st = buf.reshape(n.value, G, 8).astype(np.float64)
+    last_end = st[..., 7].max(axis=1)
+    crit = np.diff(np.concatenate([[st[0, :, 0].min()], last_end])) / 1e3
+    bits = [eng.trace.steps[-1].bits[l] for l in ids]
+    by = op_bytes(store, plan, bits, ids, g_bytes)
+    op_t = crit[kinds == 1]
+    return op_t, by[:len(op_t)], crit
+
+
 def run_ours(args):
+    import ctypes as C
     import torch
     import torch.distributed as dist
+    from paper_2508_06041_b200 import _lib
     from paper_2508_06041_b200 import runtime as R
     from paper_2508_06041_b200 import synth
 
@@ -251,20 +298,22 @@ def run_ours(args):
     calib = np.random.default_rng(7).integers(0, cfg.vocab, 48)
     synth.calibrate_thresholds(weights, store, plan, calib, high_rate=high, g_dtype=args.g_dtype)
     build_s = time.perf_counter() - t_build
+    g_bytes = {"f32": 4, "f16": 2, "e4m3": 1}[args.g_dtype]
 
     ids = store.ordered_ids()
     eng = R.DecodeEngine(weights, store, plan, g_dtype=args.g_dtype)
+    engine_kind = _lib.load().dpq_session_is_persistent(eng._h)
     stream = torch.cuda.Stream()
+    sp = C.c_void_p(stream.cuda_stream)
     prompt = np.random.default_rng(11 + rank).integers(0, cfg.vocab, PROMPT)
     eng.prefill(prompt)
-    from paper_2508_06041_b200 import _lib
-    import ctypes as C
-    sp = C.c_void_p(stream.cuda_stream)
     total = args.warmup + args.steps
-    if PROMPT + total + 4 > cfg.seq_cap:
+    if PROMPT + total + 40 > cfg.seq_cap:
         raise SystemExit("steps exceed seq_cap")
+    # warm-up: W device-loop steps (one launch)
     _lib.call("dpq_session_launch_steps", eng._h, args.warmup, sp)
     stream.synchronize()
+    pos0 = eng._pos + args.warmup
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
     clocks.start()
@@ -272,6 +321,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     e0.record(stream)
+    # timed: K greedy decode steps, ONE launch of the persistent engine kernel
     _lib.call("dpq_session_launch_steps", eng._h, args.steps, sp)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -286,33 +336,32 @@ def run_ours(args):
         ms = float(t.item())
     ms_per_step = ms / args.steps
     value = world * 1000.0 / ms_per_step
-    eff_bits = float(np.mean([s.effective_bits for s in eng.trace.steps[-args.steps:]]))
-    high_frac = float(np.mean([[s.bits[l] == plan.layers[l].pair[1] for l in ids]
-                               for s in eng.trace.steps[-args.steps:]]))
-
-    # ---- roofline of the dominant kernel: per-launch CUDA-event times of the
-    # fused selector+GEMV ops on one eager step (profile_ops)
-    n_ops = 4 * cfg.n_blocks
-    op_ms = np.zeros(n_ops, dtype=np.float32)
-    nout = C.c_int()
-    tok = int(np.random.default_rng(3).integers(0, cfg.vocab))
-    reps = []
-    for rep in range(3):
-        _lib.call("dpq_session_profile_ops", eng._h, tok, 1, C.c_void_p(op_ms.ctypes.data), n_ops, C.byref(nout))
-        eng._pos += 1
-        eng.trace.estimator_ops += eng._ops_per_step
-        eng._sync_trace()
-        bits_row = [eng.trace.steps[-1].bits[l] for l in ids]
-        by = op_bytes(store, plan, bits_row, ids, {"f32": 4, "f16": 2, "e4m3": 1}[args.g_dtype])
-        reps.append((op_ms[:nout.value].copy(), by[:nout.value]))
-    op_t = np.mean([r[0] for r in reps], axis=0)
-    op_b = np.mean([r[1] for r in reps], axis=0)
-    achieved = float(op_b.sum() / (op_t.sum() * 1e-3) / 1e9)
+    recs = eng.trace.steps[-args.steps:]
+    eff_bits = float(np.mean([s.effective_bits for s in recs]))
+    high_frac = float(np.mean([[s.bits[l] == plan.layers[l].pair[1] for l in ids] for s in recs]))
+    # algorithmic bytes of the timed steps (realized bits per step, KV growing)
+    alg = sum(step_bytes(cfg, store, plan, [r.bits[l] for l in ids], ids, g_bytes, pos0 + i)
+              for i, r in enumerate(recs))
+    achieved = alg / (ms * 1e-3) / 1e9
     peak, peak_kind = measured_peak()
-    gemv_share = float(op_t.sum())
 
-    # ---- selector overhead: static sentinel plans at l and h, interpolated at
-    # the realized effective bits (same per-layer pairs, no estimators)
+    # per-op GB/s (critical path from stage stamps) on a separate instrumented session
+    os.environ["DPQ_DEBUG_TIMES"] = "1"
+    eng2 = R.DecodeEngine(weights, store, plan, g_dtype=args.g_dtype)
+    del os.environ["DPQ_DEBUG_TIMES"]
+    eng2.prefill(prompt)
+    eng2.decode_greedy(8)
+    op_t, op_b, crit = op_stage_times(eng2, store, plan, ids, g_bytes)
+    eng2.close()
+    per_op = {}
+    for nm, i0 in (("qkv", 0), ("o", 1), ("upgate", 2), ("down", 3)):
+        t = op_t[i0::4].sum()
+        b = op_b[i0::4].sum()
+        per_op[nm] = {"us": float(t / (len(op_t) // 4)), "GBps": float(b / (t * 1e-6) / 1e9)}
+    gemv_gbs = float(op_b.sum() / (op_t.sum() * 1e-6) / 1e9)
+
+    # selector overhead: sentinel-static plans at l and h, interpolated at the
+    # realized effective bits (same engine, same decode loop)
     overhead = None
     static_ms = {}
     if not args.skip_static:
@@ -336,7 +385,7 @@ def run_ours(args):
             t_static = static_ms[bl[0]]
         overhead = (ms_per_step - t_static) / t_static
 
-    # ---- e2e through the public step API: host token in, host logits out
+    # e2e through the public step API: host token in, host logits out
     n_e2e = min(32, cfg.seq_cap - eng._pos - 1)
     toks = np.random.default_rng(5).integers(0, cfg.vocab, n_e2e)
     torch.cuda.synchronize()
@@ -349,34 +398,37 @@ def run_ours(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic: random-init Llama-3-8B-shaped weights (W ~ N(0,1/cols)), random tokens",
+            "data": "synthetic: random-init weights (W ~ N(0,1/cols), init_model law), random prompt tokens",
             "config": {"workload": f"{args.config}-shaped batch-1 greedy decode, DP plan {args.target}-bit "
-                                   f"target, (3,4) pairs, k=64 projection selector ({args.g_dtype} G)",
+                                   f"target, ({pairs[ids[0]][0]},{pairs[ids[0]][1]}) pairs, k=64 projection "
+                                   f"selector ({args.g_dtype} G)",
                        "n_blocks": cfg.n_blocks, "d_model": cfg.d_model, "n_heads": cfg.n_heads,
                        "n_kv_heads": cfg.kv_heads, "d_ff": cfg.d_ff, "vocab": cfg.vocab,
                        "n_bits": n_bits, "b_min": b_min, "prompt": PROMPT,
                        "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "l2_policy": "weights (3.5 GB of bitplanes) >> 126 MB L2; no flush needed",
+                       "engine": {2: "persistent TMA engine", 1: "persistent flag kernel", 0: "multi-kernel"}.get(
+                           engine_kind, str(engine_kind)),
+                       "l2_policy": "weights (3.0-3.6 GB of bitplanes per step) >> 126 MB L2; no flush needed",
                        "realized_effective_bits": eff_bits, "high_decision_rate": high_frac,
                        "selector_overhead": overhead, "static_ms_per_step": static_ms,
-                       "build_s": build_s},
+                       "per_op": per_op, "gemv_stage_GBps": gemv_gbs, "build_s": build_s},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "op_kernel (fused selector + bitplane GEMV)",
-                         "ops_per_step": int(nout.value), "op_ms_per_step": gemv_share,
-                         "op_bytes_per_step": float(op_b.sum())},
+                         "kernel": "engine_kernel (whole decode step: fused selector + bitplane GEMVs, "
+                                   "attention, lm_head; one launch per timed region)",
+                         "alg_bytes_per_step": alg / args.steps},
             "clocks": clk,
-            "gpu_launches": int(args.steps * (2 + 5 * cfg.n_blocks)),
+            "gpu_launches": 1,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 12,
                     "d2h_bytes_per_step": 4 * cfg.vocab}}
     if rank == 0 and not args.no_cpu_baseline and host:
         v, sample = cpu_slice_oracle(cfg, host, plan, weights)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                                 "sample": sample}
-    traffic_path = os.path.join(ROOT, "profiles", "op_kernel_traffic.json")
+    traffic_path = os.path.join(ROOT, "profiles", "engine_traffic.json")
     if os.path.exists(traffic_path):
         try:
-            line["roofline"]["traffic"] = json.load(open(traffic_path)).get("bytes_per_launch")
+            line["roofline"]["traffic"] = json.load(open(traffic_path)).get("bytes_per_step")
         except Exception:
             pass
     if rank == 0:
