@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libdpq_b200.so")
-SOURCES = ["dpq_capi.cu", "dpq_kernels.cu", "dpq_common.cuh", "dpq_session.inc"]
+SOURCES = ["dpq_capi.cu", "dpq_kernels.cu", "dpq_engine.cu", "dpq_common.cuh", "dpq_session.inc"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -40,6 +40,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-shared", "-cudart", "static", "-diag-suppress", "550,177",
            "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp",
            os.path.join(CSRC, "dpq_capi.cu")]
+    # diagnostics builds only (e.g. -DDPQ_PROFILE_WARPS for tools/engine_profile.py)
+    cmd[1:1] = os.environ.get("DPQ_BUILD_DEFINES", "").split()
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

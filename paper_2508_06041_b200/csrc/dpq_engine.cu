@@ -42,6 +42,7 @@ constexpr int kSlotBytes = kSlotTiles * 2048;
 constexpr int kMaxSlots = 8;       // ring slots (power of two: index arithmetic by shifts)
 constexpr int kMaxRuns = 96;       // (layer, window, <= 8 tiles) runs per op per CTA
 constexpr int kMaxTiles = 128;     // tiles (groups) per op per CTA (parked base sums)
+constexpr int kDbgRec = 128;   // debug record per (stage, CTA): [0,8) phase stamps, [8,88) 5 per consumer warp, [88,96) producer, [96,128) clock64 sub-stamps
 constexpr double kFxSum = 4294967296.0;       // 2^32: sum v
 constexpr double kFxSq = 16777216.0;          // 2^24: sum v^2
 
@@ -128,7 +129,7 @@ struct Prog {
   struct ECtl* ctl;
   int smem_dyn;             // dynamic shared memory bytes of the launch
   int upper_slots;          // ring slots above the LUT too
-  unsigned long long* dbg; // optional per-stage timestamps [stages][grid][8]
+  unsigned long long* dbg; // optional per-stage timestamps [stages][grid][kDbgRec]
 };
 
 struct ECtl {
@@ -182,6 +183,11 @@ __device__ __forceinline__ unsigned long long gclock() {
 // a hang). No call, so nothing is spilled around the polling loops.
 __device__ unsigned long long* g_diag = nullptr;
 __device__ volatile int* g_prog = nullptr;     // optional mapped progress words [grid][4] (debug)
+#ifdef DPQ_PROFILE_WARPS
+#define CSTAMP(st, i) do { if (st) (st)[96 + (i)] = clock64(); } while (0)
+#else
+#define CSTAMP(st, i) do { } while (0)
+#endif
 #ifdef DPQ_ENGINE_TRACE
 #define PROGRESS(slot, v) do { if (g_prog) g_prog[blockIdx.x * 4 + (slot)] = (v); } while (0)
 #define WSTATE(v) do { if (lane == 0) sm.wstate[warp] = (v); } while (0)
@@ -340,12 +346,14 @@ struct Smem {
   int dec_fin[2][kMaxOpLayers];      // published final bits (op counter parity)
   float xw[kWinCols];
   float scale, sx;         // op input scale (1/rms or 1) and sum of raw input
-  int last;
+  int last;                // base FIFO items of the current op (op stage) / last-arriver flag
+  int n_ext_items, t_ext;  // extra FIFO items / extra tasks of the current op (after the decision)
   double red[32];
   float head_v[NW];
   int head_i[NW];
   float sbuf[kMaxTiles][32];         // base-pass S of tiles whose layer has extra planes
   short fo_bo[kMaxRuns], fo_eo[kMaxRuns], fo_xt[kMaxRuns];
+  int vtile[kMaxTiles];              // reduce: emit tile of the CTA's i-th unit (values in sbuf)
 };
 
 __device__ __forceinline__ int layer_of(const Op& O, int t) {
@@ -451,106 +459,98 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 // Vector emission: statistics + estimator feeds of one 32-row tile (a warp;
 // lane = row). v = value (0 for padding rows).
 // ---------------------------------------------------------------------------
-// Pull everything emit_tile(inst, tile) will read (feed descriptors, G^T
-// blocks) into L1 ahead of the value it depends on.
-__device__ __forceinline__ void emit_prefetch(const Prog& P, int inst, int tile) {
-  const int lane = threadIdx.x & 31;
-  for (int fi = P.feed_begin[inst]; fi < P.feed_begin[inst + 1]; ++fi) {
-    const Feed* Fp = P.feeds + fi;
-    const uint4* Gt = Fp->Gt;
-    if (!Gt) continue;
-    const int nsub = Fp->kpad / 64, per = Fp->f16 ? 256 : 512;
-    const uint4* blk = Gt + (size_t)tile * nsub * per + lane;
-    for (int i = 0; i < nsub * per / 32; ++i) l1_prefetch(blk + 32 * i);
-  }
-}
+__device__ unsigned long long* g_emit_stamp = nullptr;   // profiling hook (unused by the engine)
 
-__device__ unsigned long long* g_emit_stamp = nullptr;   // profiling: [8] stamps of one emit
-__device__ __noinline__ void emit_tile(const Prog& P, const ECtl& C, int inst, int tile, float v) {
+// Statistics of one 32-row tile of vector instance inst: sum v, sum v^2.
+__device__ __forceinline__ void emit_stats(const Prog& P, const ECtl& C, int inst, float v) {
   const int lane = threadIdx.x & 31;
-  unsigned long long* es = (g_emit_stamp && blockIdx.x == 0 && threadIdx.x == 0) ? g_emit_stamp : nullptr;
-  if (es) es[0] = gclock();
-  const int cur = C.n_steps_done & 1;
   const double dv = (double)v;
   const double s = wsum(dv), q = wsum(dv * dv);
   if (lane == 0) {
-    long long* vs = P.vstat + ((size_t)cur * P.n_inst + inst) * 2;
+    long long* vs = P.vstat + ((size_t)(C.n_steps_done & 1) * P.n_inst + inst) * 2;
     red_add64(vs, fx(s, kFxSum));
     red_add64(vs + 1, fx(q, kFxSq));
   }
-  const bool dyn = C.mode == MODE_DYNAMIC;
-  const bool upd = dyn || C.prime;
-  for (int fi = P.feed_begin[inst]; fi < P.feed_begin[inst + 1]; ++fi) {
-    Feed F;
-    {
-      const int4* fp = reinterpret_cast<const int4*>(P.feeds + fi);
-      int4* fd = reinterpret_cast<int4*>(&F);
+}
+
+// Feed fi (an estimator reading the vector) with tile `tile`: G_tile^T v
+// partials and sum v^2 into its fixed-point accumulators (a warp, lane = row).
+__device__ __noinline__ void emit_feed(const Prog& P, const ECtl& C, int fi, int tile, float v) {
+  const int lane = threadIdx.x & 31;
+  Feed F;
+  {
+    const int4* fp = reinterpret_cast<const int4*>(P.feeds + fi);
+    int4* fd = reinterpret_cast<int4*>(&F);
 #pragma unroll
-      for (int q = 0; q < (int)(sizeof(Feed) / 16); ++q) fd[q] = __ldg(fp + q);
-    }
-    if (es && fi == P.feed_begin[inst]) es[1] = gclock();
-    long long* acc;
-    if (F.kind == FEED_PREV) {
-      if (!upd) continue;
-      acc = P.acc + (size_t)(2 + C.prev_w) * P.acc_stride + F.acc;
-    } else {
-      if (!dyn) continue;
-      if (F.kind == FEED_CURFB && C.has_prev) continue;
-      acc = P.acc + (size_t)cur * P.acc_stride + F.acc;
-    }
-    if (F.Gt) {
-      // block of tile: [sub][chunk][lane][16 B]; f16 chunk = 4 rows x half2,
-      // f32 chunk = 2 rows x float2; lane owns k pair (2 lane, 2 lane + 1) of sub.
-      const int nsub = F.kpad / 64;
-      for (int sub = 0; sub < nsub; ++sub) {
-        float g0 = 0.f, g1 = 0.f;
-        if (F.f16) {
-          const uint4* blk = F.Gt + ((size_t)tile * nsub + sub) * 256 + lane;
+    for (int q = 0; q < (int)(sizeof(Feed) / 16); ++q) fd[q] = __ldg(fp + q);
+  }
+  const int cur = C.n_steps_done & 1;
+  const bool dyn = C.mode == MODE_DYNAMIC;
+  long long* acc;
+  if (F.kind == FEED_PREV) {
+    if (!(dyn || C.prime)) return;
+    acc = P.acc + (size_t)(2 + C.prev_w) * P.acc_stride + F.acc;
+  } else {
+    if (!dyn) return;
+    if (F.kind == FEED_CURFB && C.has_prev) return;
+    acc = P.acc + (size_t)cur * P.acc_stride + F.acc;
+  }
+  if (F.Gt) {
+    // block of tile: [sub][chunk][lane][16 B]; f16 chunk = 4 rows x half2,
+    // f32 chunk = 2 rows x float2; lane owns k pair (2 lane, 2 lane + 1) of sub.
+    const int nsub = F.kpad / 64;
+    const double sc = ldexp(1.0, F.fb);
+    for (int sub = 0; sub < nsub; ++sub) {
+      float g0 = 0.f, g1 = 0.f;
+      if (F.f16) {
+        const uint4* blk = F.Gt + ((size_t)tile * nsub + sub) * 256 + lane;
+        uint4 c[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c[i] = __ldg(blk + 32 * i);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const __half2* hh = reinterpret_cast<const __half2*>(&c[i]);
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr) {
+            const float xr = __shfl_sync(0xffffffffu, v, 4 * i + rr);
+            const float2 gg = __half22float2(hh[rr]);
+            g0 = fmaf(gg.x, xr, g0);
+            g1 = fmaf(gg.y, xr, g1);
+          }
+        }
+      } else {
+        const uint4* blk = F.Gt + ((size_t)tile * nsub + sub) * 512 + lane;
+#pragma unroll
+        for (int hb = 0; hb < 2; ++hb) {
           uint4 c[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) c[i] = __ldg(blk + 32 * i);
-          if (es && fi == P.feed_begin[inst]) { es[2] = gclock(); es[7] = c[0].x + c[7].w; es[3] = gclock(); }
+          for (int i = 0; i < 8; ++i) c[i] = __ldg(blk + 32 * (8 * hb + i));
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const __half2* hh = reinterpret_cast<const __half2*>(&c[i]);
+            const float* ff = reinterpret_cast<const float*>(&c[i]);
 #pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-              const float xr = __shfl_sync(0xffffffffu, v, 4 * i + rr);
-              const float2 gg = __half22float2(hh[rr]);
-              g0 = fmaf(gg.x, xr, g0);
-              g1 = fmaf(gg.y, xr, g1);
-            }
-          }
-        } else {
-          const uint4* blk = F.Gt + ((size_t)tile * nsub + sub) * 512 + lane;
-#pragma unroll
-          for (int hb = 0; hb < 2; ++hb) {
-            uint4 c[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) c[i] = __ldg(blk + 32 * (8 * hb + i));
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float* ff = reinterpret_cast<const float*>(&c[i]);
-#pragma unroll
-              for (int rr = 0; rr < 2; ++rr) {
-                const float xr = __shfl_sync(0xffffffffu, v, 2 * (8 * hb + i) + rr);
-                g0 = fmaf(ff[2 * rr], xr, g0);
-                g1 = fmaf(ff[2 * rr + 1], xr, g1);
-              }
+            for (int rr = 0; rr < 2; ++rr) {
+              const float xr = __shfl_sync(0xffffffffu, v, 2 * (8 * hb + i) + rr);
+              g0 = fmaf(ff[2 * rr], xr, g0);
+              g1 = fmaf(ff[2 * rr + 1], xr, g1);
             }
           }
         }
-        if (es && fi == P.feed_begin[inst]) es[4] = gclock();
-        const int k0 = sub * 64 + 2 * lane;
-        const double sc = ldexp(1.0, F.fb);
-        if (k0 < F.k) red_add64(acc + k0, fx((double)g0, sc));
-        if (k0 + 1 < F.k) red_add64(acc + k0 + 1, fx((double)g1, sc));
       }
+      const int k0 = sub * 64 + 2 * lane;
+      if (k0 < F.k) red_add64(acc + k0, fx((double)g0, sc));
+      if (k0 + 1 < F.k) red_add64(acc + k0 + 1, fx((double)g1, sc));
     }
-    if (lane == 0) red_add64(acc + F.k, fx(q, kFxSq));
-    if (es && fi == P.feed_begin[inst]) es[5] = gclock();
   }
-  if (es) es[6] = gclock();
+  const double dv = (double)v;
+  const double q = wsum(dv * dv);
+  if (lane == 0) red_add64(acc + F.k, fx(q, kFxSq));
+}
+
+// Statistics + every feed of one tile (one warp).
+__device__ __noinline__ void emit_tile(const Prog& P, const ECtl& C, int inst, int tile, float v) {
+  emit_stats(P, C, inst, v);
+  for (int fi = P.feed_begin[inst]; fi < P.feed_begin[inst + 1]; ++fi) emit_feed(P, C, fi, tile, v);
 }
 
 // ---------------------------------------------------------------------------
@@ -699,8 +699,11 @@ __device__ __forceinline__ float tile_y(const Prog& P, const Op& O, const Work& 
   return sm.scale * (lo * sm.sx + ldexpf(span, -fin) * (S + 0.5f * sm.sx));
 }
 
-__device__ __noinline__ void reduce_unit(const Prog& P, const ECtl& C, const Op& O, const Work& W, const Smem& sm, int u,
-                                         unsigned epoch) {
+// Reduce unit u (tile, or up|gate tile pair) of op O: window sum, affine
+// epilogue, residual add / SiLU (runtime.py:364-370), output store. Returns the
+// value the output instance is fed with (0 for padding rows) and its tile.
+__device__ __noinline__ float reduce_unit(const Prog& P, const Op& O, const Work& W, const Smem& sm, int u,
+                                          unsigned epoch, int& etile) {
   const int lane = threadIdx.x & 31;
   // independent operands first (they do not wait for the window slots)
   {
@@ -716,55 +719,78 @@ __device__ __noinline__ void reduce_unit(const Prog& P, const ECtl& C, const Op&
     } else if (O.add && r < L.rows) {
       l1_prefetch(O.out + L.out_off + r);
     }
-    if (O.out_inst >= 0)
-      emit_prefetch(P, O.out_inst, O.pair ? u : (O.L[li].out_off >> 5) + (u - O.L[li].tile_off));
   }
-  unsigned long long* stp = (threadIdx.x == 0 && u == blockIdx.x * NW) ? sm.stamp : nullptr;
+  unsigned long long* stp = (threadIdx.x == 0 && u == blockIdx.x) ? sm.stamp : nullptr;
   if (stp) stp[2] = gclock();
+  CSTAMP(stp, 11);
+  float v = 0.f;
   if (O.pair) {
     const int half = O.L[0].n_tiles;
     int li, r, li2, r2;
     bool ok, ok2;
     const float up = tile_y(P, O, W, sm, u, epoch, li, r, ok);
     const float gt = tile_y(P, O, W, sm, u + half, epoch, li2, r2, ok2);
-    const float hv = ok ? up * (gt / (1.0f + expf(-gt))) : 0.f;   // runtime.py:368
-    if (ok) O.out[r] = hv;
-    if (stp) stp[3] = gclock();
-    if (O.out_inst >= 0) emit_tile(P, C, O.out_inst, u, hv);
-    if (stp) stp[4] = gclock();
+    v = ok ? up * (gt / (1.0f + expf(-gt))) : 0.f;                 // runtime.py:368
+    if (ok) O.out[r] = v;
+    etile = u;
   } else {
     int li, r;
     bool ok;
     const float y = tile_y(P, O, W, sm, u, epoch, li, r, ok);
     const int o = O.L[li].out_off + r;
-    float v = 0.f;
-    if (O.add) {
-      if (ok) {
-        v = O.out[o] + y;                                            // runtime.py:364, 370
-        O.out[o] = v;
-      }
-    } else if (ok) {
-      O.out[o] = y;
+    if (ok) {
+      v = O.add ? O.out[o] + y : y;                                 // runtime.py:364, 370
+      O.out[o] = v;
     }
-    if (stp) stp[3] = gclock();
-    if (O.out_inst >= 0) emit_tile(P, C, O.out_inst, (O.L[li].out_off >> 5) + (u - O.L[li].tile_off), v);
-    if (stp) stp[4] = gclock();
+    etile = (O.L[li].out_off >> 5) + (u - O.L[li].tile_off);
   }
+  if (stp) stp[3] = gclock();
+  CSTAMP(stp, 12);
+  return v;
 }
-
-// Contributions a tile (or pair) receives: one per window.
-
 
 // ---------------------------------------------------------------------------
 // The op stage (consumer warps 0..NW-1)
 // ---------------------------------------------------------------------------
-// Reduction duty of this warp: units u = cta * NW + warp (+ G * NW ...),
-// each reduced as soon as its window slots carry this op's epoch.
-__device__ __noinline__ void reduce_duty(const Prog& P, const ECtl& C, const Op& O, const Work& W, const Smem& sm,
-                                          int cta, int G, unsigned epoch) {
-  const int warp = threadIdx.x >> 5;
+// Reduction of the op's units: unit u belongs to CTA u mod G (spread over the
+// grid so every CTA has at most a few), its i-th unit to warp i mod NW. Phase
+// A: window sums + epilogue per unit (values parked in shared memory); phase
+// B: the estimator feeds of the output instance, one (unit, feed) task per
+// warp in parallel (independent fixed-point sums). Warp NW - 1 first prepares
+// the next op's descriptor and work.
+__device__ __noinline__ void reduce_duty(const Prog& P, const ECtl& C, const Op& O, const Work& W, Smem& sm,
+                                          int cta, int G, unsigned epoch, Op* On, Work* Wn, const Op* On_global) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n_units = O.pair ? O.L[0].n_tiles : O.n_tiles;
-  for (int u = cta * NW + warp; u < n_units; u += G * NW) reduce_unit(P, C, O, W, sm, u, epoch);
+  const int mine = n_units > cta ? (n_units - cta + G - 1) / G : 0;     // units of this CTA
+  if (warp == NW - 1 && On && !Wn->valid) {
+    const int nw4 = (int)(sizeof(Op) / 16);
+    const int4* src = reinterpret_cast<const int4*>(On_global);
+    int4* dst = reinterpret_cast<int4*>(On);
+    for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
+    __syncwarp();
+    build_work_warp(*On, C, cta, G, *Wn);
+    __syncwarp();
+    if (lane == 0) Wn->valid = 1;
+  }
+  for (int i = warp; i < mine; i += NW) {
+    int et;
+    const float v = reduce_unit(P, O, W, sm, cta + i * G, epoch, et);
+    if (O.out_inst >= 0) {
+      emit_stats(P, C, O.out_inst, v);
+      sm.sbuf[i][lane] = v;              // parked base sums are dead after the extra pass
+      if (lane == 0) sm.vtile[i] = et;
+    }
+  }
+  if (O.out_inst < 0) return;
+  const int f0 = P.feed_begin[O.out_inst], nf = P.feed_begin[O.out_inst + 1] - f0;
+  if (nf == 0) return;
+  CSYNC();
+  for (int q = warp; q < mine * nf; q += NW) {
+    const int i = q / nf;
+    emit_feed(P, C, f0 + (q - i * nf), sm.vtile[i], sm.sbuf[i][lane]);
+  }
+  if (threadIdx.x == 0) CSTAMP(sm.stamp, 13);
 }
 
 // FIFO layout of an op (relative to its first FIFO index): base items run by
@@ -791,88 +817,96 @@ __device__ __noinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, 
   if (tid == 0) {
     sm.stamp = stamp;
     build_runs(O, W, sm.runs);
+    int o = 0;                          // FIFO offsets of the base planes
+    for (int r = 0; r < sm.runs.n; ++r) { sm.fo_bo[r] = (short)o; o += W.nb[sm.runs.r[r].li]; }
+    sm.last = o;
     sm.cons_op = op_no;
     sm.cons_j = j_op;
   }
   if (do_wait) bar_wait(P, wait_target);
   if (stamp && tid == 0) stamp[0] = gclock();
+  if (tid == 0) CSTAMP(stamp, 0);
 
-  // ---- prologue: the first window's input (LUT source) in flight first, then
-  // decisions (runtime.py:184-193), input statistics, the next op's descriptor
+  // ---- prologue. Critical path: the first window's input -> LUT -> base
+  // items. The selector inputs (accumulators, statistics) are loaded in the
+  // same round trip and finished after the LUT build (runtime.py:184-193).
   const int w_first = sm.runs.n > 0 ? sm.runs.r[0].w : -1;
   if (w_first >= 0) {
     const int col = w_first * kWinCols + tid;
     sm.xw[tid] = col < O.cols ? __ldcg(O.in + col) : 0.f;
   }
-  if (warp < O.n_layers) {
-    const int li = warp;
-    const Layer& L = O.L[li];
-    int bit = W.nb[li];
-    double est = CUDART_NAN;
-    const bool estimating = C.mode == MODE_DYNAMIC && L.sentinel == 0 && L.est != EST_NONE;
-    if (estimating) {
-      const int slot = (L.src == SRC_PREV_STEP && C.has_prev) ? 2 + C.prev_r : cur;
-      const long long* acc = P.acc + (size_t)slot * P.acc_stride + L.acc;
-      double q = 0.0;
-      for (int kk = lane; kk < L.k; kk += 32) {
-        const double g = (double)__ldcg(acc + kk) * L.fbscale;
-        q += g * g;
-      }
-      q = wsum(q);
-      const double sq = (double)__ldcg(acc + L.k) * (1.0 / kFxSq);
-      const double sc = O.rms ? rsqrt_d(sq / (double)O.cols + (double)P.eps) : 1.0;
-      if (L.est == EST_PROJECTION) est = q > 0.0 ? sc * q * rsqrt_d(q) : 0.0;
-      else est = L.slope * (sq > 0.0 ? sc * sq * rsqrt_d(sq) : 0.0) + L.intercept;
-      if (!C.force) bit = est > L.T ? L.h : L.l;                       // strict > (runtime.py:192)
-    }
-    if (lane == 0) {
-      W.fin[li] = bit;
-      sm.dec_fin[op_no & 1][li] = bit;
-      if (C.mode == MODE_DYNAMIC && cta == 0 && L.trace >= 0 && P.n_trace > 0 && C.trace_step < P.max_steps) {
-        const size_t o = (size_t)C.trace_step * P.n_trace + L.trace;
-        P.tr_bits[o] = (signed char)bit;
-        P.tr_est[o] = estimating ? (float)est : CUDART_NAN_F;
-      }
-    }
-  } else if (warp == kMaxOpLayers) {
-    if (lane == 0) {
-      const long long* vs = P.vstat + ((size_t)cur * P.n_inst + O.in_inst) * 2;
-      const double s1 = (double)__ldcg(vs) * (1.0 / kFxSum);
-      const double s2 = (double)__ldcg(vs + 1) * (1.0 / kFxSq);
-      sm.sx = (float)s1;
-      sm.scale = O.rms ? (float)rsqrt_d(s2 / (double)O.cols + (double)P.eps) : 1.f;
-    }
-  } else if (warp == kMaxOpLayers + 1 && On && !Wn->valid) {
-    const int nw4 = (int)(sizeof(Op) / 16);
-    const int4* src = reinterpret_cast<const int4*>(On_global);
-    int4* dst = reinterpret_cast<int4*>(On);
-    for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
-    __syncwarp();
-    build_work_warp(*On, C, cta, G, *Wn);
-    __syncwarp();
-    if (lane == 0) Wn->valid = 1;
-  } else if (warp == kMaxOpLayers + 2) {
+  // decision warps: accumulator loads in flight (k <= 128: 4 per lane)
+  const bool dec_warp = warp < O.n_layers;
+  const Layer& Ld = O.L[dec_warp ? warp : 0];
+  const bool estimating = dec_warp && C.mode == MODE_DYNAMIC && Ld.sentinel == 0 && Ld.est != EST_NONE;
+  long long ga[4] = {0, 0, 0, 0}, gsq = 0;
+  if (estimating) {
+    const int slot = (Ld.src == SRC_PREV_STEP && C.has_prev) ? 2 + C.prev_r : cur;
+    const long long* acc = P.acc + (size_t)slot * P.acc_stride + Ld.acc;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (lane + 32 * q < Ld.k) ga[q] = __ldcg(acc + lane + 32 * q);
+    gsq = __ldcg(acc + Ld.k);
+  }
+  long long vs1 = 0, vs2 = 0;
+  if (warp == kMaxOpLayers && lane == 0) {
+    const long long* vs = P.vstat + ((size_t)cur * P.n_inst + O.in_inst) * 2;
+    vs1 = __ldcg(vs);
+    vs2 = __ldcg(vs + 1);
+  } else if (warp == kMaxOpLayers + 1) {
     prefetch_feeds_l2(P, C, O.out_inst, O.n_tiles * 32, cta, G);
   }
-  CSYNC();
-  if (tid == 0) {
-    __threadfence_block();
-    sm.dec_op = op_no + 1;            // the producer may now stream the extra planes
-  }
+  CSYNC();                             // input window in shared memory
+  if (tid == 0) CSTAMP(stamp, 1);
   float* lut = reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLut - smem_u32(&sm)));
   int lut_w = -1;
-  if (w_first >= 0) {                 // LUT of the first window (its input loaded above)
+  if (w_first >= 0) {                 // LUT of the first window
     build_lut(lut, sm.xw);
     if (tid < 64) lut[256 * kGroups + tid] = 0.f;
     lut_w = w_first;
   }
-  // FIFO offsets of the runs (thread 0; a few dozen runs at most)
+  if (tid == 0) CSTAMP(stamp, 2);
+  if (dec_warp) {
+    const int li = warp;
+    int bit = W.nb[li];
+    double est = CUDART_NAN;
+    if (estimating) {
+      double q = 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double g = (double)ga[i] * Ld.fbscale;
+        q += g * g;
+      }
+      q = wsum(q);
+      const double sq = (double)gsq * (1.0 / kFxSq);
+      const double sc = O.rms ? rsqrt_d(sq / (double)O.cols + (double)P.eps) : 1.0;
+      if (Ld.est == EST_PROJECTION) est = q > 0.0 ? sc * q * rsqrt_d(q) : 0.0;
+      else est = Ld.slope * (sq > 0.0 ? sc * sq * rsqrt_d(sq) : 0.0) + Ld.intercept;
+      if (!C.force) bit = est > Ld.T ? Ld.h : Ld.l;                      // strict > (runtime.py:192)
+    }
+    if (lane == 0) {
+      CSTAMP(stamp, 4 + li);
+      W.fin[li] = bit;
+      sm.dec_fin[op_no & 1][li] = bit;
+      if (C.mode == MODE_DYNAMIC && cta == 0 && Ld.trace >= 0 && P.n_trace > 0 && C.trace_step < P.max_steps) {
+        const size_t o = (size_t)C.trace_step * P.n_trace + Ld.trace;
+        P.tr_bits[o] = (signed char)bit;
+        P.tr_est[o] = estimating ? (float)est : CUDART_NAN_F;
+      }
+    }
+  } else if (warp == kMaxOpLayers && lane == 0) {
+    sm.sx = (float)((double)vs1 * (1.0 / kFxSum));
+    sm.scale = O.rms ? (float)rsqrt_d((double)vs2 * (1.0 / kFxSq) / (double)O.cols + (double)P.eps) : 1.f;
+    CSTAMP(stamp, 7);
+  }
+  CSYNC();                             // decisions and LUT visible
   const RunList& R = sm.runs;
-  int n_base = 0, n_ext = 0, t_ext = 0;
   if (tid == 0) {
-    int o = 0;
-    for (int r = 0; r < R.n; ++r) { sm.fo_bo[r] = (short)o; o += W.nb[R.r[r].li]; }
-    n_base = o;
+    __threadfence_block();
+    sm.dec_op = op_no + 1;            // the producer may now stream the extra planes
+    // FIFO offsets of the extra planes (base offsets were set before the barrier)
+    int o = sm.last;
+    const int o_base = o;
     int xt = 0;
     for (int r = R.n - 1; r >= 0; --r) {
       const int ex = W.fin[R.r[r].li] - W.nb[R.r[r].li];
@@ -880,22 +914,25 @@ __device__ __noinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, 
       sm.fo_xt[r] = (short)xt;
       if (ex > 0) { o += ex; xt += R.r[r].nt; }
     }
-    n_ext = o - n_base;
-    t_ext = xt;
-    sm.last = n_base | (n_ext << 16);
-    reinterpret_cast<int*>(sm.red)[0] = t_ext;
+    sm.n_ext_items = o - o_base;
+    sm.t_ext = xt;
   }
-  CSYNC();
-  n_base = sm.last & 0xffff;
-  n_ext = sm.last >> 16;
-  t_ext = reinterpret_cast<int*>(sm.red)[0];
+  const int n_base = sm.last;
   if (stamp && tid == 0) stamp[1] = gclock();
+  if (tid == 0) CSTAMP(stamp, 3);
   if (tid == 0) PROGRESS(1, 1);
   const int n_tasks_base = W.gb - W.ga;
+#ifdef DPQ_PROFILE_WARPS
+  unsigned long long w_first_t = 0, w_last_t = 0, w_seq = 0, w_mb = 0, w_task0 = 0;   // per-warp profiling (stamp != nullptr)
+  int w_planes = 0;
+#define WPROF(x) do { if (stamp) { x; } } while (0)
+#else
+#define WPROF(x) do { } while (0)
+#endif
   // ---- stream: tasks (run, tile) in FIFO order, LUT rebuilt per window segment
   const unsigned char* dyn0 = reinterpret_cast<const unsigned char*>(&sm);
   for (int kind = 0; kind < 2; ++kind) {
-    const int n_tasks = kind ? t_ext : n_tasks_base;
+    const int n_tasks = kind ? sm.t_ext : n_tasks_base;
     int k = 0;                          // task index at the segment start
     int rr = kind ? R.n - 1 : 0;        // run index at the segment start
     while (k < n_tasks) {
@@ -921,6 +958,7 @@ __device__ __noinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, 
       }
       const uint32_t lanereg = kLut | ((uint32_t)lane * 4u);
       for (int kt = k + warp; kt < k_end; kt += NW) {
+        WPROF(if (!w_task0) w_task0 = clock64());
         // task kt -> run and tile
         int r = rr, base_k = k;
         while (true) {
@@ -940,38 +978,30 @@ __device__ __noinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, 
           const int j = jr + (p - p0);
           const int slot = j & (kMaxSlots - 1);
           WSTATE(j * 16 + 1);
+#ifdef DPQ_PROFILE_WARPS
+          const unsigned long long tw0 = stamp ? clock64() : 0;
+#endif
           if (lane == 0) {
-            if (sm.seq[slot] > j) hang("ring overtaken", ((long long)j << 32) | (unsigned)sm.seq[slot], ((long long)r << 32) | (unsigned)kt);
-            if (!(sm.seq[slot] == j)) {
-              unsigned n_ = 0;
-              unsigned long long t0_ = 0;
-              while (!(sm.seq[slot] == j)) {
-                if ((++n_ & 4095u) == 0) {
-                  const unsigned long long t_ = gclock();
-                  if (t0_ == 0) t0_ = t_;
-                  else if (t_ - t0_ > 1000000000ull) {
-                    if (g_diag) {
-                      volatile unsigned long long* d_ = g_diag;
-                      d_[6] = ((unsigned long long)W.ga << 32) | (unsigned)W.gb;
-                      d_[7] = ((unsigned long long)sm.pw.ga << 32) | (unsigned)sm.pw.gb;
-                      d_[8] = (unsigned long long)(W.nb[0] | W.nb[1] << 8 | W.nb[2] << 16 | W.fin[0] << 24) |
-                              ((unsigned long long)(sm.pw.nb[0] | sm.pw.nb[1] << 8 | sm.pw.nb[2] << 16) << 32);
-                      d_[9] = ((unsigned long long)R.n << 32) | (unsigned)sm.pruns.n;
-                      d_[10] = ((unsigned long long)(unsigned)sm.fo_bo[1] << 32) | (unsigned)(j_op);
-                      d_[11] = ((unsigned long long)C.mode << 32) | (unsigned)C.force;
-                      for (int q2 = 0; q2 < NW; ++q2) d_[12 + q2] = (unsigned long long)sm.wstate[q2];
-                    }
-                    hang("ring sequence", ((long long)j << 32) | (unsigned)sm.seq[slot],
-                         ((long long)(kind * 1000 + r) << 32) | (unsigned)kt);
-                  }
-                }
-              }
-            }
+            if (sm.seq[slot] > j) hang("ring overtaken", j, sm.seq[slot]);
+            SPIN_UNTIL_NS(sm.seq[slot] == j, "ring sequence", j, sm.seq[slot], 1000000000ull);
           }
           __syncwarp();
           WSTATE(j * 16 + 2);
+#ifdef DPQ_PROFILE_WARPS
+          const unsigned long long tw1 = stamp ? clock64() : 0;
+#endif
           mbar_wait(&sm.full[slot], (unsigned)((j / kMaxSlots) & 1));
           WSTATE(j * 16 + 3);
+#ifdef DPQ_PROFILE_WARPS
+          if (stamp) {
+            const unsigned long long tn = clock64();
+            w_seq += tw1 - tw0;
+            w_mb += tn - tw1;
+            if (!w_first_t) w_first_t = tn;
+            w_last_t = tn;
+            ++w_planes;
+          }
+#endif
           const uint4* d = reinterpret_cast<const uint4*>(dyn0 + sm.slot_off[slot] + i * kTileBytes) + lane;
           const uint4 d0 = d[0], d1 = d[32], d2 = d[64], d3 = d[96];
           S = 2.f * S + plane_sum(d0, d1, d2, d3, lanereg);       // Horner over planes
@@ -990,16 +1020,24 @@ __device__ __noinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, 
       k = k_end;
       rr = re;
     }
+#ifdef DPQ_PROFILE_WARPS
+    if (stamp && lane == 0) {
+      unsigned long long* ws = stamp + 8 + warp * 5;
+      ws[0] = w_task0; ws[1] = w_first_t; ws[2] = w_last_t; ws[3] = clock64(); ws[4] = (unsigned long long)w_planes | (min(w_seq, 0xffffffull) << 16) | (min(w_mb, 0xffffffull) << 40);
+    }
+#endif
     if (!kind) CSYNC();                   // parked base sums visible before the extra pass
   }
   if (tid == 0) PROGRESS(1, 2);
   if (stamp && tid == 0) stamp[5] = gclock();
-  reduce_duty(P, C, O, W, sm, cta, G, epoch);
+  if (tid == 0) CSTAMP(stamp, 10);
+  reduce_duty(P, C, O, W, sm, cta, G, epoch, On, Wn, On_global);
   if (tid == 0) PROGRESS(1, 3);
   if (stamp && tid == 0) stamp[6] = gclock();
+  if (tid == 0) CSTAMP(stamp, 15);
   CSYNC();
-  if (tid == 0) W.valid = 0;
-  return n_base + n_ext;
+  if (tid == 0) { W.valid = 0; CSTAMP(stamp, 16); }
+  return n_base + sm.n_ext_items;
 }
 
 // ---------------------------------------------------------------------------
@@ -1066,23 +1104,32 @@ __device__ __noinline__ void producer(const Prog& P, Smem& sm, int cta, int G, i
         }
       }
       if (lane == 0) {
+        unsigned long long* pd = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec + 8 + 5 * NW : nullptr;
+        const int j0 = j;
+        if (pd) pd[0] = gclock();
         const Op& O = sm.pop;
         build_runs(O, sm.pw, sm.pruns);
         const RunList& R = sm.pruns;
         for (int r = 0; r < R.n; ++r)
-          for (int p = 0; p < sm.pw.nb[R.r[r].li]; ++p) issue(O, R.r[r], p);
+          for (int p = 0; p < sm.pw.nb[R.r[r].li]; ++p) {
+            issue(O, R.r[r], p);
+            if (pd && j == j0 + 1) pd[1] = gclock();
+          }
+        if (pd) pd[2] = gclock();
         bool may_extra = false;
         if (C.mode == MODE_DYNAMIC && !C.force)
           for (int li = 0; li < O.n_layers; ++li) may_extra |= O.L[li].sentinel == 0 && O.L[li].l < O.L[li].h;
         if (may_extra && R.n > 0) {
           SPIN_UNTIL_NS(sm.dec_op >= op_no + 1, "producer decision", op_no, 0, 12000000000ull);
           __threadfence_block();
+          if (pd) pd[3] = gclock();
           for (int r = R.n - 1; r >= 0; --r) {
             const int li = R.r[r].li;
             const int fin = sm.dec_fin[op_no & 1][li];
             for (int p = sm.pw.nb[li]; p < fin; ++p) issue(O, R.r[r], p);
           }
         }
+        if (pd) { pd[4] = gclock(); pd[5] = (unsigned long long)(j - j0); }
       }
       __syncwarp();
       ++op_no;
@@ -1417,12 +1464,12 @@ extern "C" __global__ void __launch_bounds__(NTB, 1) engine_kernel(const Prog Pk
         }
         j_op += op_stage(P, C, sm.op[wi], sm.work[wi], has_next ? &sm.op[wi ^ 1] : nullptr, &sm.work[wi ^ 1],
                          has_next ? P.ops + P.stages[nsi].y : nullptr, sm, cta, G, target, wait,
-                         P.dbg ? P.dbg + ((size_t)si * G + cta) * 8 : nullptr, op_no, j_op);
+                         P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr, op_no, j_op);
         ++op_no;
         wi ^= 1;
       } else {
         if (wait) bar_wait(P, target);
-        if (P.dbg && tid == 0) P.dbg[((size_t)si * G + cta) * 8] = gclock();
+        if (P.dbg && tid == 0) P.dbg[((size_t)si * G + cta) * kDbgRec] = gclock();
         if (st.x == ST_BEGIN) {
           read_ctl(P, C);
           if (tid == 0) {
@@ -1438,8 +1485,9 @@ extern "C" __global__ void __launch_bounds__(NTB, 1) engine_kernel(const Prog Pk
           head_stage(P, C, sm, cta, G);
         }
       }
-      if (P.dbg && tid == 0) P.dbg[((size_t)si * G + cta) * 8 + 7] = gclock();
+      if (P.dbg && tid == 0) P.dbg[((size_t)si * G + cta) * kDbgRec + 7] = gclock();
       bar_arrive(P, e0 + k + 1, G);
+      if (tid == 0) CSTAMP(P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr, 17);
       ++k;
     }
   }

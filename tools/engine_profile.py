@@ -68,12 +68,17 @@ def main():
     per = C.c_int()
     _lib.call("dpq_session_debug_times", eng._h, None, -8, C.byref(per))
     _lib.call("dpq_session_debug_times", eng._h, None, 0, C.byref(per))
-    G = per.value // 8
-    buf = np.zeros(n.value * G * 8, dtype=np.uint64)
+    G = torch.cuda.get_device_properties(0).multi_processor_count
+    rec = per.value // G
+    buf = np.zeros(n.value * G * rec, dtype=np.uint64)
     _lib.call("dpq_session_debug_times", eng._h, C.c_void_p(buf.ctypes.data), buf.size, C.byref(per))
-    st = buf.reshape(n.value, G, 8).astype(np.float64)
+    full = buf.reshape(n.value, G, rec)
+    st = full[..., :8].astype(np.float64)
+    wst = full[..., 8:88].reshape(n.value, G, 16, 5)
+    pst = full[..., 88:96]
+    cst = full[..., 96:128]
     if args.dump:
-        np.savez(args.dump, st=st, kinds=kinds, idx=idx)
+        np.savez(args.dump, st=st, wst=wst, pst=pst, cst=cst, kinds=kinds, idx=idx)
     start, end = st[..., 0], st[..., 7]
     pro, loop = st[..., 4], st[..., 5]
     last_end = end.max(axis=1)
@@ -127,7 +132,7 @@ def main():
         nm = opn[oi % 4]
         oi += 1
         s_ = st[k]
-        ok = s_[:, 4] > 0
+        ok = s_[:, 5] > 0
         rel = (s_[ok] - s_[ok][:, :1]) / 1e3
         ph_acc.setdefault(nm, []).append(rel.mean(axis=0))
     for nm, v in ph_acc.items():
