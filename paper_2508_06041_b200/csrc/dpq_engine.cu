@@ -29,14 +29,14 @@
 #include "dpq_common.cuh"
 
 // Consumer-only CTA barrier (the producer warp never joins).
-#define CSYNC() asm volatile("bar.sync 1, 512;" ::: "memory")
+#define CSYNC() asm volatile("bar.sync 1, %0;" :: "n"(dpq::eng::NT) : "memory")
 
 namespace dpq {
 namespace eng {
 
-constexpr int NT = 512;            // consumer threads per CTA (warps 0..15)
+constexpr int NT = 480;            // consumer threads per CTA (warps 0..14): 16 warps in all -> 128 registers
 constexpr int NW = NT / 32;        // consumer warps
-constexpr int NTB = NT + 32;       // block: consumers + one TMA producer warp (warp 16)
+constexpr int NTB = NT + 32;       // block: consumers + one TMA producer warp (warp 15)
 constexpr int kSlotTiles = 8;      // tiles per ring slot (one plane of up to 8 consecutive tiles)
 constexpr int kSlotBytes = kSlotTiles * 2048;
 constexpr int kMaxSlots = 8;       // ring slots (power of two: index arithmetic by shifts)
@@ -261,32 +261,54 @@ __device__ __forceinline__ float plane_sum(const uint4 d0, const uint4 d1, const
 }
 
 // LUT of one 512-column window: row e, slot g = sum_{t: bit t of e} x[8g + t];
-// row 256 = 0 (target of the wrapped "e - 1" encoding for e = 0).
-__device__ __forceinline__ void build_lut(float* lut, const float* xw) {
-  for (int u = threadIdx.x; u < 512; u += NT) {
-    const int g = u & 63, rb = u >> 6;   // rb: 8 blocks of 32 rows
-    const float* xg = xw + 8 * g;
-    float L[16];
-    L[0] = 0.f;
+// row 256 = 0 (target of the wrapped "e - 1" encoding for e = 0). Thread u <
+// 256 builds rows [64 q, 64 q + 64) of group g (u = 64 q + g) straight from
+// the input in global memory (lut_load issues the loads, lut_store writes
+// the rows once they arrived; no staging, no barrier in between).
+struct LutSrc { float4 a, b; };
+__device__ __forceinline__ LutSrc lut_load(const float* x, int cols, int w) {
+  LutSrc r;
+  r.a = r.b = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int u = threadIdx.x;
+  if (u < 256) {
+    const int c0 = w * kWinCols + 8 * (u & 63);
+    if (c0 + 8 <= cols) {
+      r.a = __ldcg(reinterpret_cast<const float4*>(x + c0));
+      r.b = __ldcg(reinterpret_cast<const float4*>(x + c0 + 4));
+    } else {
+      float t[8];
 #pragma unroll
-    for (int n = 1; n < 16; ++n) {
-      const int low = n & (-n);
-      L[n] = L[n ^ low] + xg[__ffs(low) - 1];
+      for (int j = 0; j < 8; ++j) t[j] = c0 + j < cols ? __ldcg(x + c0 + j) : 0.f;
+      r.a = make_float4(t[0], t[1], t[2], t[3]);
+      r.b = make_float4(t[4], t[5], t[6], t[7]);
     }
-    const float x4 = xg[4], x5 = xg[5], x6 = xg[6], x7 = xg[7];
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int m = 2 * rb + hh;
-      float H = 0.f;
-      if (m & 1) H += x4;
-      if (m & 2) H += x5;
-      if (m & 4) H += x6;
-      if (m & 8) H += x7;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) lut[(16 * m + i) * kGroups + g] = L[i] + H;
-    }
-    if (rb == 0) lut[256 * kGroups + g] = 0.f;
   }
+  return r;
+}
+__device__ __forceinline__ void lut_store(float* lut, const LutSrc& x) {
+  const int u = threadIdx.x;
+  if (u >= 256) return;
+  const int g = u & 63, q = u >> 6;
+  const float xs[4] = {x.a.x, x.a.y, x.a.z, x.a.w};
+  float L[16];
+  L[0] = 0.f;
+#pragma unroll
+  for (int n = 1; n < 16; ++n) {
+    const int low = n & (-n);
+    L[n] = L[n ^ low] + xs[__ffs(low) - 1];
+  }
+#pragma unroll
+  for (int mm = 0; mm < 4; ++mm) {
+    const int m = 4 * q + mm;
+    float H = 0.f;
+    if (m & 1) H += x.b.x;
+    if (m & 2) H += x.b.y;
+    if (m & 4) H += x.b.z;
+    if (m & 8) H += x.b.w;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) lut[(16 * m + i) * kGroups + g] = L[i] + H;
+  }
+  if (u < 64) lut[256 * kGroups + u] = 0.f;
 }
 
 // ---------------------------------------------------------------------------
@@ -344,7 +366,6 @@ struct Smem {
   unsigned long long* stamp;         // current stage's timestamps (profiling) or nullptr
   volatile int wstate[NW];           // per consumer warp: item it waits for * 16 + state
   int dec_fin[2][kMaxOpLayers];      // published final bits (op counter parity)
-  float xw[kWinCols];
   float scale, sx;         // op input scale (1/rms or 1) and sum of raw input
   int last;                // base FIFO items of the current op (op stage) / last-arriver flag
   int n_ext_items, t_ext;  // extra FIFO items / extra tasks of the current op (after the decision)
@@ -831,10 +852,7 @@ __device__ __noinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, 
   // items. The selector inputs (accumulators, statistics) are loaded in the
   // same round trip and finished after the LUT build (runtime.py:184-193).
   const int w_first = sm.runs.n > 0 ? sm.runs.r[0].w : -1;
-  if (w_first >= 0) {
-    const int col = w_first * kWinCols + tid;
-    sm.xw[tid] = col < O.cols ? __ldcg(O.in + col) : 0.f;
-  }
+  const LutSrc xsrc = lut_load(O.in, O.cols, max(w_first, 0));
   // decision warps: accumulator loads in flight (k <= 128: 4 per lane)
   const bool dec_warp = warp < O.n_layers;
   const Layer& Ld = O.L[dec_warp ? warp : 0];
@@ -856,13 +874,11 @@ __device__ __noinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, 
   } else if (warp == kMaxOpLayers + 1) {
     prefetch_feeds_l2(P, C, O.out_inst, O.n_tiles * 32, cta, G);
   }
-  CSYNC();                             // input window in shared memory
   if (tid == 0) CSTAMP(stamp, 1);
   float* lut = reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLut - smem_u32(&sm)));
   int lut_w = -1;
   if (w_first >= 0) {                 // LUT of the first window
-    build_lut(lut, sm.xw);
-    if (tid < 64) lut[256 * kGroups + tid] = 0.f;
+    lut_store(lut, xsrc);
     lut_w = w_first;
   }
   if (tid == 0) CSTAMP(stamp, 2);
@@ -947,12 +963,9 @@ __device__ __noinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, 
         re += kind ? -1 : 1;
       }
       if (w != lut_w) {
+        const LutSrc xs2 = lut_load(O.in, O.cols, w);
         CSYNC();                          // previous LUT users done
-        const int col = w * kWinCols + tid;
-        sm.xw[tid] = col < O.cols ? __ldcg(O.in + col) : 0.f;
-        CSYNC();
-        build_lut(lut, sm.xw);
-        if (tid < 64) lut[256 * kGroups + tid] = 0.f;
+        lut_store(lut, xs2);
         CSYNC();
         lut_w = w;
       }
@@ -1139,130 +1152,136 @@ __device__ __noinline__ void producer(const Prog& P, Smem& sm, int cta, int G, i
 
 // ---------------------------------------------------------------------------
 // Attention stage (runtime.py:351-362): RoPE, KV append, causal softmax.
-// Unit = (kv head g, position chunk); a unit serves the H/KV query heads of
-// its group with an online softmax over 32-position sub-chunks; chunk
-// partials are merged by the last unit of the group.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float rope_at(const float* v, int i, int hd, const float* c, const float* s) {
+// Unit = (query head h, chunk of <= kAttnChunkE positions). Warp w takes the
+// chunk's positions s0 + w, s0 + w + NW, ... with a per-warp online softmax
+// (lane = 4 consecutive dims, float4 loads; RoPE half-split recomputed per
+// warp from the q / k outputs, runtime.py:351-352); the NW partial (m, l, o)
+// are merged in shared memory in fixed warp order. Chunk partials of a head
+// are merged by the last unit of the head. The unit holding position t of the
+// first query head of each KV group appends k_t / v_t (runtime.py:355-356).
+constexpr int kAttnChunkE = 32;
+
+// RoPE of 4 consecutive dims [i0, i0 + 4) of a head vector v (i0 % 4 == 0).
+__device__ __forceinline__ float4 rope4(const float* v, int i0, int hd, const float* c, const float* s) {
   const int half = hd / 2;
-  if (i < half) return __ldcg(v + i) * c[i] - __ldcg(v + i + half) * s[i];
-  if (i < 2 * half) return __ldcg(v + i - half) * s[i - half] + __ldcg(v + i) * c[i - half];
-  return __ldcg(v + i);
+  const float4 a = __ldcg(reinterpret_cast<const float4*>(v + i0));
+  if (i0 >= 2 * half) return a;                                  // odd hd tail: identity
+  const bool lo = i0 < half;
+  const int j0 = lo ? i0 : i0 - half;                            // index into cos / sin
+  const float4 b = __ldcg(reinterpret_cast<const float4*>(v + (lo ? i0 + half : i0 - half)));
+  const float cc[4] = {__ldg(c + j0), __ldg(c + j0 + 1), __ldg(c + j0 + 2), __ldg(c + j0 + 3)};
+  const float ss[4] = {__ldg(s + j0), __ldg(s + j0 + 1), __ldg(s + j0 + 2), __ldg(s + j0 + 3)};
+  float4 r;
+  if (lo) {   // x_i c_i - x_{i+half} s_i
+    r.x = a.x * cc[0] - b.x * ss[0]; r.y = a.y * cc[1] - b.y * ss[1];
+    r.z = a.z * cc[2] - b.z * ss[2]; r.w = a.w * cc[3] - b.w * ss[3];
+  } else {    // x_{i-half} s_j + x_i c_j
+    r.x = b.x * ss[0] + a.x * cc[0]; r.y = b.y * ss[1] + a.y * cc[1];
+    r.z = b.z * ss[2] + a.z * cc[2]; r.w = b.w * ss[3] + a.w * cc[3];
+  }
+  return r;
 }
 
-__device__ __noinline__ void attn_emit_head(const Prog& P, const ECtl& C, int inst, int h) {
-  // emit the hd/32 tiles of head h (warps of this CTA), values already in P.attn
+__device__ __forceinline__ float dot4(float4 a, float4 b) { return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w; }
+
+// Statistics + feeds of head h's output tiles (values in vals[hd]): one
+// (tile, feed) task per warp.
+__device__ __noinline__ void attn_emit_head(const Prog& P, const ECtl& C, int inst, int h, const float* vals) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nt = (P.hd + 31) / 32;
-  for (int tt = warp; tt < nt; tt += NW) {
+  const int f0 = P.feed_begin[inst], nf = P.feed_begin[inst + 1] - f0;
+  for (int q = warp; q < nt * (nf + 1); q += NW) {
+    const int tt = q / (nf + 1), f = q - tt * (nf + 1);
     const int i = tt * 32 + lane;
-    const float v = i < P.hd ? __ldcg(P.attn + h * P.hd + i) : 0.f;
-    emit_tile(P, C, inst, (h * P.hd) / 32 + tt, v);
+    const float v = i < P.hd ? vals[i] : 0.f;
+    const int tile = (h * P.hd) / 32 + tt;
+    if (f == nf) emit_stats(P, C, inst, v);
+    else emit_feed(P, C, f0 + f, tile, v);
   }
 }
-
-// Unit = (query head h, chunk of <= kAttnChunkE positions). K/V rows of the
-// chunk are staged in shared memory (the LUT region is free here); chunk
-// partials (m, l, o) are merged by the last unit of the head. The unit that
-// holds position t of the first head of each KV group appends k_t / v_t.
-constexpr int kAttnChunkE = 32;   // K/V staging stays inside the LUT region
 
 __device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, float* sh, int cta, int G, int* s_last) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t = C.pos, n = t + 1;
-  const int hd = P.hd, H = P.H, qh = P.H / P.KV, half = hd / 2;
+  const int hd = P.hd, qh = P.H / P.KV, nv = hd / 4;
   const int nch = (n + kAttnChunkE - 1) / kAttnChunkE;
-  const int units = H * nch;
+  const int units = P.H * nch;
   const float scale = 1.0f / sqrtf((float)hd);
-  const float* cs = P.cosv + (size_t)t * half;
-  const float* sn = P.sinv + (size_t)t * half;
+  const float* cs = P.cosv + (size_t)t * (hd / 2);
+  const float* sn = P.sinv + (size_t)t * (hd / 2);
   float* kc = P.kc[b];
   float* vc = P.vc[b];
   const int inst = 4 * b + 1;
   // G^T blocks the attention output feeds (o-proj estimators) -> L2
   if (warp == NW - 1) prefetch_feeds_l2(P, C, inst, P.d, cta, G);
-  // smem: Ks[64][hd] Vs[64][hd] q[hd] kt[hd] vt[hd] sc[64] o[hd] red[NW][hd]
-  float* Ks = sh;
-  float* Vs = Ks + kAttnChunkE * hd;
-  float* q = Vs + kAttnChunkE * hd;
-  float* kt = q + hd;
-  float* vt = kt + hd;
-  float* sc = vt + hd;
-  float* stat = sc + kAttnChunkE;          // [0] m, [1] l
+  const int ps = hd + 4;                   // part row stride (16-byte aligned)
+  float* part = sh;                        // [NW][ps]: o, m, l of each warp
+  float* outv = sh + NW * ps;              // [hd] merged head output
   for (int u = cta; u < units; u += G) {
     const int h = u / nch, ch = u - h * nch;
     const int g = h / qh;
-    const int s0 = ch * kAttnChunkE, s1 = min(n, s0 + kAttnChunkE), ns = s1 - s0;
-    const bool has_t = s1 == n;
-    CSYNC();
-    // q (RoPE), and the new k / v when this chunk holds position t
-    for (int i = tid; i < hd; i += NT) {
-      q[i] = rope_at(P.qkv + h * hd, i, hd, cs, sn);
-      if (has_t) {
-        kt[i] = rope_at(P.qkv + P.d + g * hd, i, hd, cs, sn);
-        vt[i] = __ldcg(P.qkv + P.d + P.dkv + g * hd + i);
-      }
-    }
-    // K / V rows of the chunk (positions < t from the cache), 16-byte loads
-    const int nv = hd / 4;
-    for (int idx = tid; idx < (ns - (has_t ? 1 : 0)) * nv; idx += NT) {
-      const int sp = idx / nv, c4 = idx - sp * nv;
-      const size_t off = (size_t)(s0 + sp) * P.dkv + g * hd + 4 * c4;
-      reinterpret_cast<float4*>(Ks + sp * hd)[c4] = __ldcg(reinterpret_cast<const float4*>(kc + off));
-      reinterpret_cast<float4*>(Vs + sp * hd)[c4] = __ldcg(reinterpret_cast<const float4*>(vc + off));
-    }
-    CSYNC();
-    if (has_t) {
-      for (int i = tid; i < hd; i += NT) {
-        Ks[(ns - 1) * hd + i] = kt[i];
-        Vs[(ns - 1) * hd + i] = vt[i];
-        if (h % qh == 0) {                         // runtime.py:355-356 (KV append)
-          kc[(size_t)t * P.dkv + g * hd + i] = kt[i];
-          vc[(size_t)t * P.dkv + g * hd + i] = vt[i];
+    const int s0 = ch * kAttnChunkE, s1 = min(n, s0 + kAttnChunkE);
+    // per-warp online softmax over positions s0 + warp + NW k (lane = dims 4 lane .. 4 lane + 3)
+    float m = -CUDART_INF_F, l = 0.f;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool act = lane < nv;
+    const int i0 = 4 * lane;
+    const float4 q4 = act ? rope4(P.qkv + h * hd, i0, hd, cs, sn) : o;
+    for (int s = s0 + warp; s < s1; s += NW) {
+      float4 k4 = make_float4(0.f, 0.f, 0.f, 0.f), v4 = k4;
+      if (act) {
+        if (s == t) {                    // the new position: RoPE'd k from this step's projection
+          k4 = rope4(P.qkv + P.d + g * hd, i0, hd, cs, sn);
+          v4 = __ldcg(reinterpret_cast<const float4*>(P.qkv + P.d + P.dkv + g * hd + i0));
+          if (h % qh == 0) {             // runtime.py:355-356 (KV append)
+            *reinterpret_cast<float4*>(kc + (size_t)t * P.dkv + g * hd + i0) = k4;
+            *reinterpret_cast<float4*>(vc + (size_t)t * P.dkv + g * hd + i0) = v4;
+          }
+        } else {
+          const size_t off = (size_t)s * P.dkv + g * hd + i0;
+          k4 = __ldcg(reinterpret_cast<const float4*>(kc + off));
+          v4 = __ldcg(reinterpret_cast<const float4*>(vc + off));
         }
       }
-      CSYNC();
+      const float a = wsum(dot4(q4, k4)) * scale;            // runtime.py:358
+      const float mn = fmaxf(m, a);
+      const float corr = expf(m - mn), p = expf(a - mn);     // runtime.py:359-361
+      l = l * corr + p;
+      o.x = o.x * corr + p * v4.x; o.y = o.y * corr + p * v4.y;
+      o.z = o.z * corr + p * v4.z; o.w = o.w * corr + p * v4.w;
+      m = mn;
     }
-    // scores (runtime.py:358): one warp per position
-    for (int sp = warp; sp < ns; sp += NW) {
-      float a = 0.f;
-      for (int i = lane; i < hd; i += 32) a += q[i] * Ks[sp * hd + i];
-      a = wsum(a);
-      if (lane == 0) sc[sp] = a * scale;
-    }
+    CSYNC();                                 // previous unit's readers of part / outv done
+    if (act) *reinterpret_cast<float4*>(part + warp * ps + i0) = o;
+    if (lane == 0) { part[warp * ps + hd] = m; part[warp * ps + hd + 1] = l; }
     CSYNC();
-    // softmax over the chunk (runtime.py:359-361), warp 0
-    if (warp == 0) {
-      float mx = -CUDART_INF_F;
-      for (int sp = lane; sp < ns; sp += 32) mx = fmaxf(mx, sc[sp]);
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      float l = 0.f;
-      for (int sp = lane; sp < ns; sp += 32) {
-        const float e = expf(sc[sp] - mx);
-        sc[sp] = e;
-        l += e;
+    // merge the warps (fixed order): thread i = dim i
+    if (tid < hd) {
+      float M = -CUDART_INF_F;
+      for (int w = 0; w < NW; ++w) M = fmaxf(M, part[w * ps + hd]);
+      float L = 0.f, acc = 0.f;
+      for (int w = 0; w < NW; ++w) {
+        const float mw = part[w * ps + hd];
+        if (mw == -CUDART_INF_F) continue;   // warp had no position
+        const float e = expf(mw - M);
+        L += part[w * ps + hd + 1] * e;
+        acc += part[w * ps + tid] * e;
       }
-      l = wsum(l);
-      if (lane == 0) { stat[0] = mx; stat[1] = l; }
-    }
-    CSYNC();
-    // o = sum_s p_s v_s (runtime.py:362)
-    for (int i = tid; i < hd; i += NT) {
-      float acc = 0.f;
-      for (int sp = 0; sp < ns; ++sp) acc += sc[sp] * Vs[sp * hd + i];
-      if (nch == 1) P.attn[h * hd + i] = acc / stat[1];
-      else P.attn_part[((size_t)h * P.attn_max_chunks + ch) * (hd + 2) + i] = acc;
+      if (nch == 1) {
+        const float r = acc / L;            // runtime.py:362
+        P.attn[h * hd + tid] = r;
+        outv[tid] = r;
+      } else {
+        float* pp = P.attn_part + ((size_t)h * P.attn_max_chunks + ch) * (hd + 2);
+        pp[tid] = acc;
+        if (tid == 0) { pp[hd] = M; pp[hd + 1] = L; }
+      }
     }
     if (nch == 1) {
       CSYNC();
-      if (P.attn_emit) attn_emit_head(P, C, inst, h);
+      if (P.attn_emit) attn_emit_head(P, C, inst, h, outv);
       continue;
-    }
-    if (tid == 0) {
-      float* pp = P.attn_part + ((size_t)h * P.attn_max_chunks + ch) * (hd + 2);
-      pp[hd] = stat[0];
-      pp[hd + 1] = stat[1];
     }
     __threadfence();
     CSYNC();
@@ -1271,20 +1290,22 @@ __device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, flo
     if (!*s_last) continue;
     __threadfence();
     const float* base = P.attn_part + (size_t)h * P.attn_max_chunks * (hd + 2);
-    for (int i = tid; i < hd; i += NT) {
+    if (tid < hd) {
       float M = -CUDART_INF_F;
       for (int c = 0; c < nch; ++c) M = fmaxf(M, __ldcg(base + c * (hd + 2) + hd));
       float Ls = 0.f, acc = 0.f;
       for (int c = 0; c < nch; ++c) {
         const float e = expf(__ldcg(base + c * (hd + 2) + hd) - M);
         Ls += __ldcg(base + c * (hd + 2) + hd + 1) * e;
-        acc += __ldcg(base + c * (hd + 2) + i) * e;
+        acc += __ldcg(base + c * (hd + 2) + tid) * e;
       }
-      P.attn[h * hd + i] = acc / Ls;
+      const float r = acc / Ls;
+      P.attn[h * hd + tid] = r;
+      outv[tid] = r;
     }
     if (tid == 0) P.attn_cnt[h] = 0u;
     CSYNC();
-    if (P.attn_emit) attn_emit_head(P, C, inst, h);
+    if (P.attn_emit) attn_emit_head(P, C, inst, h, outv);
   }
 }
 
