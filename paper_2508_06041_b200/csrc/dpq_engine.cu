@@ -1160,7 +1160,8 @@ __device__ __noinline__ void producer(const Prog& P, Smem& sm, int cta, int G, i
 // are merged in shared memory in fixed warp order. Chunk partials of a head
 // are merged by the last unit of the head. The unit holding position t of the
 // first query head of each KV group appends k_t / v_t (runtime.py:355-356).
-constexpr int kAttnChunkE = 32;
+constexpr int kAttnPerWarp = 16;                 // positions per warp and chunk
+constexpr int kAttnChunkE = NW * kAttnPerWarp;   // positions per unit
 
 // RoPE of 4 consecutive dims [i0, i0 + 4) of a head vector v (i0 % 4 == 0).
 __device__ __forceinline__ float4 rope4(const float* v, int i0, int hd, const float* c, const float* s) {
@@ -1201,7 +1202,8 @@ __device__ __noinline__ void attn_emit_head(const Prog& P, const ECtl& C, int in
   }
 }
 
-__device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, float* sh, int cta, int G, int* s_last) {
+__device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, float* sh, int cta, int G, int* s_last,
+                                       unsigned long long wait_target, bool do_wait, unsigned long long* stamp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t = C.pos, n = t + 1;
   const int hd = P.hd, qh = P.H / P.KV, nv = hd / 4;
@@ -1215,35 +1217,57 @@ __device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, flo
   const int inst = 4 * b + 1;
   // G^T blocks the attention output feeds (o-proj estimators) -> L2
   if (warp == NW - 1) prefetch_feeds_l2(P, C, inst, P.d, cta, G);
+  // shared memory (LUT region): per-warp partials [NW][hd + 4], merged head output [hd]
   const int ps = hd + 4;                   // part row stride (16-byte aligned)
-  float* part = sh;                        // [NW][ps]: o, m, l of each warp
-  float* outv = sh + NW * ps;              // [hd] merged head output
+  float* part = sh;
+  float* outv = part + NW * ps;
+  const bool act = lane < nv;
+  const int i0 = 4 * lane;
+  // positions s0 + warp + NW j of a unit stream through a 2-deep register
+  // pipeline; the first row of the CTA's first unit (cached positions do not
+  // depend on this step) is loaded before the barrier
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 ka = z4, va = z4;
+#define ATTN_ROW(s_, lim_, g_, K_, V_)                                             \
+  do {                                                                             \
+    if (act && (s_) < (lim_)) {                                                    \
+      const size_t off_ = (size_t)(s_) * P.dkv + (g_) * hd + i0;                   \
+      K_ = __ldcg(reinterpret_cast<const float4*>(kc + off_));                     \
+      V_ = __ldcg(reinterpret_cast<const float4*>(vc + off_));                     \
+    }                                                                              \
+  } while (0)
+  if (cta < units) {
+    const int h_ = cta / nch, s0_ = (cta - h_ * nch) * kAttnChunkE;
+    ATTN_ROW(s0_ + warp, min(t, s0_ + kAttnChunkE), h_ / qh, ka, va);
+  }
+  if (do_wait) bar_wait(P, wait_target);
+  if (stamp && tid == 0) stamp[0] = gclock();
+  if (tid == 0) CSTAMP(stamp, 0);
   for (int u = cta; u < units; u += G) {
     const int h = u / nch, ch = u - h * nch;
     const int g = h / qh;
+    unsigned long long* stp = (tid == 0 && u == cta) ? stamp : nullptr;
     const int s0 = ch * kAttnChunkE, s1 = min(n, s0 + kAttnChunkE);
-    // per-warp online softmax over positions s0 + warp + NW k (lane = dims 4 lane .. 4 lane + 3)
+    const int lim = min(t, s1);            // cached rows of the chunk: [s0, lim)
+    if (u != cta) ATTN_ROW(s0 + warp, lim, g, ka, va);
+    // per-warp online softmax (lane = dims 4 lane .. 4 lane + 3)
     float m = -CUDART_INF_F, l = 0.f;
-    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-    const bool act = lane < nv;
-    const int i0 = 4 * lane;
+    float4 o = z4;
     const float4 q4 = act ? rope4(P.qkv + h * hd, i0, hd, cs, sn) : o;
-    for (int s = s0 + warp; s < s1; s += NW) {
-      float4 k4 = make_float4(0.f, 0.f, 0.f, 0.f), v4 = k4;
-      if (act) {
-        if (s == t) {                    // the new position: RoPE'd k from this step's projection
-          k4 = rope4(P.qkv + P.d + g * hd, i0, hd, cs, sn);
-          v4 = __ldcg(reinterpret_cast<const float4*>(P.qkv + P.d + P.dkv + g * hd + i0));
-          if (h % qh == 0) {             // runtime.py:355-356 (KV append)
-            *reinterpret_cast<float4*>(kc + (size_t)t * P.dkv + g * hd + i0) = k4;
-            *reinterpret_cast<float4*>(vc + (size_t)t * P.dkv + g * hd + i0) = v4;
-          }
-        } else {
-          const size_t off = (size_t)s * P.dkv + g * hd + i0;
-          k4 = __ldcg(reinterpret_cast<const float4*>(kc + off));
-          v4 = __ldcg(reinterpret_cast<const float4*>(vc + off));
-        }
+    CSTAMP(q4.x == 1.2345e-30f ? nullptr : stp, 1);         // after the q loads landed
+    float4 kt = o, vt = o;
+    if (act && s1 == n && (t - s0) % NW == warp) {          // this warp holds the new position t
+      kt = rope4(P.qkv + P.d + g * hd, i0, hd, cs, sn);      // RoPE'd k of this step
+      vt = __ldcg(reinterpret_cast<const float4*>(P.qkv + P.d + P.dkv + g * hd + i0));
+      if (h % qh == 0) {                 // runtime.py:355-356 (KV append)
+        *reinterpret_cast<float4*>(kc + (size_t)t * P.dkv + g * hd + i0) = kt;
+        *reinterpret_cast<float4*>(vc + (size_t)t * P.dkv + g * hd + i0) = vt;
       }
+    }
+    for (int s = s0 + warp; s < s1; s += NW) {
+      float4 kb = z4, vb = z4;
+      ATTN_ROW(s + NW, lim, g, kb, vb);  // next row in flight
+      const float4 k4 = s == t ? kt : ka, v4 = s == t ? vt : va;
       const float a = wsum(dot4(q4, k4)) * scale;            // runtime.py:358
       const float mn = fmaxf(m, a);
       const float corr = expf(m - mn), p = expf(a - mn);     // runtime.py:359-361
@@ -1251,16 +1275,22 @@ __device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, flo
       o.x = o.x * corr + p * v4.x; o.y = o.y * corr + p * v4.y;
       o.z = o.z * corr + p * v4.z; o.w = o.w * corr + p * v4.w;
       m = mn;
+      ka = kb;
+      va = vb;
     }
+    CSTAMP(stp, 2);
     CSYNC();                                 // previous unit's readers of part / outv done
     if (act) *reinterpret_cast<float4*>(part + warp * ps + i0) = o;
     if (lane == 0) { part[warp * ps + hd] = m; part[warp * ps + hd + 1] = l; }
     CSYNC();
+    CSTAMP(stp, 3);
     // merge the warps (fixed order): thread i = dim i
     if (tid < hd) {
       float M = -CUDART_INF_F;
+#pragma unroll 1
       for (int w = 0; w < NW; ++w) M = fmaxf(M, part[w * ps + hd]);
       float L = 0.f, acc = 0.f;
+#pragma unroll 1
       for (int w = 0; w < NW; ++w) {
         const float mw = part[w * ps + hd];
         if (mw == -CUDART_INF_F) continue;   // warp had no position
@@ -1280,7 +1310,9 @@ __device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, flo
     }
     if (nch == 1) {
       CSYNC();
+      CSTAMP(stp, 4);
       if (P.attn_emit) attn_emit_head(P, C, inst, h, outv);
+      CSTAMP(stp, 5);
       continue;
     }
     __threadfence();
@@ -1292,8 +1324,10 @@ __device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, flo
     const float* base = P.attn_part + (size_t)h * P.attn_max_chunks * (hd + 2);
     if (tid < hd) {
       float M = -CUDART_INF_F;
+#pragma unroll 1
       for (int c = 0; c < nch; ++c) M = fmaxf(M, __ldcg(base + c * (hd + 2) + hd));
       float Ls = 0.f, acc = 0.f;
+#pragma unroll 1
       for (int c = 0; c < nch; ++c) {
         const float e = expf(__ldcg(base + c * (hd + 2) + hd) - M);
         Ls += __ldcg(base + c * (hd + 2) + hd + 1) * e;
@@ -1305,8 +1339,11 @@ __device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, flo
     }
     if (tid == 0) P.attn_cnt[h] = 0u;
     CSYNC();
+    CSTAMP(stp, 4);
     if (P.attn_emit) attn_emit_head(P, C, inst, h, outv);
+    CSTAMP(stp, 5);
   }
+  if (tid == 0) CSTAMP(stamp, 6);
 }
 
 // EMIT: statistics + feeds of a whole vector (attention output when heads
@@ -1489,8 +1526,8 @@ extern "C" __global__ void __launch_bounds__(NTB, 1) engine_kernel(const Prog Pk
         ++op_no;
         wi ^= 1;
       } else {
-        if (wait) bar_wait(P, target);
-        if (P.dbg && tid == 0) P.dbg[((size_t)si * G + cta) * kDbgRec] = gclock();
+        if (wait && st.x != ST_ATTN) bar_wait(P, target);     // attention waits after its K/V prefetch
+        if (P.dbg && tid == 0 && st.x != ST_ATTN) P.dbg[((size_t)si * G + cta) * kDbgRec] = gclock();
         if (st.x == ST_BEGIN) {
           read_ctl(P, C);
           if (tid == 0) {
@@ -1499,7 +1536,8 @@ extern "C" __global__ void __launch_bounds__(NTB, 1) engine_kernel(const Prog Pk
           }
           begin_stage(P, C, cta, G);
         } else if (st.x == ST_ATTN) {
-          attn_stage(P, C, st.y, lut, cta, G, &s_last);
+          attn_stage(P, C, st.y, lut, cta, G, &s_last, target, wait,
+                     P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr);
         } else if (st.x == ST_EMIT) {
           emit_stage(P, C, P.attn, P.d, 4 * st.y + 1, cta, G);
         } else {
