@@ -496,7 +496,7 @@ __device__ __forceinline__ void emit_stats(const Prog& P, const ECtl& C, int ins
 
 // Feed fi (an estimator reading the vector) with tile `tile`: G_tile^T v
 // partials and sum v^2 into its fixed-point accumulators (a warp, lane = row).
-__device__ __noinline__ void emit_feed(const Prog& P, const ECtl& C, int fi, int tile, float v) {
+__device__ __forceinline__ void emit_feed(const Prog& P, const ECtl& C, int fi, int tile, float v) {
   const int lane = threadIdx.x & 31;
   Feed F;
   {
@@ -569,7 +569,7 @@ __device__ __noinline__ void emit_feed(const Prog& P, const ECtl& C, int fi, int
 }
 
 // Statistics + every feed of one tile (one warp).
-__device__ __noinline__ void emit_tile(const Prog& P, const ECtl& C, int inst, int tile, float v) {
+__device__ __forceinline__ void emit_tile(const Prog& P, const ECtl& C, int inst, int tile, float v) {
   emit_stats(P, C, inst, v);
   for (int fi = P.feed_begin[inst]; fi < P.feed_begin[inst + 1]; ++fi) emit_feed(P, C, fi, tile, v);
 }
@@ -649,7 +649,7 @@ __device__ __forceinline__ void prefetch_work_l2(const Op& O, const Work& W, int
 }
 
 // L2 prefetch of slice cta/G of the G^T blocks the op's output feeds.
-__device__ __noinline__ void prefetch_feeds_l2(const Prog& P, const ECtl& C, int inst, int n, int cta, int G) {
+__device__ __forceinline__ void prefetch_feeds_l2(const Prog& P, const ECtl& C, int inst, int n, int cta, int G) {
   if (inst < 0 || C.mode != MODE_DYNAMIC && !C.prime) return;
   const int nt = (n + 31) / 32;
   for (int fi = P.feed_begin[inst] + (int)threadIdx.x; fi < P.feed_begin[inst + 1]; fi += NT) {
@@ -723,7 +723,7 @@ __device__ __forceinline__ float tile_y(const Prog& P, const Op& O, const Work& 
 // Reduce unit u (tile, or up|gate tile pair) of op O: window sum, affine
 // epilogue, residual add / SiLU (runtime.py:364-370), output store. Returns the
 // value the output instance is fed with (0 for padding rows) and its tile.
-__device__ __noinline__ float reduce_unit(const Prog& P, const Op& O, const Work& W, const Smem& sm, int u,
+__device__ __forceinline__ float reduce_unit(const Prog& P, const Op& O, const Work& W, const Smem& sm, int u,
                                           unsigned epoch, int& etile) {
   const int lane = threadIdx.x & 31;
   // independent operands first (they do not wait for the window slots)
@@ -779,7 +779,7 @@ __device__ __noinline__ float reduce_unit(const Prog& P, const Op& O, const Work
 // B: the estimator feeds of the output instance, one (unit, feed) task per
 // warp in parallel (independent fixed-point sums). Warp NW - 1 first prepares
 // the next op's descriptor and work.
-__device__ __noinline__ void reduce_duty(const Prog& P, const ECtl& C, const Op& O, const Work& W, Smem& sm,
+__device__ __forceinline__ void reduce_duty(const Prog& P, const ECtl& C, const Op& O, const Work& W, Smem& sm,
                                           int cta, int G, unsigned epoch, Op* On, Work* Wn, const Op* On_global) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n_units = O.pair ? O.L[0].n_tiles : O.n_tiles;
@@ -818,7 +818,7 @@ __device__ __noinline__ void reduce_duty(const Prog& P, const ECtl& C, const Op&
 // run, planes [0, nb); then extra items for runs in reverse order, planes
 // [nb, fin). Returns the total and fills per-run offsets (lane-parallel).
 // Returns the number of ring items the op consumed (FIFO advance).
-__device__ __noinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, Work& W, Op* On, Work* Wn,
+__device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, Work& W, Op* On, Work* Wn,
                                      const Op* On_global, Smem& sm, int cta, int G,
                                      unsigned long long wait_target, bool do_wait, unsigned long long* stamp,
                                      int op_no, int j_op) {
@@ -1058,7 +1058,7 @@ __device__ __noinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, 
 // ahead of the consumers across stage barriers (bounded by ring space, and by
 // each op's decision for its extra planes).
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void producer(const Prog& P, Smem& sm, int cta, int G, int n_steps) {
+__device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G, int n_steps) {
   const int lane = threadIdx.x & 31;
   int j = 0, op_no = 0;
   const unsigned char* dyn0 = reinterpret_cast<const unsigned char*>(&sm);
@@ -1188,7 +1188,7 @@ __device__ __forceinline__ float dot4(float4 a, float4 b) { return a.x * b.x + a
 
 // Statistics + feeds of head h's output tiles (values in vals[hd]): one
 // (tile, feed) task per warp.
-__device__ __noinline__ void attn_emit_head(const Prog& P, const ECtl& C, int inst, int h, const float* vals) {
+__device__ __forceinline__ void attn_emit_head(const Prog& P, const ECtl& C, int inst, int h, const float* vals) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nt = (P.hd + 31) / 32;
   const int f0 = P.feed_begin[inst], nf = P.feed_begin[inst + 1] - f0;
@@ -1202,7 +1202,7 @@ __device__ __noinline__ void attn_emit_head(const Prog& P, const ECtl& C, int in
   }
 }
 
-__device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, float* sh, int cta, int G, int* s_last,
+__device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, float* sh, int cta, int G, int* s_last,
                                        unsigned long long wait_target, bool do_wait, unsigned long long* stamp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t = C.pos, n = t + 1;
@@ -1348,7 +1348,7 @@ __device__ __noinline__ void attn_stage(const Prog& P, const ECtl& C, int b, flo
 
 // EMIT: statistics + feeds of a whole vector (attention output when heads
 // are not 32-aligned).
-__device__ __noinline__ void emit_stage(const Prog& P, const ECtl& C, const float* v, int n, int inst, int cta, int G) {
+__device__ __forceinline__ void emit_stage(const Prog& P, const ECtl& C, const float* v, int n, int inst, int cta, int G) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n_t = (n + 31) / 32;
   for (int tt = cta * NW + warp; tt < n_t; tt += G * NW) {
@@ -1361,7 +1361,7 @@ __device__ __noinline__ void emit_stage(const Prog& P, const ECtl& C, const floa
 // Head stage: final RMSNorm + lm_head logits (runtime.py:372), greedy argmax
 // (runtime.py:405-408) and the end-of-step control update (runtime.py:373-380).
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void head_stage(const Prog& P, const ECtl& C, Smem& sm, int cta, int G) {
+__device__ __forceinline__ void head_stage(const Prog& P, const ECtl& C, Smem& sm, int cta, int G) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cur = C.n_steps_done & 1;
   const int fin_inst = 4 * P.n_blocks;
@@ -1437,7 +1437,7 @@ __device__ __noinline__ void head_stage(const Prog& P, const ECtl& C, Smem& sm, 
 
 // BEGIN: zero the next step's accumulator slots, x = embed[token]
 // (runtime.py:345) with its statistics and block-0 estimator feeds.
-__device__ __noinline__ void begin_stage(const Prog& P, const ECtl& C, int cta, int G) {
+__device__ __forceinline__ void begin_stage(const Prog& P, const ECtl& C, int cta, int G) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nxt = (C.n_steps_done + 1) & 1;
   {
