@@ -1161,25 +1161,23 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
 // are merged by the last unit of the head. The unit holding position t of the
 // first query head of each KV group appends k_t / v_t (runtime.py:355-356).
 constexpr int kAttnPerWarp = 16;                 // positions per warp and chunk
+constexpr int kAttnStaged = 3;                   // of which staged in shared memory (LUT region)
 constexpr int kAttnChunkE = NW * kAttnPerWarp;   // positions per unit
 
-// RoPE of 4 consecutive dims [i0, i0 + 4) of a head vector v (i0 % 4 == 0).
-__device__ __forceinline__ float4 rope4(const float* v, int i0, int hd, const float* c, const float* s) {
+// RoPE of 4 consecutive dims [i0, i0 + 4) of a head vector v (i0 % 4 == 0,
+// hd % 8 == 0), with the position's cos / sin of those dims preloaded.
+__device__ __forceinline__ float4 rope4(const float* v, int i0, int hd, float4 c, float4 s) {
   const int half = hd / 2;
-  const float4 a = __ldcg(reinterpret_cast<const float4*>(v + i0));
-  if (i0 >= 2 * half) return a;                                  // odd hd tail: identity
   const bool lo = i0 < half;
-  const int j0 = lo ? i0 : i0 - half;                            // index into cos / sin
+  const float4 a = __ldcg(reinterpret_cast<const float4*>(v + i0));
   const float4 b = __ldcg(reinterpret_cast<const float4*>(v + (lo ? i0 + half : i0 - half)));
-  const float cc[4] = {__ldg(c + j0), __ldg(c + j0 + 1), __ldg(c + j0 + 2), __ldg(c + j0 + 3)};
-  const float ss[4] = {__ldg(s + j0), __ldg(s + j0 + 1), __ldg(s + j0 + 2), __ldg(s + j0 + 3)};
   float4 r;
   if (lo) {   // x_i c_i - x_{i+half} s_i
-    r.x = a.x * cc[0] - b.x * ss[0]; r.y = a.y * cc[1] - b.y * ss[1];
-    r.z = a.z * cc[2] - b.z * ss[2]; r.w = a.w * cc[3] - b.w * ss[3];
+    r.x = a.x * c.x - b.x * s.x; r.y = a.y * c.y - b.y * s.y;
+    r.z = a.z * c.z - b.z * s.z; r.w = a.w * c.w - b.w * s.w;
   } else {    // x_{i-half} s_j + x_i c_j
-    r.x = b.x * ss[0] + a.x * cc[0]; r.y = b.y * ss[1] + a.y * cc[1];
-    r.z = b.z * ss[2] + a.z * cc[2]; r.w = b.w * ss[3] + a.w * cc[3];
+    r.x = b.x * s.x + a.x * c.x; r.y = b.y * s.y + a.y * c.y;
+    r.z = b.z * s.z + a.z * c.z; r.w = b.w * s.w + a.w * c.w;
   }
   return r;
 }
@@ -1217,17 +1215,34 @@ __device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, 
   const int inst = 4 * b + 1;
   // G^T blocks the attention output feeds (o-proj estimators) -> L2
   if (warp == NW - 1) prefetch_feeds_l2(P, C, inst, P.d, cta, G);
-  // shared memory (LUT region): per-warp partials [NW][hd + 4], merged head output [hd]
+  // shared memory (LUT region): K / V staging [NW][kAttnStaged][2][hd], the
+  // per-warp partials [NW][hd + 4] and the merged head output [hd]
+  float* kvs = sh;
   const int ps = hd + 4;                   // part row stride (16-byte aligned)
-  float* part = sh;
+  float* part = sh + NW * kAttnStaged * 2 * hd;
   float* outv = part + NW * ps;
   const bool act = lane < nv;
   const int i0 = 4 * lane;
-  // positions s0 + warp + NW j of a unit stream through a 2-deep register
-  // pipeline; the first row of the CTA's first unit (cached positions do not
-  // depend on this step) is loaded before the barrier
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 ka = z4, va = z4;
+  // Rows of unit positions s0 + warp + NW j: j < kAttnStaged are copied
+  // asynchronously into shared memory (for the CTA's first unit before the
+  // barrier: cached positions do not depend on this step; a lane copies and
+  // later reads only its own 16 bytes), the rest stream through a 4-deep
+  // register pipeline.
+#define ATTN_STAGE_ROWS(u_)                                                              \
+  do {                                                                                   \
+    const int h_ = (u_) / nch, g_ = h_ / qh;                                             \
+    const int s0_ = ((u_) - h_ * nch) * kAttnChunkE, lim_ = min(t, s0_ + kAttnChunkE);   \
+    _Pragma("unroll") for (int j = 0; j < kAttnStaged; ++j) {                            \
+      const int s_ = s0_ + warp + NW * j;                                                \
+      if (act && s_ < lim_) {                                                            \
+        const size_t off_ = (size_t)s_ * P.dkv + g_ * hd + i0;                           \
+        float* d_ = kvs + ((warp * kAttnStaged + j) * 2) * hd + i0;                      \
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_u32(d_)), "l"(kc + off_) : "memory"); \
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_u32(d_ + hd)), "l"(vc + off_) : "memory"); \
+      }                                                                                  \
+    }                                                                                    \
+  } while (0)
 #define ATTN_ROW(s_, lim_, g_, K_, V_)                                             \
   do {                                                                             \
     if (act && (s_) < (lim_)) {                                                    \
@@ -1236,10 +1251,10 @@ __device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, 
       V_ = __ldcg(reinterpret_cast<const float4*>(vc + off_));                     \
     }                                                                              \
   } while (0)
-  if (cta < units) {
-    const int h_ = cta / nch, s0_ = (cta - h_ * nch) * kAttnChunkE;
-    ATTN_ROW(s0_ + warp, min(t, s0_ + kAttnChunkE), h_ / qh, ka, va);
-  }
+  if (cta < units) ATTN_STAGE_ROWS(cta);
+  const int j0 = i0 < hd / 2 ? i0 : i0 - hd / 2;
+  const float4 c4 = act ? __ldg(reinterpret_cast<const float4*>(cs + j0)) : z4;
+  const float4 s4 = act ? __ldg(reinterpret_cast<const float4*>(sn + j0)) : z4;
   if (do_wait) bar_wait(P, wait_target);
   if (stamp && tid == 0) stamp[0] = gclock();
   if (tid == 0) CSTAMP(stamp, 0);
@@ -1249,34 +1264,61 @@ __device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, 
     unsigned long long* stp = (tid == 0 && u == cta) ? stamp : nullptr;
     const int s0 = ch * kAttnChunkE, s1 = min(n, s0 + kAttnChunkE);
     const int lim = min(t, s1);            // cached rows of the chunk: [s0, lim)
-    if (u != cta) ATTN_ROW(s0 + warp, lim, g, ka, va);
+    if (u != cta) {
+      CSYNC();                             // previous unit's readers of the staging done
+      ATTN_STAGE_ROWS(u);
+    }
+    // register pipeline rows (j = kAttnStaged ...)
+    const int sr = s0 + warp + NW * kAttnStaged;
+    float4 k0 = z4, v0 = z4, k1 = z4, v1 = z4, k2 = z4, v2 = z4, k3 = z4, v3 = z4;
+    ATTN_ROW(sr, lim, g, k0, v0);
+    ATTN_ROW(sr + NW, lim, g, k1, v1);
+    ATTN_ROW(sr + 2 * NW, lim, g, k2, v2);
+    ATTN_ROW(sr + 3 * NW, lim, g, k3, v3);
     // per-warp online softmax (lane = dims 4 lane .. 4 lane + 3)
     float m = -CUDART_INF_F, l = 0.f;
     float4 o = z4;
-    const float4 q4 = act ? rope4(P.qkv + h * hd, i0, hd, cs, sn) : o;
+    const float4 q4 = act ? rope4(P.qkv + h * hd, i0, hd, c4, s4) : o;
     CSTAMP(q4.x == 1.2345e-30f ? nullptr : stp, 1);         // after the q loads landed
     float4 kt = o, vt = o;
     if (act && s1 == n && (t - s0) % NW == warp) {          // this warp holds the new position t
-      kt = rope4(P.qkv + P.d + g * hd, i0, hd, cs, sn);      // RoPE'd k of this step
+      kt = rope4(P.qkv + P.d + g * hd, i0, hd, c4, s4);      // RoPE'd k of this step
       vt = __ldcg(reinterpret_cast<const float4*>(P.qkv + P.d + P.dkv + g * hd + i0));
       if (h % qh == 0) {                 // runtime.py:355-356 (KV append)
         *reinterpret_cast<float4*>(kc + (size_t)t * P.dkv + g * hd + i0) = kt;
         *reinterpret_cast<float4*>(vc + (size_t)t * P.dkv + g * hd + i0) = vt;
       }
     }
-    for (int s = s0 + warp; s < s1; s += NW) {
-      float4 kb = z4, vb = z4;
-      ATTN_ROW(s + NW, lim, g, kb, vb);  // next row in flight
-      const float4 k4 = s == t ? kt : ka, v4 = s == t ? vt : va;
-      const float a = wsum(dot4(q4, k4)) * scale;            // runtime.py:358
-      const float mn = fmaxf(m, a);
-      const float corr = expf(m - mn), p = expf(a - mn);     // runtime.py:359-361
-      l = l * corr + p;
-      o.x = o.x * corr + p * v4.x; o.y = o.y * corr + p * v4.y;
-      o.z = o.z * corr + p * v4.z; o.w = o.w * corr + p * v4.w;
-      m = mn;
-      ka = kb;
-      va = vb;
+#define ATTN_UPDATE(s_, K_, V_)                                                    \
+    {                                                                              \
+      const float4 k4 = (s_) == t ? kt : K_, v4 = (s_) == t ? vt : V_;             \
+      const float a = wsum(dot4(q4, k4)) * scale;            /* runtime.py:358 */  \
+      const float mn = fmaxf(m, a);                                                \
+      const float corr = expf(m - mn), p = expf(a - mn);     /* runtime.py:359-361 */ \
+      l = l * corr + p;                                                            \
+      o.x = o.x * corr + p * v4.x; o.y = o.y * corr + p * v4.y;                    \
+      o.z = o.z * corr + p * v4.z; o.w = o.w * corr + p * v4.w;                    \
+      m = mn;                                                                      \
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < kAttnStaged; ++j) {
+      const int s = s0 + warp + NW * j;
+      if (s < s1) {
+        const float* r_ = kvs + ((warp * kAttnStaged + j) * 2) * hd + i0;
+        const float4 ks = act ? *reinterpret_cast<const float4*>(r_) : z4;
+        const float4 vs = act ? *reinterpret_cast<const float4*>(r_ + hd) : z4;
+        ATTN_UPDATE(s, ks, vs)
+      }
+    }
+#define ATTN_STEP(s_, K_, V_)                                                      \
+    if ((s_) < s1) ATTN_UPDATE(s_, K_, V_)                                         \
+    ATTN_ROW((s_) + 4 * NW, lim, g, K_, V_);   /* refill this register slot */
+    for (int s = sr; s < s1; s += 4 * NW) {
+      ATTN_STEP(s, k0, v0)
+      ATTN_STEP(s + NW, k1, v1)
+      ATTN_STEP(s + 2 * NW, k2, v2)
+      ATTN_STEP(s + 3 * NW, k3, v3)
     }
     CSTAMP(stp, 2);
     CSYNC();                                 // previous unit's readers of part / outv done
@@ -1287,10 +1329,10 @@ __device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, 
     // merge the warps (fixed order): thread i = dim i
     if (tid < hd) {
       float M = -CUDART_INF_F;
-#pragma unroll 1
+#pragma unroll
       for (int w = 0; w < NW; ++w) M = fmaxf(M, part[w * ps + hd]);
       float L = 0.f, acc = 0.f;
-#pragma unroll 1
+#pragma unroll
       for (int w = 0; w < NW; ++w) {
         const float mw = part[w * ps + hd];
         if (mw == -CUDART_INF_F) continue;   // warp had no position
