@@ -496,7 +496,19 @@ __device__ __forceinline__ void emit_stats(const Prog& P, const ECtl& C, int ins
 
 // Feed fi (an estimator reading the vector) with tile `tile`: G_tile^T v
 // partials and sum v^2 into its fixed-point accumulators (a warp, lane = row).
-__device__ __forceinline__ void emit_feed(const Prog& P, const ECtl& C, int fi, int tile, float v) {
+// G^T block of feed F for tile `tile` (f16, k <= 64: the common case) into
+// registers ahead of the value it is applied to.
+__device__ __forceinline__ bool feed_preload(const Prog& P, int fi, int tile, uint4 (&c)[8]) {
+  const Feed* F = P.feeds + fi;
+  if (!F->Gt || !F->f16 || F->kpad != 64) return false;
+  const uint4* blk = F->Gt + (size_t)tile * 256 + (threadIdx.x & 31);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i] = __ldg(blk + 32 * i);
+  return true;
+}
+
+__device__ __forceinline__ void emit_feed(const Prog& P, const ECtl& C, int fi, int tile, float v,
+                                          const uint4 (*pre)[8] = nullptr) {
   const int lane = threadIdx.x & 31;
   Feed F;
   {
@@ -527,7 +539,7 @@ __device__ __forceinline__ void emit_feed(const Prog& P, const ECtl& C, int fi, 
         const uint4* blk = F.Gt + ((size_t)tile * nsub + sub) * 256 + lane;
         uint4 c[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) c[i] = __ldg(blk + 32 * i);
+        for (int i = 0; i < 8; ++i) c[i] = pre ? (*pre)[i] : __ldg(blk + 32 * i);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const __half2* hh = reinterpret_cast<const __half2*>(&c[i]);
@@ -794,6 +806,8 @@ __device__ __forceinline__ void reduce_duty(const Prog& P, const ECtl& C, const 
     __syncwarp();
     if (lane == 0) Wn->valid = 1;
   }
+  const int f0 = O.out_inst >= 0 ? P.feed_begin[O.out_inst] : 0;
+  const int nf = O.out_inst >= 0 ? P.feed_begin[O.out_inst + 1] - f0 : 0;
   for (int i = warp; i < mine; i += NW) {
     int et;
     const float v = reduce_unit(P, O, W, sm, cta + i * G, epoch, et);
@@ -803,8 +817,6 @@ __device__ __forceinline__ void reduce_duty(const Prog& P, const ECtl& C, const 
       if (lane == 0) sm.vtile[i] = et;
     }
   }
-  if (O.out_inst < 0) return;
-  const int f0 = P.feed_begin[O.out_inst], nf = P.feed_begin[O.out_inst + 1] - f0;
   if (nf == 0) return;
   CSYNC();
   for (int q = warp; q < mine * nf; q += NW) {
@@ -854,8 +866,13 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
   const int w_first = sm.runs.n > 0 ? sm.runs.r[0].w : -1;
   const LutSrc xsrc = lut_load(O.in, O.cols, max(w_first, 0));
   // decision warps: accumulator loads in flight (k <= 128: 4 per lane)
-  const bool dec_warp = warp < O.n_layers;
-  const Layer& Ld = O.L[dec_warp ? warp : 0];
+  // roles: warps 0..7 build the LUT (lut_store: threads < 256), warps 8.. take
+  // the decisions (one per layer), the input statistics and the feed prefetch
+  constexpr int kDecW = 8, kStatW = kDecW + kMaxOpLayers, kPfW = kStatW + 1;
+  static_assert(kPfW < NW, "prologue roles need more consumer warps");
+  const int li_d = warp - kDecW;
+  const bool dec_warp = li_d >= 0 && li_d < O.n_layers;
+  const Layer& Ld = O.L[dec_warp ? li_d : 0];
   const bool estimating = dec_warp && C.mode == MODE_DYNAMIC && Ld.sentinel == 0 && Ld.est != EST_NONE;
   long long ga[4] = {0, 0, 0, 0}, gsq = 0;
   if (estimating) {
@@ -867,11 +884,11 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
     gsq = __ldcg(acc + Ld.k);
   }
   long long vs1 = 0, vs2 = 0;
-  if (warp == kMaxOpLayers && lane == 0) {
+  if (warp == kStatW && lane == 0) {
     const long long* vs = P.vstat + ((size_t)cur * P.n_inst + O.in_inst) * 2;
     vs1 = __ldcg(vs);
     vs2 = __ldcg(vs + 1);
-  } else if (warp == kMaxOpLayers + 1) {
+  } else if (warp == kPfW) {
     prefetch_feeds_l2(P, C, O.out_inst, O.n_tiles * 32, cta, G);
   }
   if (tid == 0) CSTAMP(stamp, 1);
@@ -883,7 +900,7 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
   }
   if (tid == 0) CSTAMP(stamp, 2);
   if (dec_warp) {
-    const int li = warp;
+    const int li = li_d;
     int bit = W.nb[li];
     double est = CUDART_NAN;
     if (estimating) {
@@ -910,7 +927,7 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
         P.tr_est[o] = estimating ? (float)est : CUDART_NAN_F;
       }
     }
-  } else if (warp == kMaxOpLayers && lane == 0) {
+  } else if (warp == kStatW && lane == 0) {
     sm.sx = (float)((double)vs1 * (1.0 / kFxSum));
     sm.scale = O.rms ? (float)rsqrt_d((double)vs2 * (1.0 / kFxSq) / (double)O.cols + (double)P.eps) : 1.f;
     CSTAMP(stamp, 7);
