@@ -1285,26 +1285,26 @@ __device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, 
       CSYNC();                             // previous unit's readers of the staging done
       ATTN_STAGE_ROWS(u);
     }
-    // register pipeline rows (j = kAttnStaged ...)
+    // per-warp online softmax (lane = dims 4 lane .. 4 lane + 3)
+    float m = -CUDART_INF_F, l = 0.f;
+    float4 o = z4;
+    const float4 q4 = act ? rope4(P.qkv + h * hd, i0, hd, c4, s4) : o;
+    float4 kt = o, vt = o;
+    const bool own_t = act && s1 == n && (t - s0) % NW == warp;   // this warp holds the new position t
+    if (own_t) {
+      kt = rope4(P.qkv + P.d + g * hd, i0, hd, c4, s4);      // RoPE'd k of this step
+      vt = __ldcg(reinterpret_cast<const float4*>(P.qkv + P.d + P.dkv + g * hd + i0));
+    }
+    // register pipeline rows (j = kAttnStaged ...), in flight with q / k_t / v_t
     const int sr = s0 + warp + NW * kAttnStaged;
     float4 k0 = z4, v0 = z4, k1 = z4, v1 = z4, k2 = z4, v2 = z4, k3 = z4, v3 = z4;
     ATTN_ROW(sr, lim, g, k0, v0);
     ATTN_ROW(sr + NW, lim, g, k1, v1);
     ATTN_ROW(sr + 2 * NW, lim, g, k2, v2);
     ATTN_ROW(sr + 3 * NW, lim, g, k3, v3);
-    // per-warp online softmax (lane = dims 4 lane .. 4 lane + 3)
-    float m = -CUDART_INF_F, l = 0.f;
-    float4 o = z4;
-    const float4 q4 = act ? rope4(P.qkv + h * hd, i0, hd, c4, s4) : o;
-    CSTAMP(q4.x == 1.2345e-30f ? nullptr : stp, 1);         // after the q loads landed
-    float4 kt = o, vt = o;
-    if (act && s1 == n && (t - s0) % NW == warp) {          // this warp holds the new position t
-      kt = rope4(P.qkv + P.d + g * hd, i0, hd, c4, s4);      // RoPE'd k of this step
-      vt = __ldcg(reinterpret_cast<const float4*>(P.qkv + P.d + P.dkv + g * hd + i0));
-      if (h % qh == 0) {                 // runtime.py:355-356 (KV append)
-        *reinterpret_cast<float4*>(kc + (size_t)t * P.dkv + g * hd + i0) = kt;
-        *reinterpret_cast<float4*>(vc + (size_t)t * P.dkv + g * hd + i0) = vt;
-      }
+    if (own_t && h % qh == 0) {          // runtime.py:355-356 (KV append)
+      *reinterpret_cast<float4*>(kc + (size_t)t * P.dkv + g * hd + i0) = kt;
+      *reinterpret_cast<float4*>(vc + (size_t)t * P.dkv + g * hd + i0) = vt;
     }
 #define ATTN_UPDATE(s_, K_, V_)                                                    \
     {                                                                              \
@@ -1340,31 +1340,35 @@ __device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, 
     CSTAMP(stp, 2);
     CSYNC();                                 // previous unit's readers of part / outv done
     if (act) *reinterpret_cast<float4*>(part + warp * ps + i0) = o;
+    // warp weights (fixed order): lane w of every warp computes the global max M
+    // and e_w = exp(m_w - M); L = sum_w e_w l_w
     if (lane == 0) { part[warp * ps + hd] = m; part[warp * ps + hd + 1] = l; }
     CSYNC();
-    CSTAMP(stp, 3);
-    // merge the warps (fixed order): thread i = dim i
-    if (tid < hd) {
-      float M = -CUDART_INF_F;
+    CSTAMP(stp, 7);
+    {
+      const float mw = lane < NW ? part[lane * ps + hd] : -CUDART_INF_F;
+      const float lw = lane < NW ? part[lane * ps + hd + 1] : 0.f;
+      float M = mw;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) M = fmaxf(M, part[w * ps + hd]);
-      float L = 0.f, acc = 0.f;
+      for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+      const float e = mw == -CUDART_INF_F ? 0.f : expf(mw - M);      // warps without positions: 0
+      // fixed-order sum over lanes 0..NW-1 (the shuffle tree is the same in every warp)
+      const float L = wsum(e * lw);
+      const int di = tid < hd ? tid : 0;
+      float acc = 0.f;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const float mw = part[w * ps + hd];
-        if (mw == -CUDART_INF_F) continue;   // warp had no position
-        const float e = expf(mw - M);
-        L += part[w * ps + hd + 1] * e;
-        acc += part[w * ps + tid] * e;
-      }
-      if (nch == 1) {
-        const float r = acc / L;            // runtime.py:362
-        P.attn[h * hd + tid] = r;
-        outv[tid] = r;
-      } else {
-        float* pp = P.attn_part + ((size_t)h * P.attn_max_chunks + ch) * (hd + 2);
-        pp[tid] = acc;
-        if (tid == 0) { pp[hd] = M; pp[hd + 1] = L; }
+      for (int w = 0; w < NW; ++w) acc += __shfl_sync(0xffffffffu, e, w) * part[w * ps + di];
+      CSTAMP(stp, 8);
+      if (tid < hd) {
+        if (nch == 1) {
+          const float r = acc / L;            // runtime.py:362
+          P.attn[h * hd + tid] = r;
+          outv[tid] = r;
+        } else {
+          float* pp = P.attn_part + ((size_t)h * P.attn_max_chunks + ch) * (hd + 2);
+          pp[tid] = acc;
+          if (tid == 0) { pp[hd] = M; pp[hd + 1] = L; }
+        }
       }
     }
     if (nch == 1) {
