@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--g-dtype", default="f16", choices=["f32", "f16", "e4m3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-static", action="store_true")
+    ap.add_argument("--tp", action="store_true",
+                    help="tensor-parallel decode of ONE sequence over the N ranks (strong scaling, "
+                         "paper_2508_06041_b200.tp); default N>1 runs N replicas")
     return ap.parse_args()
 
 
@@ -438,10 +441,73 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_tp(args):
+    """Tensor-parallel decode of one sequence over WORLD_SIZE ranks:
+    row-sharded linears, NCCL all-gather per op group, host-driven steps."""
+    import torch
+    import torch.distributed as dist
+    from paper_2508_06041_b200 import runtime as R
+    from paper_2508_06041_b200 import synth
+    from paper_2508_06041_b200 import tp as TP
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    cfg, n_bits, b_min = model_config(args.config)
+    weights, store, _, sds = synth.random_device_model(cfg, n_bits, b_min, seed=1234, shard=(world, rank))
+    pairs, prefill, high = pairs_for_target(store, args.target)
+    plan = synth.projection_plan(store, pairs, prefill, k=64, seed=0, target=args.target)
+    calib = np.random.default_rng(7).integers(0, cfg.vocab, 48)
+    synth.calibrate_thresholds(weights, store, plan, calib, high_rate=high, g_dtype=args.g_dtype)
+    eng = TP.TPDecodeEngine(weights, store, plan, g_dtype=args.g_dtype, shard_store=sds)
+    prompt = np.random.default_rng(11).integers(0, cfg.vocab, PROMPT)
+    logits = eng.prefill(prompt)
+    tok = int(np.argmax(logits))
+    for _ in range(args.warmup):
+        tok = int(np.argmax(eng.step(tok)))
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        tok = int(np.argmax(eng.step(tok)))       # logits reach the host every step (greedy)
+    torch.cuda.synchronize()
+    s = time.perf_counter() - t0
+    t = torch.tensor([s], dtype=torch.float64)
+    if world > 1:
+        t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) * 1e3 / args.steps
+    eff = float(np.mean([r.effective_bits for r in eng.trace.steps[-args.steps:]]))
+    line = {"metric": METRIC, "value": 1000.0 / ms_per_step, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: random-init weights, random prompt tokens",
+            "config": {"workload": f"{args.config}-shaped batch-1 greedy decode of ONE sequence, "
+                                   f"tensor parallel over {world} GPU(s), DP plan {args.target}-bit",
+                       "parallelism": f"tp{world}", "realized_effective_bits": eff,
+                       "path": "row-sharded dpq_select_gemv + NCCL all-gather per op group, host-driven"},
+            "gpu_launches": None,
+            "e2e": {"value": 1000.0 / ms_per_step, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 8 * cfg.vocab}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.tp:
+        run_tp(args)
     else:
         run_ours(args)
 

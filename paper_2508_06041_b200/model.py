@@ -113,6 +113,17 @@ class ModelConfig:
         return hashlib.sha256(json.dumps(self.to_dict(), sort_keys=True).encode()).hexdigest()
 
 
+def rope_tables(n_pos: int, head_dim: int):
+    """Half-split RoPE tables (reference model.py:206-212): cos, sin of shape
+    (n_pos, head_dim // 2), float64; (None, None) when head_dim < 2."""
+    half = head_dim // 2
+    if half == 0:
+        return None, None
+    inv_freq = ROPE_BASE ** (-np.arange(half, dtype=np.float64) * 2.0 / head_dim)
+    angles = np.arange(n_pos, dtype=np.float64)[:, None] * inv_freq[None, :]
+    return np.cos(angles), np.sin(angles)
+
+
 def layer_ids(config: ModelConfig) -> list:
     """Canonical order: blocks ascending, kinds q,k,v,o,up,gate,down."""
     return [LayerId(b, k) for b in range(config.n_blocks) for k in KINDS]

@@ -25,11 +25,16 @@ from . import runtime as R
 
 
 def random_device_model(cfg: M.ModelConfig, n_bits: int, b_min: int, seed: int = 0,
-                        keep_host_blocks: int = 0):
+                        keep_host_blocks: int = 0, shard=None):
     """init_model-law weights (W ~ N(0, 1/cols)) generated and quantized on the
     GPU. Returns (ModelWeights with embed/lm_head only, DeviceBitPlaneStore,
     host_layers) where host_layers holds QuantizedLayer copies of the first
-    ``keep_host_blocks`` blocks (for the CPU baseline slice)."""
+    ``keep_host_blocks`` blocks (for the CPU baseline slice).
+
+    shard=(world, rank): also return, as a 4th value, a DeviceStore of this
+    rank's row shards (tp.shard_rows, zero-padded) of every layer, quantized
+    from the same weights (per-row quantization: identical codes).
+    """
     import torch
     dev = _lib.torch_device()
     rng = np.random.default_rng(seed)
@@ -38,7 +43,7 @@ def random_device_model(cfg: M.ModelConfig, n_bits: int, b_min: int, seed: int =
     lm_head = (rng.normal(0.0, 1.0, (cfg.vocab, d)) * (0.1 / np.sqrt(d))).astype(np.float32)
     gen = torch.Generator(device=dev)
     gen.manual_seed(seed)
-    specs, shapes, host = [], {}, {}
+    specs, shapes, host, sspecs = [], {}, {}, []
     for lid in M.layer_ids(cfg):
         rows, cols = M.layer_shape(cfg, lid)
         W = torch.randn((rows, cols), generator=gen, device=dev, dtype=torch.float32)
@@ -49,6 +54,17 @@ def random_device_model(cfg: M.ModelConfig, n_bits: int, b_min: int, seed: int =
         _lib.call("dpq_quantize_device", dev.index, C.c_void_p(W.data_ptr()), rows, cols, n_bits,
                   C.c_void_p(codes.data_ptr()), C.c_void_p(lo.data_ptr()), C.c_void_p(hi.data_ptr()),
                   _lib.stream_ptr())
+        if shard is not None:
+            from . import tp as TP
+            world, rank = shard
+            r0, r1, per = TP.shard_rows(rows, world, rank)
+            sc = torch.zeros((per, cols), dtype=torch.int16, device=dev)
+            sc[: r1 - r0] = codes[r0:r1]
+            slo = np.zeros(per, dtype=np.float32)
+            shi = np.zeros(per, dtype=np.float32)
+            slo[: r1 - r0] = lo[r0:r1].cpu().numpy()
+            shi[: r1 - r0] = hi[r0:r1].cpu().numpy()
+            sspecs.append((sc, slo, shi, n_bits, b_min))
         del W
         lo_h, hi_h = lo.cpu().numpy(), hi.cpu().numpy()
         specs.append((codes, lo_h, hi_h, n_bits, b_min))
@@ -60,6 +76,11 @@ def random_device_model(cfg: M.ModelConfig, n_bits: int, b_min: int, seed: int =
     del specs
     torch.cuda.empty_cache()
     store = Q.DeviceBitPlaneStore(cfg.hash(), n_bits, b_min, shapes, ds)
+    if shard is not None:
+        sds = Q.DeviceStore.from_device_codes(sspecs, dev)
+        del sspecs
+        torch.cuda.empty_cache()
+        return M.ModelWeights(cfg, embed, lm_head, {}), store, host, sds
     return M.ModelWeights(cfg, embed, lm_head, {}), store, host
 
 
