@@ -414,7 +414,18 @@ __device__ __forceinline__ void build_work_warp(const Op& O, const ECtl& C, int 
   }
   const unsigned N = (unsigned)wsum * (unsigned)O.n_win;   // host guarantees N * G < 2^32
   if (lane < 2) {
-    const int g = group_at(O, nb, wsum, (int)(N * (unsigned)(cta + lane) / (unsigned)G));
+    int item;
+    if (O.n_win <= G) {
+      // window-aligned: CTAs [ceil(w G / n_win), ceil((w + 1) G / n_win)) share
+      // window w (one LUT per CTA, no rebuild), its items split evenly
+      const int w = (int)((unsigned)cta * (unsigned)O.n_win / (unsigned)G);
+      const int cb = (w * G + O.n_win - 1) / O.n_win, ce = ((w + 1) * G + O.n_win - 1) / O.n_win;
+      const int m = ce - cb, idx = cta - cb + lane;
+      item = w * wsum + (int)((unsigned)idx * (unsigned)wsum / (unsigned)m);
+    } else {
+      item = (int)(N * (unsigned)(cta + lane) / (unsigned)G);
+    }
+    const int g = group_at(O, nb, wsum, item);
     if (lane == 0) W.ga = g;
     else W.gb = g;
   }
