@@ -21,6 +21,9 @@ plan = synth.projection_plan(store, pairs, prefill, k=64, seed=0, target=3.5)
 synth.calibrate_thresholds(w, store, plan, np.random.default_rng(7).integers(0, cfg.vocab, 8), high_rate=high)
 eng = R.DecodeEngine(w, store, plan)
 eng.prefill(np.random.default_rng(11).integers(0, cfg.vocab, 4))
+torch.cuda.synchronize()
+torch.cuda.profiler.start()          # ncu --profile-from-start off: only this launch
 eng.decode_greedy(4)
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("steps", len(eng.trace.steps), "eff bits", eng.trace.steps[-1].effective_bits)
