@@ -362,3 +362,39 @@ def test_engine_matches_multi_kernel_and_is_deterministic(gqa):
     got = np.array([[b[l] for l in ids] for b in runs[0][1]])
     near = np.abs(est_o - T) <= 1e-3 * np.abs(T)
     assert np.all((got == want) | near)
+
+
+@pytest.mark.gpu
+def test_engine_llama_width_two_blocks():
+    """The engine at the bench's layer widths (d 4096, 32 heads / 8 KV, d_ff
+    14336: 8 and 28 column windows, window-aligned CTA split, several runs per
+    CTA, extra planes across windows) against the per-op kernel graph under
+    forced-bits replay, and bit-identical across runs."""
+    import paper_2508_06041_b200.synth as S
+    cfg = M.ModelConfig(n_blocks=2, d_model=4096, n_heads=32, d_ff=14336, vocab=256, seq_cap=64,
+                        n_kv_heads=8)
+    w, store, _ = S.random_device_model(cfg, 4, 3, seed=77)
+    ids = store.ordered_ids()
+    pairs = {l: (3, 4) for l in ids}
+    plan = S.projection_plan(store, pairs, {l: 4 for l in ids}, k=64, seed=3, target=3.5)
+    toks = np.random.default_rng(12).integers(0, 256, 14)
+    S.calibrate_thresholds(w, store, plan, toks[:6], high_rate=0.5)
+    runs = []
+    for _ in range(2):
+        eng = R.DecodeEngine(w, store, plan)
+        assert eng.persistent
+        lg = [eng.step(int(toks[0]), dynamic=False)]
+        for t in toks[1:]:
+            lg.append(eng.step(int(t), dynamic=True))
+        runs.append((np.array(lg), [s.bits for s in eng.trace.steps]))
+        eng.close()
+    assert np.array_equal(runs[0][0], runs[1][0]) and runs[0][1] == runs[1][1]
+    highs = np.mean([[b[l] == 4 for l in ids] for b in runs[0][1]])
+    assert 0.05 < highs < 0.95                    # both precisions exercised
+    old = R.DecodeEngine(w, store, plan, use_persistent=False)
+    lg = [old.step(int(toks[0]), dynamic=False)]
+    for t, bits in zip(toks[1:], runs[0][1]):
+        lg.append(old.step(int(t), dynamic=True, forced_bits=bits))
+    lg = np.array(lg)
+    assert np.max(np.abs(lg - runs[0][0])) <= 1e-4 * np.max(np.abs(lg))
+    assert np.array_equal(np.argmax(lg, axis=1), np.argmax(runs[0][0], axis=1))
