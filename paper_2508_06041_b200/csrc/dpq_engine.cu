@@ -1013,7 +1013,7 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
         const int i = kt - base_k;
         const int nb = W.nb[q.li], fin = W.fin[q.li];
         const int p0 = kind ? nb : 0, p1 = kind ? fin : nb;
-        const int jr = j_op + (kind ? sm.fo_eo[r] : sm.fo_bo[r]);
+        const int jr = sm.cons_j + (kind ? sm.fo_eo[r] : sm.fo_bo[r]);   // FIFO base from shared memory (no spill reload)
         float S = kind ? sm.sbuf[q.k0 + i][lane] : 0.f;
         for (int p = p0; p < p1; ++p) {
           const int j = jr + (p - p0);
