@@ -1306,13 +1306,11 @@ __device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, 
       kt = rope4(P.qkv + P.d + g * hd, i0, hd, c4, s4);      // RoPE'd k of this step
       vt = __ldcg(reinterpret_cast<const float4*>(P.qkv + P.d + P.dkv + g * hd + i0));
     }
-    // register pipeline rows (j = kAttnStaged ...), in flight with q / k_t / v_t
+    // register pipeline rows (j = kAttnStaged ..., 2 deep), in flight with q / k_t / v_t
     const int sr = s0 + warp + NW * kAttnStaged;
-    float4 k0 = z4, v0 = z4, k1 = z4, v1 = z4, k2 = z4, v2 = z4, k3 = z4, v3 = z4;
+    float4 k0 = z4, v0 = z4, k1 = z4, v1 = z4;
     ATTN_ROW(sr, lim, g, k0, v0);
     ATTN_ROW(sr + NW, lim, g, k1, v1);
-    ATTN_ROW(sr + 2 * NW, lim, g, k2, v2);
-    ATTN_ROW(sr + 3 * NW, lim, g, k3, v3);
     if (own_t && h % qh == 0) {          // runtime.py:355-356 (KV append)
       *reinterpret_cast<float4*>(kc + (size_t)t * P.dkv + g * hd + i0) = kt;
       *reinterpret_cast<float4*>(vc + (size_t)t * P.dkv + g * hd + i0) = vt;
@@ -1341,12 +1339,10 @@ __device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, 
     }
 #define ATTN_STEP(s_, K_, V_)                                                      \
     if ((s_) < s1) ATTN_UPDATE(s_, K_, V_)                                         \
-    ATTN_ROW((s_) + 4 * NW, lim, g, K_, V_);   /* refill this register slot */
-    for (int s = sr; s < s1; s += 4 * NW) {
+    ATTN_ROW((s_) + 2 * NW, lim, g, K_, V_);   /* refill this register slot */
+    for (int s = sr; s < s1; s += 2 * NW) {
       ATTN_STEP(s, k0, v0)
       ATTN_STEP(s + NW, k1, v1)
-      ATTN_STEP(s + 2 * NW, k2, v2)
-      ATTN_STEP(s + 3 * NW, k3, v3)
     }
     CSTAMP(stp, 2);
     CSYNC();                                 // previous unit's readers of part / outv done
