@@ -610,16 +610,27 @@ __device__ __forceinline__ void bar_arrive(const Prog& P, unsigned long long epo
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" :: "l"(P.bar) : "memory");
   }
 }
+__shared__ unsigned long long s_bar_seen;     // last barrier epoch seen released (zeroed at kernel start)
 __device__ __forceinline__ void bar_wait(const Prog& P, unsigned long long epoch) {
-  if (threadIdx.x == 0) {
+  // lane 0 of warps 0..kPollers-1 poll, staggered by a fraction of the L2
+  // round trip; the first to see the release publishes it in shared memory
+  constexpr int kPollers = 4;
+  volatile unsigned long long& s_seen = s_bar_seen;
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0 && warp < kPollers) {
     const unsigned long long target = epoch * (unsigned long long)gridDim.x;
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(P.bar) : "memory");
-    auto poll = [&]() {
-      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(P.bar) : "memory");
-      return v >= target;
-    };
-    if (v < target) SPIN_UNTIL_NS(poll(), "grid barrier", 0, (long long)epoch, 3000000000ull);
+    if (v < target && s_seen < epoch) {
+      if (warp) __nanosleep(120u * (unsigned)warp);
+      auto poll = [&]() {
+        if (s_seen >= epoch) return true;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(P.bar) : "memory");
+        return v >= target;
+      };
+      SPIN_UNTIL_NS(poll(), "grid barrier", 0, (long long)epoch, 3000000000ull);
+    }
+    if (v >= target && s_seen < epoch) s_seen = epoch;
     __threadfence();
   }
   CSYNC();
@@ -1540,6 +1551,7 @@ extern "C" __global__ void __launch_bounds__(NTB, 1) engine_kernel(const Prog Pk
     sm.work[1].valid = 0;
     sm.dec_op = 0;
     sm.step_ready = 0;
+    s_bar_seen = 0;
     // ring slots: below the LUT (after Smem) and above its zero row
     const uint32_t base = smem_u32(smem_raw);
     uint32_t lo = (base + (uint32_t)sizeof(Smem) + 1023u) & ~1023u;
