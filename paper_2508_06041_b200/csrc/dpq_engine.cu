@@ -361,6 +361,7 @@ struct Smem {
   unsigned slot_off[kMaxSlots];      // slot byte offset from the dynamic smem base
   int n_slots;
   volatile int dec_op;               // op counter whose decision is published
+  int runs_op;                       // op counter whose base runs / FIFO offsets are in runs, fo_bo, last
   volatile int step_ready;           // step whose control block consumers have loaded
   volatile int cons_op, cons_j;      // consumer progress (watchdog diagnostics)
   unsigned long long* stamp;         // current stage's timestamps (profiling) or nullptr
@@ -814,7 +815,8 @@ __device__ __forceinline__ float reduce_unit(const Prog& P, const Op& O, const W
 // warp in parallel (independent fixed-point sums). Warp NW - 1 first prepares
 // the next op's descriptor and work.
 __device__ __forceinline__ void reduce_duty(const Prog& P, const ECtl& C, const Op& O, const Work& W, Smem& sm,
-                                          int cta, int G, unsigned epoch, Op* On, Work* Wn, const Op* On_global) {
+                                          int cta, int G, unsigned epoch, Op* On, Work* Wn, const Op* On_global,
+                                          int op_no) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n_units = O.pair ? O.L[0].n_tiles : O.n_tiles;
   const int mine = n_units > cta ? (n_units - cta + G - 1) / G : 0;     // units of this CTA
@@ -826,7 +828,16 @@ __device__ __forceinline__ void reduce_duty(const Prog& P, const ECtl& C, const 
     __syncwarp();
     build_work_warp(*On, C, cta, G, *Wn);
     __syncwarp();
-    if (lane == 0) Wn->valid = 1;
+    if (lane == 0) {
+      Wn->valid = 1;
+      // the next op's base runs and FIFO offsets (this op's are dead after
+      // its items): off the next stage's pre-barrier path
+      build_runs(*On, *Wn, sm.runs);
+      int o = 0;
+      for (int r = 0; r < sm.runs.n; ++r) { sm.fo_bo[r] = (short)o; o += Wn->nb[sm.runs.r[r].li]; }
+      sm.last = o;
+      sm.runs_op = op_no + 1;
+    }
   }
   const int f0 = O.out_inst >= 0 ? P.feed_begin[O.out_inst] : 0;
   const int nf = O.out_inst >= 0 ? P.feed_begin[O.out_inst + 1] - f0 : 0;
@@ -871,10 +882,12 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
   }
   if (tid == 0) {
     sm.stamp = stamp;
-    build_runs(O, W, sm.runs);
-    int o = 0;                          // FIFO offsets of the base planes
-    for (int r = 0; r < sm.runs.n; ++r) { sm.fo_bo[r] = (short)o; o += W.nb[sm.runs.r[r].li]; }
-    sm.last = o;
+    if (sm.runs_op != op_no) {          // not prepared during the previous op's reduce phase
+      build_runs(O, W, sm.runs);
+      int o = 0;                        // FIFO offsets of the base planes
+      for (int r = 0; r < sm.runs.n; ++r) { sm.fo_bo[r] = (short)o; o += W.nb[sm.runs.r[r].li]; }
+      sm.last = o;
+    }
     sm.cons_op = op_no;
     sm.cons_j = j_op;
   }
@@ -1078,12 +1091,14 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
       ws[0] = w_task0; ws[1] = w_first_t; ws[2] = w_last_t; ws[3] = clock64(); ws[4] = (unsigned long long)w_planes | (min(w_seq, 0xffffffull) << 16) | (min(w_mb, 0xffffffull) << 40);
     }
 #endif
-    if (!kind) CSYNC();                   // parked base sums visible before the extra pass
+    // kind 0: parked base sums visible before the extra pass; kind 1: every warp
+    // done with the runs before the reduce phase rebuilds them for the next op
+    if (!kind || n_tasks > 0) CSYNC();
   }
   if (tid == 0) PROGRESS(1, 2);
   if (stamp && tid == 0) stamp[5] = gclock();
   if (tid == 0) CSTAMP(stamp, 10);
-  reduce_duty(P, C, O, W, sm, cta, G, epoch, On, Wn, On_global);
+  reduce_duty(P, C, O, W, sm, cta, G, epoch, On, Wn, On_global, op_no);
   if (tid == 0) PROGRESS(1, 3);
   if (stamp && tid == 0) stamp[6] = gclock();
   if (tid == 0) CSTAMP(stamp, 15);
@@ -1550,6 +1565,7 @@ extern "C" __global__ void __launch_bounds__(NTB, 1) engine_kernel(const Prog Pk
     sm.work[0].valid = 0;
     sm.work[1].valid = 0;
     sm.dec_op = 0;
+    sm.runs_op = -1;
     sm.step_ready = 0;
     s_bar_seen = 0;
     // ring slots: below the LUT (after Smem) and above its zero row
