@@ -969,7 +969,7 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
   }
   CSYNC();                             // decisions and LUT visible
   const RunList& R = sm.runs;
-  if (tid == 0) {
+  if (tid == NT - 32) {                 // last warp: fewest items (tasks go round-robin from warp 0)
     __threadfence_block();
     sm.dec_op = op_no + 1;            // the producer may now stream the extra planes
     // FIFO offsets of the extra planes (base offsets were set before the barrier)
