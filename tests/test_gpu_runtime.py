@@ -398,3 +398,32 @@ def test_engine_llama_width_two_blocks():
     lg = np.array(lg)
     assert np.max(np.abs(lg - runs[0][0])) <= 1e-4 * np.max(np.abs(lg))
     assert np.array_equal(np.argmax(lg, axis=1), np.argmax(runs[0][0], axis=1))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d_model,n_heads", [(128, 4), (64, 4)])
+def test_engine_long_context_chunked_attention(d_model, n_heads):
+    """Past one attention unit (15 warps x 16 positions = 240) the engine splits
+    a head's positions into chunks merged by the last unit; head_dim 32 emits
+    per head, head_dim 16 goes through the EMIT stage. Compared with the per-op
+    kernel graph under forced-bits replay."""
+    cfg = M.ModelConfig(n_blocks=1, d_model=d_model, n_heads=n_heads, d_ff=2 * d_model, vocab=256,
+                        seq_cap=320)
+    w = M.init_model(5, cfg)
+    store = Q.quantize_model(w, 5, 3)
+    plan = synthetic_projection_plan(store, {l: (3, 4) for l in store.layers}, k=16, seed=8)
+    toks = np.random.default_rng(13).integers(0, 256, 300)
+    calibrate_T(w, store, plan, toks[:10])
+    eng = R.DecodeEngine(w, store, plan)
+    assert eng.persistent
+    lg = [eng.step(int(toks[0]), dynamic=False)]
+    for t in toks[1:]:
+        lg.append(eng.step(int(t), dynamic=True))
+    bits = [s.bits for s in eng.trace.steps]
+    old = R.DecodeEngine(w, store, plan, use_persistent=False)
+    lo = [old.step(int(toks[0]), dynamic=False)]
+    for t, b in zip(toks[1:], bits):
+        lo.append(old.step(int(t), dynamic=True, forced_bits=b))
+    lg, lo = np.array(lg), np.array(lo)
+    assert np.max(np.abs(lg - lo)) <= 1e-4 * np.max(np.abs(lo))
+    assert np.max(np.abs(lg[250:] - lo[250:])) <= 1e-4 * np.max(np.abs(lo))   # the chunked positions
