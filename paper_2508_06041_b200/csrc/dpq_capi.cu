@@ -249,7 +249,6 @@ struct dpq_session {
   int eng_smem = 0;
   int eng_grid = 0;
   unsigned long long* eng_dbg = nullptr;
-  unsigned long long* eng_emit = nullptr;
 };
 
 // ---------------------------------------------------------------------------

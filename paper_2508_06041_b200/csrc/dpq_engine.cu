@@ -492,7 +492,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 // Vector emission: statistics + estimator feeds of one 32-row tile (a warp;
 // lane = row). v = value (0 for padding rows).
 // ---------------------------------------------------------------------------
-__device__ unsigned long long* g_emit_stamp = nullptr;   // profiling hook (unused by the engine)
 
 // Statistics of one 32-row tile of vector instance inst: sum v, sum v^2.
 __device__ __forceinline__ void emit_stats(const Prog& P, const ECtl& C, int inst, float v) {

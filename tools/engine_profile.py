@@ -66,7 +66,6 @@ def main():
     _lib.call("dpq_session_engine_stages", eng._h, C.byref(n), C.c_void_p(kinds.ctypes.data),
               C.c_void_p(idx.ctypes.data))
     per = C.c_int()
-    _lib.call("dpq_session_debug_times", eng._h, None, -8, C.byref(per))
     _lib.call("dpq_session_debug_times", eng._h, None, 0, C.byref(per))
     G = torch.cuda.get_device_properties(0).multi_processor_count
     rec = per.value // G
