@@ -264,12 +264,14 @@ def op_stage_times(eng, store, plan, ids, g_bytes):
     idx = np.zeros(n.value, dtype=np.int32)
     _lib.call("dpq_session_engine_stages", eng._h, C.byref(n), C.c_void_p(kinds.ctypes.data),
               C.c_void_p(idx.ctypes.data))
+    import torch
     per = C.c_int()
     _lib.call("dpq_session_debug_times", eng._h, None, 0, C.byref(per))
-    G = per.value // 8
-    buf = np.zeros(n.value * G * 8, dtype=np.uint64)
+    G = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    rec = per.value // G                      # record per (stage, CTA): [0, 8) are the phase stamps
+    buf = np.zeros(n.value * G * rec, dtype=np.uint64)
     _lib.call("dpq_session_debug_times", eng._h, C.c_void_p(buf.ctypes.data), buf.size, C.byref(per))
-    st = buf.reshape(n.value, G, 8).astype(np.float64)
+    st = buf.reshape(n.value, G, rec)[..., :8].astype(np.float64)
     last_end = st[..., 7].max(axis=1)
     crit = np.diff(np.concatenate([[st[0, :, 0].min()], last_end])) / 1e3
     bits = [eng.trace.steps[-1].bits[l] for l in ids]
