@@ -41,7 +41,8 @@ constexpr int kSlotTiles = 8;      // tiles per ring slot (one plane of up to 8 
 constexpr int kSlotBytes = kSlotTiles * 2048;
 constexpr int kMaxSlots = 8;       // ring slots (power of two: index arithmetic by shifts)
 constexpr int kMaxRuns = 96;       // (layer, window, <= 8 tiles) runs per op per CTA
-constexpr int kMaxTiles = 128;     // tiles (groups) per op per CTA (parked base sums)
+constexpr int kMaxTiles = 128;
+
 constexpr int kDbgRec = 128;   // debug record per (stage, CTA): [0,8) phase stamps, [8,88) 5 per consumer warp, [88,96) producer, [96,128) clock64 sub-stamps
 constexpr double kFxSum = 4294967296.0;       // 2^32: sum v
 constexpr double kFxSq = 16777216.0;          // 2^24: sum v^2
@@ -353,8 +354,6 @@ struct Smem {
   RunList runs;            // consumer run list of the current op
   Op pop;                  // producer copy of the op it streams
   Work pw;                 // producer work
-  Op pop2;                 // producer copy of the following op (L2 prefetch)
-  Work pw2;
   RunList pruns;           // producer run list
   unsigned long long full[kMaxSlots], empty[kMaxSlots];   // ring mbarriers
   volatile int seq[kMaxSlots];       // FIFO index armed in each slot (phase disambiguation)
@@ -652,34 +651,6 @@ __device__ __forceinline__ void load4(uint4* dst, const uint4* a) {
   dst[1] = ld_nc(a + 32);
   dst[2] = ld_nc(a + 64);
   dst[3] = ld_nc(a + 96);
-}
-
-// L2 prefetch of this CTA's planes [p_lo, p_hi(layer)) of op O (one warp;
-// lane = (window of the CTA range, layer, plane) stripe of contiguous tiles).
-// hi_fin: 0 -> base planes [0, nb), 1 -> extra planes [nb, fin).
-__device__ __forceinline__ void prefetch_work_l2(const Op& O, const Work& W, int extra) {
-  if (W.ga >= W.gb) return;
-  const int lane = threadIdx.x & 31;
-  const int w_first = W.ga / O.n_tiles, w_last = (W.gb - 1) / O.n_tiles;
-  const int nwin = min(2, w_last - w_first + 1);
-  for (int idx = lane; idx < nwin * O.n_layers * 8; idx += 32) {
-    const int wi = idx / (O.n_layers * 8), rem = idx - wi * O.n_layers * 8, li = rem >> 3, p = rem & 7;
-    const int p0 = extra ? W.nb[li] : 0, p1 = extra ? W.fin[li] : W.nb[li];
-    if (p < p0 || p >= p1) continue;
-    const int w = w_first + wi;
-    const int t_lo = max(W.ga - w * O.n_tiles, 0), t_hi = min(W.gb - w * O.n_tiles, O.n_tiles);
-    const Layer& L = O.L[li];
-    const int t0 = max(t_lo, L.tile_off), t1 = min(t_hi, L.tile_off + L.n_tiles);
-    if (t0 >= t1) continue;
-    const char* a = reinterpret_cast<const char*>(L.planes + p * L.pstride + ((long long)w * L.n_tiles + (t0 - L.tile_off)) * 128);
-    long long bytes = (long long)(t1 - t0) * kTileBytes;
-    while (bytes > 0) {
-      const unsigned c = (unsigned)min(bytes, 65536LL);
-      l2_prefetch(a, c);
-      a += c;
-      bytes -= c;
-    }
-  }
 }
 
 // L2 prefetch of slice cta/G of the G^T blocks the op's output feeds.
@@ -1155,20 +1126,8 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
       __syncwarp();
       build_work_warp(sm.pop, C, cta, G, sm.pw);
       __syncwarp();
-      // the next op's base planes -> L2 while this op streams through the ring
-      {
-        int nsi = si + 1;
-        while (nsi < P.n_stages && P.stages[nsi].x != ST_OP) ++nsi;
-        if (nsi < P.n_stages) {
-          const int4* src2 = reinterpret_cast<const int4*>(P.ops + P.stages[nsi].y);
-          int4* dst2 = reinterpret_cast<int4*>(&sm.pop2);
-          for (int q = lane; q < nw4; q += 32) dst2[q] = __ldg(src2 + q);
-          __syncwarp();
-          build_work_warp(sm.pop2, C, cta, G, sm.pw2);
-          __syncwarp();
-          prefetch_work_l2(sm.pop2, sm.pw2, 0);
-        }
-      }
+      // (no L2 bulk prefetch of the next op's planes: measured slower -- it
+      // competes with the current stage's loads; the ring alone runs ahead)
       if (lane == 0) {
         unsigned long long* pd = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec + 8 + 5 * NW : nullptr;
         const int j0 = j;
