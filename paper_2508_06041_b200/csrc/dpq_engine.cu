@@ -653,25 +653,6 @@ __device__ __forceinline__ void load4(uint4* dst, const uint4* a) {
   dst[3] = ld_nc(a + 96);
 }
 
-// L2 prefetch of slice cta/G of the G^T blocks the op's output feeds.
-__device__ __forceinline__ void prefetch_feeds_l2(const Prog& P, const ECtl& C, int inst, int n, int cta, int G) {
-  if (inst < 0 || C.mode != MODE_DYNAMIC && !C.prime) return;
-  const int nt = (n + 31) / 32;
-  for (int fi = P.feed_begin[inst] + (int)threadIdx.x; fi < P.feed_begin[inst + 1]; fi += NT) {
-    const Feed F = P.feeds[fi];
-    if (!F.Gt) continue;
-    const long long bytes = (long long)nt * (F.kpad / 64) * (F.f16 ? 4096 : 8192);
-    const long long lo = bytes * cta / G / 16 * 16, hi = bytes * (cta + 1) / G / 16 * 16;
-    const char* a = reinterpret_cast<const char*>(F.Gt) + lo;
-    long long left = hi - lo;
-    while (left > 0) {
-      const unsigned c = (unsigned)min(left, 65536LL);
-      l2_prefetch(a, c);
-      a += c;
-      left -= c;
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Tile reduction + epilogue (one warp, lane = row of the tile)
@@ -872,9 +853,9 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
   const LutSrc xsrc = lut_load(O.in, O.cols, max(w_first, 0));
   // decision warps: accumulator loads in flight (k <= 128: 4 per lane)
   // roles: warps 0..7 build the LUT (lut_store: threads < 256), warps 8.. take
-  // the decisions (one per layer), the input statistics and the feed prefetch
-  constexpr int kDecW = 8, kStatW = kDecW + kMaxOpLayers, kPfW = kStatW + 1;
-  static_assert(kPfW < NW, "prologue roles need more consumer warps");
+  // the decisions (one per layer) and the input statistics
+  constexpr int kDecW = 8, kStatW = kDecW + kMaxOpLayers;
+  static_assert(kStatW < NW, "prologue roles need more consumer warps");
   const int li_d = warp - kDecW;
   const bool dec_warp = li_d >= 0 && li_d < O.n_layers;
   const Layer& Ld = O.L[dec_warp ? li_d : 0];
@@ -893,8 +874,6 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
     const long long* vs = P.vstat + ((size_t)cur * P.n_inst + O.in_inst) * 2;
     vs1 = __ldcg(vs);
     vs2 = __ldcg(vs + 1);
-  } else if (warp == kPfW) {
-    prefetch_feeds_l2(P, C, O.out_inst, O.n_tiles * 32, cta, G);
   }
   if (tid == 0) CSTAMP(stamp, 1);
   float* lut = reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLut - smem_u32(&sm)));
@@ -1225,8 +1204,6 @@ __device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, 
   float* kc = P.kc[b];
   float* vc = P.vc[b];
   const int inst = 4 * b + 1;
-  // G^T blocks the attention output feeds (o-proj estimators) -> L2
-  if (warp == NW - 1) prefetch_feeds_l2(P, C, inst, P.d, cta, G);
   // shared memory (LUT region): K / V staging [NW][kAttnStaged][2][hd], the
   // per-warp partials [NW][hd + 4] and the merged head output [hd]
   float* kvs = sh;
