@@ -482,9 +482,18 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
   };
   SPIN_UNTIL_NS(test(), "ring slot", (long long)a, (long long)parity, 1000000000ull);
 }
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+// Bitplanes are streamed once per step (GBs >> L2): marked evict-first so they
+// do not push the small, re-read state (vectors, window slots, accumulators,
+// G^T, KV rows) out of L2.
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                            unsigned long long policy) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -1065,6 +1074,7 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
   const int lane = threadIdx.x & 31;
   int j = 0, op_no = 0;
   const unsigned char* dyn0 = reinterpret_cast<const unsigned char*>(&sm);
+  const unsigned long long l2pol = l2_evict_first_policy();
   auto issue = [&](const Op& O, const Run& r, int p) {
     const int slot = j & (kMaxSlots - 1);
     if (j >= kMaxSlots) {
@@ -1087,7 +1097,8 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
     const Layer& L = O.L[r.li];
     const uint4* src = L.planes + p * L.pstride + ((long long)r.w * L.n_tiles + (r.t0 - L.tile_off)) * (kTileBytes / 16);
     mbar_expect_tx(&sm.full[slot], (unsigned)r.nt * kTileBytes);
-    tma_load_1d(const_cast<unsigned char*>(dyn0) + sm.slot_off[slot], src, (unsigned)r.nt * kTileBytes, &sm.full[slot]);
+    tma_load_1d(const_cast<unsigned char*>(dyn0) + sm.slot_off[slot], src, (unsigned)r.nt * kTileBytes, &sm.full[slot],
+                l2pol);
     ++j;
   };
   for (int step = 0; step < n_steps; ++step) {
