@@ -490,6 +490,12 @@ __device__ __forceinline__ unsigned long long l2_evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+__device__ __forceinline__ uint4 ld_stream(const uint4* p, unsigned long long policy) {
+  uint4 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(policy));
+  return r;
+}
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
                                             unsigned long long policy) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
@@ -515,16 +521,6 @@ __device__ __forceinline__ void emit_stats(const Prog& P, const ECtl& C, int ins
 
 // Feed fi (an estimator reading the vector) with tile `tile`: G_tile^T v
 // partials and sum v^2 into its fixed-point accumulators (a warp, lane = row).
-// G^T block of feed F for tile `tile` (f16, k <= 64: the common case) into
-// registers ahead of the value it is applied to.
-__device__ __forceinline__ bool feed_preload(const Prog& P, int fi, int tile, uint4 (&c)[8]) {
-  const Feed* F = P.feeds + fi;
-  if (!F->Gt || !F->f16 || F->kpad != 64) return false;
-  const uint4* blk = F->Gt + (size_t)tile * 256 + (threadIdx.x & 31);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) c[i] = __ldg(blk + 32 * i);
-  return true;
-}
 
 __device__ __forceinline__ void emit_feed(const Prog& P, const ECtl& C, int fi, int tile, float v,
                                           const uint4 (*pre)[8] = nullptr) {
@@ -552,13 +548,14 @@ __device__ __forceinline__ void emit_feed(const Prog& P, const ECtl& C, int fi, 
     // f32 chunk = 2 rows x float2; lane owns k pair (2 lane, 2 lane + 1) of sub.
     const int nsub = F.kpad / 64;
     const double sc = ldexp(1.0, F.fb);
+    const unsigned long long pol = l2_evict_first_policy();   // G^T (~150 MB/step at 8B) streams like the planes
     for (int sub = 0; sub < nsub; ++sub) {
       float g0 = 0.f, g1 = 0.f;
       if (F.f16) {
         const uint4* blk = F.Gt + ((size_t)tile * nsub + sub) * 256 + lane;
         uint4 c[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) c[i] = pre ? (*pre)[i] : __ldg(blk + 32 * i);
+        for (int i = 0; i < 8; ++i) c[i] = pre ? (*pre)[i] : ld_stream(blk + 32 * i, pol);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const __half2* hh = reinterpret_cast<const __half2*>(&c[i]);
@@ -576,7 +573,7 @@ __device__ __forceinline__ void emit_feed(const Prog& P, const ECtl& C, int fi, 
         for (int hb = 0; hb < 2; ++hb) {
           uint4 c[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) c[i] = __ldg(blk + 32 * (8 * hb + i));
+          for (int i = 0; i < 8; ++i) c[i] = ld_stream(blk + 32 * (8 * hb + i), pol);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float* ff = reinterpret_cast<const float*>(&c[i]);
