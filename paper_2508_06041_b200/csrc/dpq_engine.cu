@@ -490,6 +490,17 @@ __device__ __forceinline__ unsigned long long l2_evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+__device__ __forceinline__ unsigned long long l2_evict_last_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float4 ld_keep(const float* p, unsigned long long policy) {
+  float4 r;
+  asm volatile("ld.global.cg.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(policy));
+  return r;
+}
 __device__ __forceinline__ uint4 ld_stream(const uint4* p, unsigned long long policy) {
   uint4 r;
   asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
@@ -1221,6 +1232,7 @@ __device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, 
   const bool act = lane < nv;
   const int i0 = 4 * lane;
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  const unsigned long long kvpol = l2_evict_last_policy();   // the KV cache is re-read every step: keep it in L2
   // Rows of unit positions s0 + warp + NW j: j < kAttnStaged are copied
   // asynchronously into shared memory (for the CTA's first unit before the
   // barrier: cached positions do not depend on this step; a lane copies and
@@ -1235,8 +1247,8 @@ __device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, 
       if (act && s_ < lim_) {                                                            \
         const size_t off_ = (size_t)s_ * P.dkv + g_ * hd + i0;                           \
         float* d_ = kvs + ((warp * kAttnStaged + j) * 2) * hd + i0;                      \
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_u32(d_)), "l"(kc + off_) : "memory"); \
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_u32(d_ + hd)), "l"(vc + off_) : "memory"); \
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(smem_u32(d_)), "l"(kc + off_), "l"(kvpol) : "memory"); \
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(smem_u32(d_ + hd)), "l"(vc + off_), "l"(kvpol) : "memory"); \
       }                                                                                  \
     }                                                                                    \
   } while (0)
@@ -1244,8 +1256,8 @@ __device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, 
   do {                                                                             \
     if (act && (s_) < (lim_)) {                                                    \
       const size_t off_ = (size_t)(s_) * P.dkv + (g_) * hd + i0;                   \
-      K_ = __ldcg(reinterpret_cast<const float4*>(kc + off_));                     \
-      V_ = __ldcg(reinterpret_cast<const float4*>(vc + off_));                     \
+      K_ = ld_keep(kc + off_, kvpol);                                             \
+      V_ = ld_keep(vc + off_, kvpol);                                             \
     }                                                                              \
   } while (0)
   if (cta < units) ATTN_STAGE_ROWS(cta);
