@@ -374,6 +374,7 @@ struct Smem {
   int head_i[NW];
   float sbuf[kMaxTiles][32];         // base-pass S of tiles whose layer has extra planes
   short fo_bo[kMaxRuns], fo_eo[kMaxRuns], fo_xt[kMaxRuns];
+  unsigned char task_rb[kMaxTiles], task_rx[kMaxTiles];   // run of each base / extra task (kMaxRuns <= 255)
   int vtile[kMaxTiles];              // reduce: emit tile of the CTA's i-th unit (values in sbuf)
 };
 
@@ -802,7 +803,12 @@ __device__ __forceinline__ void reduce_duty(const Prog& P, const ECtl& C, const 
       // its items): off the next stage's pre-barrier path
       build_runs(*On, *Wn, sm.runs);
       int o = 0;
-      for (int r = 0; r < sm.runs.n; ++r) { sm.fo_bo[r] = (short)o; o += Wn->nb[sm.runs.r[r].li]; }
+      for (int r = 0; r < sm.runs.n; ++r) {
+        const Run& q = sm.runs.r[r];
+        sm.fo_bo[r] = (short)o;
+        o += Wn->nb[q.li];
+        for (int t = 0; t < q.nt; ++t) sm.task_rb[q.k0 + t] = (unsigned char)r;
+      }
       sm.last = o;
       sm.runs_op = op_no + 1;
     }
@@ -852,8 +858,13 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
     sm.stamp = stamp;
     if (sm.runs_op != op_no) {          // not prepared during the previous op's reduce phase
       build_runs(O, W, sm.runs);
-      int o = 0;                        // FIFO offsets of the base planes
-      for (int r = 0; r < sm.runs.n; ++r) { sm.fo_bo[r] = (short)o; o += W.nb[sm.runs.r[r].li]; }
+      int o = 0;                        // FIFO offsets of the base planes, task -> run table
+      for (int r = 0; r < sm.runs.n; ++r) {
+        const Run& q = sm.runs.r[r];
+        sm.fo_bo[r] = (short)o;
+        o += W.nb[q.li];
+        for (int t = 0; t < q.nt; ++t) sm.task_rb[q.k0 + t] = (unsigned char)r;
+      }
       sm.last = o;
     }
     sm.cons_op = op_no;
@@ -946,7 +957,11 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
       const int ex = W.fin[R.r[r].li] - W.nb[R.r[r].li];
       sm.fo_eo[r] = (short)o;
       sm.fo_xt[r] = (short)xt;
-      if (ex > 0) { o += ex; xt += R.r[r].nt; }
+      if (ex > 0) {
+        for (int t = 0; t < R.r[r].nt; ++t) sm.task_rx[xt + t] = (unsigned char)r;
+        o += ex;
+        xt += R.r[r].nt;
+      }
     }
     sm.n_ext_items = o - o_base;
     sm.t_ext = xt;
@@ -990,17 +1005,10 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
       const uint32_t lanereg = kLut | ((uint32_t)lane * 4u);
       for (int kt = k + warp; kt < k_end; kt += NW) {
         WPROF(if (!w_task0) w_task0 = clock64());
-        // task kt -> run and tile
-        int r = rr, base_k = k;
-        while (true) {
-          const Run& q = R.r[r];
-          const bool has = !kind || W.fin[q.li] > W.nb[q.li];
-          if (has && kt < base_k + q.nt) break;
-          if (has) base_k += q.nt;
-          r += kind ? -1 : 1;
-        }
+        // task kt -> run and tile (tables built with the FIFO offsets)
+        const int r = kind ? sm.task_rx[kt] : sm.task_rb[kt];
         const Run& q = R.r[r];
-        const int i = kt - base_k;
+        const int i = kt - (kind ? sm.fo_xt[r] : q.k0);
         const int nb = W.nb[q.li], fin = W.fin[q.li];
         const int p0 = kind ? nb : 0, p1 = kind ? fin : nb;
         const int jr = sm.cons_j + (kind ? sm.fo_eo[r] : sm.fo_bo[r]);   // FIFO base from shared memory (no spill reload)
