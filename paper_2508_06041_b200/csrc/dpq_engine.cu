@@ -1020,10 +1020,7 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
 #ifdef DPQ_PROFILE_WARPS
           const unsigned long long tw0 = stamp ? clock64() : 0;
 #endif
-          if (lane == 0) {
-            if (sm.seq[slot] > j) hang("ring overtaken", j, sm.seq[slot]);
-            SPIN_UNTIL_NS(sm.seq[slot] == j, "ring sequence", j, sm.seq[slot], 1000000000ull);
-          }
+          if (lane == 0) SPIN_UNTIL_NS(sm.seq[slot] == j, "ring sequence", j, sm.seq[slot], 1000000000ull);
           __syncwarp();
           WSTATE(j * 16 + 2);
 #ifdef DPQ_PROFILE_WARPS
