@@ -672,6 +672,26 @@ __device__ __forceinline__ void load4(uint4* dst, const uint4* a) {
 }
 
 
+// L2 prefetch of the G^T blocks this CTA's reduce units will feed (one 4 KB
+// block per (unit, feed) for f16, k <= 64), issued in the prologue so the
+// feed loads at the end of the stage hit L2.
+__device__ __forceinline__ void prefetch_own_feeds(const Prog& P, const ECtl& C, const Op& O, int cta, int G) {
+  if (O.out_inst < 0 || (C.mode != MODE_DYNAMIC && !C.prime)) return;
+  const int lane = threadIdx.x & 31;
+  const int f0 = P.feed_begin[O.out_inst], nf = P.feed_begin[O.out_inst + 1] - f0;
+  const int n_units = O.pair ? O.L[0].n_tiles : O.n_tiles;
+  const int mine = n_units > cta ? (n_units - cta + G - 1) / G : 0;
+  for (int q = lane; q < mine * nf; q += 32) {
+    const int i = q / nf, u = cta + i * G;
+    const Feed* F = P.feeds + f0 + (q - i * nf);
+    if (!F->Gt) continue;
+    const int li = layer_of(O, u);
+    const int et = O.pair ? u : (O.L[li].out_off >> 5) + (u - O.L[li].tile_off);
+    const int blk = (F->kpad / 64) * (F->f16 ? 4096 : 8192);
+    l2_prefetch(reinterpret_cast<const char*>(F->Gt) + (size_t)et * blk, (unsigned)blk);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Tile reduction + epilogue (one warp, lane = row of the tile)
 // ---------------------------------------------------------------------------
@@ -883,7 +903,7 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
   // roles: warps 0..7 build the LUT (lut_store: threads < 256), warps 8.. take
   // the decisions (one per layer) and the input statistics
   constexpr int kDecW = 8, kStatW = kDecW + kMaxOpLayers;
-  static_assert(kStatW < NW, "prologue roles need more consumer warps");
+  static_assert(kStatW + 1 < NW, "prologue roles need more consumer warps");
   const int li_d = warp - kDecW;
   const bool dec_warp = li_d >= 0 && li_d < O.n_layers;
   const Layer& Ld = O.L[dec_warp ? li_d : 0];
@@ -898,6 +918,7 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
     gsq = __ldcg(acc + Ld.k);
   }
   long long vs1 = 0, vs2 = 0;
+  if (warp == kStatW + 1) prefetch_own_feeds(P, C, O, cta, G);
   if (warp == kStatW && lane == 0) {
     const long long* vs = P.vstat + ((size_t)cur * P.n_inst + O.in_inst) * 2;
     vs1 = __ldcg(vs);
