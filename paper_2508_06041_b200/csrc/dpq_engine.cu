@@ -810,11 +810,7 @@ __device__ __forceinline__ void reduce_duty(const Prog& P, const ECtl& C, const 
   const int n_units = O.pair ? O.L[0].n_tiles : O.n_tiles;
   const int mine = n_units > cta ? (n_units - cta + G - 1) / G : 0;     // units of this CTA
   if (warp == NW - 1 && On && !Wn->valid) {
-    const int nw4 = (int)(sizeof(Op) / 16);
-    const int4* src = reinterpret_cast<const int4*>(On_global);
-    int4* dst = reinterpret_cast<int4*>(On);
-    for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
-    __syncwarp();
+    // (descriptor copied into *On during the prologue)
     build_work_warp(*On, C, cta, G, *Wn);
     __syncwarp();
     if (lane == 0) {
@@ -903,7 +899,7 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
   // roles: warps 0..7 build the LUT (lut_store: threads < 256), warps 8.. take
   // the decisions (one per layer) and the input statistics
   constexpr int kDecW = 8, kStatW = kDecW + kMaxOpLayers;
-  static_assert(kStatW + 1 < NW, "prologue roles need more consumer warps");
+  static_assert(kStatW + 2 < NW - 1, "prologue roles need more consumer warps");
   const int li_d = warp - kDecW;
   const bool dec_warp = li_d >= 0 && li_d < O.n_layers;
   const Layer& Ld = O.L[dec_warp ? li_d : 0];
@@ -919,6 +915,14 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
   }
   long long vs1 = 0, vs2 = 0;
   if (warp == kStatW + 1) prefetch_own_feeds(P, C, O, cta, G);
+  if (warp == kStatW + 2 && On && !Wn->valid) {
+    // the next op's descriptor -> shared memory now (its work and runs are
+    // built during this op's reduce phase, no global round trip there)
+    const int nw4 = (int)(sizeof(Op) / 16);
+    const int4* src = reinterpret_cast<const int4*>(On_global);
+    int4* dst = reinterpret_cast<int4*>(On);
+    for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
+  }
   if (warp == kStatW && lane == 0) {
     const long long* vs = P.vstat + ((size_t)cur * P.n_inst + O.in_inst) * 2;
     vs1 = __ldcg(vs);
