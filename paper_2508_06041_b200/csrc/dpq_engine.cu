@@ -460,6 +460,103 @@ __device__ void build_runs(const Op& O, const Work& W, RunList& R) {
   }
 }
 
+
+// Warp-parallel run list + base FIFO offsets + task -> run table of work W
+// (the serial loops were a dependent chain of shared-memory round trips,
+// ~1-3 us per op). Segments = (window, layer) pieces of [ga, gb), one per
+// lane (<= 32: host sizing keeps CTA ranges within a few windows); runs of
+// <= kSlotTiles tiles per segment; returns the number of base items.
+__device__ int build_runs_warp(const Op& O, const Work& W, RunList& R, short* fo_bo, unsigned char* task_r) {
+  const int lane = threadIdx.x & 31;
+  const int nt = O.n_tiles;
+  if (W.ga >= W.gb) {
+    if (lane == 0) R.n = 0;
+    __syncwarp();
+    return 0;
+  }
+  const int wa = W.ga / nt, wb = (W.gb - 1) / nt;
+  const int S = (wb - wa + 1) * O.n_layers;
+  if (S > 32) __trap();                 // host sizing guarantees this cannot happen
+  int lo = 0, len = 0, nr = 0, items = 0, li = 0, w = wa;
+  if (lane < S) {
+    w = wa + lane / O.n_layers;
+    li = lane - (lane / O.n_layers) * O.n_layers;
+    const Layer& L = O.L[li];
+    lo = max(max(W.ga - w * nt, 0), L.tile_off);
+    const int hi = min(min(W.gb - w * nt, nt), L.tile_off + L.n_tiles);
+    len = max(hi - lo, 0);
+    nr = (len + kSlotTiles - 1) / kSlotTiles;
+    items = nr * W.nb[li];
+  }
+  // exclusive prefix sums over the segments (lane order = window-major, layer order)
+  int rb = nr, ib = items;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, rb, o), b = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) { rb += a; ib += b; }
+  }
+  const int n_runs = __shfl_sync(0xffffffffu, rb, 31), n_items = __shfl_sync(0xffffffffu, ib, 31);
+  rb -= nr;
+  ib -= items;
+  if (n_runs > kMaxRuns) __trap();
+  for (int q = 0; q < nr; ++q) {
+    Run& r = R.r[rb + q];
+    r.li = (short)li;
+    r.w = (short)w;
+    r.t0 = (short)(lo + q * kSlotTiles);
+    r.nt = (short)min(kSlotTiles, len - q * kSlotTiles);
+    r.k0 = (short)(w * nt + lo + q * kSlotTiles - W.ga);
+    fo_bo[rb + q] = (short)(ib + q * W.nb[li]);
+  }
+  // task kt = tile ga + kt -> its run
+  for (int k0 = 0; k0 < W.gb - W.ga; k0 += 32) {   // uniform trip count: the shuffles need every lane
+    const int kt = k0 + lane;
+    const bool ok = kt < W.gb - W.ga;
+    const int g = W.ga + (ok ? kt : 0), ww = g / nt, t = g - ww * nt;
+    int l2 = 0;
+    while (l2 + 1 < O.n_layers && t >= O.L[l2 + 1].tile_off) ++l2;
+    const int sg = (ww - wa) * O.n_layers + l2;
+    const int slo = __shfl_sync(0xffffffffu, lo, sg & 31), srb = __shfl_sync(0xffffffffu, rb, sg & 31);
+    if (ok) task_r[kt] = (unsigned char)(srb + (t - slo) / kSlotTiles);
+  }
+  if (lane == 0) R.n = n_runs;
+  __syncwarp();
+  return n_items;
+}
+
+// Warp-parallel FIFO offsets of the extra planes [nb, fin) once the decision
+// is known: runs in reverse order (the producer's issue order), exclusive
+// prefix sums of items and tasks, and the extra task -> run table.
+__device__ void extra_fifo_warp(const Op& O, const Work& W, const RunList& R, int base_items, short* fo_eo,
+                                short* fo_xt, unsigned char* task_rx, int& n_items, int& n_tasks) {
+  const int lane = threadIdx.x & 31;
+  int carry_i = base_items, carry_t = 0;
+  for (int c0 = 0; c0 < R.n; c0 += 32) {
+    const int idx = c0 + lane;                  // position in the reversed order
+    const int r = R.n - 1 - idx;
+    int ex = 0, nt = 0;
+    if (idx < R.n) {
+      ex = W.fin[R.r[r].li] - W.nb[R.r[r].li];
+      nt = ex > 0 ? R.r[r].nt : 0;
+    }
+    int si = ex, st = nt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, si, o), b = __shfl_up_sync(0xffffffffu, st, o);
+      if (lane >= o) { si += a; st += b; }
+    }
+    if (idx < R.n) {
+      fo_eo[r] = (short)(carry_i + si - ex);
+      fo_xt[r] = (short)(carry_t + st - nt);
+      for (int t = 0; t < nt; ++t) task_rx[carry_t + st - nt + t] = (unsigned char)r;
+    }
+    carry_i += __shfl_sync(0xffffffffu, si, 31);
+    carry_t += __shfl_sync(0xffffffffu, st, 31);
+  }
+  n_items = carry_i - base_items;
+  n_tasks = carry_t;
+}
+
 // ---------------------------------------------------------------------------
 // TMA / mbarrier helpers
 // ---------------------------------------------------------------------------
@@ -813,19 +910,12 @@ __device__ __forceinline__ void reduce_duty(const Prog& P, const ECtl& C, const 
     // (descriptor copied into *On during the prologue)
     build_work_warp(*On, C, cta, G, *Wn);
     __syncwarp();
+    // the next op's base runs, FIFO offsets and task table (this op's are dead
+    // after its items): off the next stage's pre-barrier path
+    const int nbi = build_runs_warp(*On, *Wn, sm.runs, sm.fo_bo, sm.task_rb);
     if (lane == 0) {
       Wn->valid = 1;
-      // the next op's base runs and FIFO offsets (this op's are dead after
-      // its items): off the next stage's pre-barrier path
-      build_runs(*On, *Wn, sm.runs);
-      int o = 0;
-      for (int r = 0; r < sm.runs.n; ++r) {
-        const Run& q = sm.runs.r[r];
-        sm.fo_bo[r] = (short)o;
-        o += Wn->nb[q.li];
-        for (int t = 0; t < q.nt; ++t) sm.task_rb[q.k0 + t] = (unsigned char)r;
-      }
-      sm.last = o;
+      sm.last = nbi;
       sm.runs_op = op_no + 1;
     }
   }
@@ -870,19 +960,12 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
     if (warp == 0) build_work_warp(O, C, cta, G, W);
     CSYNC();
   }
+  if (warp == 0 && sm.runs_op != op_no) {   // not prepared during the previous op's reduce phase
+    const int nbi = build_runs_warp(O, W, sm.runs, sm.fo_bo, sm.task_rb);
+    if (lane == 0) sm.last = nbi;
+  }
   if (tid == 0) {
     sm.stamp = stamp;
-    if (sm.runs_op != op_no) {          // not prepared during the previous op's reduce phase
-      build_runs(O, W, sm.runs);
-      int o = 0;                        // FIFO offsets of the base planes, task -> run table
-      for (int r = 0; r < sm.runs.n; ++r) {
-        const Run& q = sm.runs.r[r];
-        sm.fo_bo[r] = (short)o;
-        o += W.nb[q.li];
-        for (int t = 0; t < q.nt; ++t) sm.task_rb[q.k0 + t] = (unsigned char)r;
-      }
-      sm.last = o;
-    }
     sm.cons_op = op_no;
     sm.cons_j = j_op;
   }
@@ -971,25 +1054,18 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
   }
   CSYNC();                             // decisions and LUT visible
   const RunList& R = sm.runs;
-  if (tid == NT - 32) {                 // last warp: fewest items (tasks go round-robin from warp 0)
-    __threadfence_block();
-    sm.dec_op = op_no + 1;            // the producer may now stream the extra planes
-    // FIFO offsets of the extra planes (base offsets were set before the barrier)
-    int o = sm.last;
-    const int o_base = o;
-    int xt = 0;
-    for (int r = R.n - 1; r >= 0; --r) {
-      const int ex = W.fin[R.r[r].li] - W.nb[R.r[r].li];
-      sm.fo_eo[r] = (short)o;
-      sm.fo_xt[r] = (short)xt;
-      if (ex > 0) {
-        for (int t = 0; t < R.r[r].nt; ++t) sm.task_rx[xt + t] = (unsigned char)r;
-        o += ex;
-        xt += R.r[r].nt;
-      }
+  if (warp == NW - 1) {                 // last warp: fewest items (tasks go round-robin from warp 0)
+    if (lane == 0) {
+      __threadfence_block();
+      sm.dec_op = op_no + 1;          // the producer may now stream the extra planes
     }
-    sm.n_ext_items = o - o_base;
-    sm.t_ext = xt;
+    // FIFO offsets of the extra planes (base offsets were set before the barrier)
+    int ni, nt;
+    extra_fifo_warp(O, W, R, sm.last, sm.fo_eo, sm.fo_xt, sm.task_rx, ni, nt);
+    if (lane == 0) {
+      sm.n_ext_items = ni;
+      sm.t_ext = nt;
+    }
   }
   const int n_base = sm.last;
   if (stamp && tid == 0) stamp[1] = gclock();
