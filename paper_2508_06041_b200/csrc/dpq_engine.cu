@@ -355,6 +355,8 @@ struct Smem {
   Op pop;                  // producer copy of the op it streams
   Work pw;                 // producer work
   RunList pruns;           // producer run list
+  short pfo[kMaxRuns];     // producer scratch (FIFO offsets / task table it does not need)
+  unsigned char ptask[kMaxTiles];
   unsigned long long full[kMaxSlots], empty[kMaxSlots];   // ring mbarriers
   volatile int seq[kMaxSlots];       // FIFO index armed in each slot (phase disambiguation)
   unsigned slot_off[kMaxSlots];      // slot byte offset from the dynamic smem base
@@ -1232,12 +1234,12 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
       __syncwarp();
       // (no L2 bulk prefetch of the next op's planes: measured slower -- it
       // competes with the current stage's loads; the ring alone runs ahead)
+      build_runs_warp(sm.pop, sm.pw, sm.pruns, sm.pfo, sm.ptask);   // same runs as the consumers'
       if (lane == 0) {
         unsigned long long* pd = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec + 8 + 5 * NW : nullptr;
         const int j0 = j;
         if (pd) pd[0] = gclock();
         const Op& O = sm.pop;
-        build_runs(O, sm.pw, sm.pruns);
         const RunList& R = sm.pruns;
         for (int r = 0; r < R.n; ++r)
           for (int p = 0; p < sm.pw.nb[R.r[r].li]; ++p) {
