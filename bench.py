@@ -332,9 +332,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
-    eng._pos += total
-    eng.trace.estimator_ops += eng._ops_per_step * total
-    eng._sync_trace()
+    eng.note_device_steps(total)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

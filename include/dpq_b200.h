@@ -33,7 +33,11 @@ typedef struct dpq_session dpq_session;
 
 /* One quantized layer (reference QuantizedLayer, quant.py:27-40). Codes are
  * row-major rows*cols, uint16 (code_bytes=2) or uint8 (code_bytes=1), each
- * < 2^n_bits; codes_on_device selects host or device memory for `codes`. */
+ * < 2^n_bits, or (code_bytes=0) the .dpqs file's packed code stream as it lies
+ * on disk: code-major, LSB-first, n_bits per code, ceil(rows*cols*n_bits/8)
+ * bytes (reference pack_codes, quant.py:123-126) -- repacked into bitplanes on
+ * the device, never unpacked on the host. codes_on_device selects host or
+ * device memory for `codes`. */
 typedef struct {
   int32_t rows, cols, n_bits, b_min;
   int32_t code_bytes;

@@ -12,7 +12,7 @@ of scope; plans built by the reference load unchanged.
 from .model import (KINDS, LayerId, ModelConfig, ModelWeights, init_model, export_weights,
                     load_weights, layer_ids, layer_shape)
 from .quant import (QuantizedLayer, BitPlaneStore, QuantError, quantize_layer, dequantize,
-                    delta_weights, gemv, quantize_model, save_store, load_store, file_hash,
+                    delta_weights, gemv, quantize_model, save_store, load_store, load_device_store, file_hash,
                     pack_codes, unpack_codes)
 from .estimator import (ErrorEstimator, LinearEstimator, ProjectionEstimator, ExactEstimator,
                         IMMEDIATE, PREVIOUS_RESIDUAL, exact_error, resolve_input_source)

@@ -364,7 +364,7 @@ extern "C" int dpq_store_create(int device, int n_layers, const dpq_layer_desc* 
   for (int i = 0; i < n_layers; ++i) {
     const dpq_layer_desc& d = descs[i];
     if (d.rows < 1 || d.cols < 1 || d.n_bits < 2 || d.n_bits > 8 || d.b_min < 1 || d.b_min > d.n_bits ||
-        (d.code_bytes != 1 && d.code_bytes != 2) || !d.codes || !d.lo || !d.hi)
+        (d.code_bytes < 0 || d.code_bytes > 2) || !d.codes || !d.lo || !d.hi)
       return fail(set_err(DPQ_ERR_ARG, "dpq_store_create: bad layer %d", i));
     DevLayer L{};
     L.rows = d.rows;
@@ -379,7 +379,8 @@ extern "C" int dpq_store_create(int device, int n_layers, const dpq_layer_desc* 
     if (s->arena.alloc(&planes, pbytes)) return fail(DPQ_ERR_CUDA);
     const void* codes_dev = d.codes;
     void* tmp = nullptr;
-    const size_t cbytes = (size_t)d.rows * d.cols * d.code_bytes;
+    const size_t cbytes = d.code_bytes ? (size_t)d.rows * d.cols * d.code_bytes
+                                       : ((size_t)d.rows * d.cols * d.n_bits + 7) / 8;   // .dpqs packed
     if (!d.codes_on_device) {
       if (cudaMalloc(&tmp, cbytes) != cudaSuccess ||
           cudaMemcpy(tmp, d.codes, cbytes, cudaMemcpyHostToDevice) != cudaSuccess)

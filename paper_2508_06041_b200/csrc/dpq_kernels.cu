@@ -1238,11 +1238,22 @@ step_kernel(const StepDesc SD, Control* __restrict__ ctl) {
 // Store construction
 // ---------------------------------------------------------------------------
 
-// codes (row-major, uint16 or uint8) -> device plane layout. One thread per
-// (row, 8-column group); writes one byte per plane.
+// codes (row-major, uint16 or uint8, or code_bytes == 0: the .dpqs packed
+// stream, code-major LSB-first n_bits per code, quant.py:123-126) -> device
+// plane layout. One thread per (row, 8-column group); writes one byte per plane.
+__device__ __forceinline__ unsigned packed_code(const unsigned char* __restrict__ blob, long long o, int n_bits,
+                                                long long nbytes) {
+  const long long bit = o * n_bits;
+  const long long i = bit >> 3;
+  unsigned w = blob[i];
+  if (i + 1 < nbytes) w |= (unsigned)blob[i + 1] << 8;        // n_bits <= 8: at most two bytes
+  return (w >> (bit & 7)) & ((1u << n_bits) - 1u);
+}
+
 extern "C" __global__ void repack_kernel(const void* __restrict__ codes, int code_bytes, int rows,
                                          int cols, int n_bits, int n_win, int n_tiles,
                                          unsigned char* __restrict__ planes) {
+  const long long nbytes = ((long long)rows * cols * n_bits + 7) >> 3;   // packed stream size
   const long long n_groups = (long long)n_tiles * 32 * n_win * kGroups;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n_groups;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -1258,8 +1269,9 @@ extern "C" __global__ void repack_kernel(const void* __restrict__ codes, int cod
       unsigned v = 0;
       if (row < rows && col < cols) {
         const long long o = (long long)row * cols + col;
-        v = code_bytes == 2 ? reinterpret_cast<const unsigned short*>(codes)[o]
-                            : reinterpret_cast<const unsigned char*>(codes)[o];
+        v = code_bytes == 2   ? reinterpret_cast<const unsigned short*>(codes)[o]
+            : code_bytes == 1 ? reinterpret_cast<const unsigned char*>(codes)[o]
+                              : packed_code(reinterpret_cast<const unsigned char*>(codes), o, n_bits, nbytes);
       }
       c8[t] = v;
     }

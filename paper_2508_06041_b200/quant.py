@@ -296,6 +296,58 @@ def load_store(path: str) -> BitPlaneStore:
     return BitPlaneStore(layers, n_bits, b_min, config_hash)
 
 
+def load_device_store(path: str, device=None) -> "DeviceBitPlaneStore":
+    """Open a ``.dpqs`` file (quant.py:140-181) straight into device bitplanes.
+
+    Same header checks and errors as ``load_store`` (quant.py:160-167), but each
+    layer's packed code stream is uploaded as it lies on disk and repacked into
+    MSB-first bitplanes by the device (``dpq_layer_desc.code_bytes = 0``): the
+    host never materialises uint16 codes (numpy ``unpack_codes`` is the slow
+    part of the reference loader at 7B+ sizes). The result quacks like a
+    ``BitPlaneStore`` for the decode engine (``DeviceBitPlaneStore``).
+    """
+    with open(path, "rb") as f:
+        if f.read(4) != STORE_MAGIC:
+            raise QuantError("not a dpq store file")
+        version, n_bits, b_min, bit_order, n_layers = struct.unpack("<IBBBI", f.read(11))
+        if version != STORE_VERSION:
+            raise QuantError(f"unsupported store version {version}")
+        if bit_order != 0:
+            raise QuantError("unsupported code bit order")
+        config_hash = f.read(64).decode("ascii")
+        entries = []
+        for _ in range(n_layers):
+            (nlen,) = struct.unpack("<H", f.read(2))
+            lid = LayerId.from_name(f.read(nlen).decode("ascii"))
+            rows, cols, plen = struct.unpack("<IIQ", f.read(16))
+            if plen != (rows * cols * n_bits + 7) // 8:
+                raise QuantError(f"{lid.name}: packed code length {plen} != rows*cols*n_bits/8")
+            lo = np.frombuffer(f.read(4 * rows), dtype="<f4").astype(np.float32)
+            hi = np.frombuffer(f.read(4 * rows), dtype="<f4").astype(np.float32)
+            blob = np.frombuffer(f.read(plen), dtype=np.uint8)
+            if blob.size != plen:
+                raise QuantError(f"{lid.name}: truncated store file")
+            entries.append((lid, rows, cols, lo, hi, blob))
+    import torch
+    dev = torch.device(device if device is not None else _lib.torch_device())
+    # the engine indexes layers in (block, kind) order: 7*b + k
+    entries.sort(key=lambda e: (e[0].block, KINDS.index(e[0].kind)))
+    descs = (_lib.LayerDesc * len(entries))()
+    for i, (lid, rows, cols, lo, hi, blob) in enumerate(entries):
+        descs[i] = _lib.LayerDesc(rows, cols, n_bits, b_min, 0, 0, blob.ctypes.data,
+                                  lo.ctypes.data, hi.ctypes.data)
+    h = C.c_void_p()
+    with torch.cuda.device(dev):
+        _lib.call("dpq_store_create", dev.index, len(entries), descs, C.byref(h))
+    ds = DeviceStore.__new__(DeviceStore)
+    ds.device, ds.handle = dev, h
+    ds.shapes = [(e[1], e[2]) for e in entries]
+    ds.bits = [(b_min, n_bits)] * len(entries)
+    ds._fin = weakref.finalize(ds, _destroy, "dpq_store_destroy", h.value)
+    return DeviceBitPlaneStore(config_hash, n_bits, b_min,
+                               {e[0]: (e[1], e[2]) for e in entries}, ds)
+
+
 def file_hash(path: str) -> str:
     h = hashlib.sha256()
     with open(path, "rb") as f:
