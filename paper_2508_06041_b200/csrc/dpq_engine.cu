@@ -409,13 +409,17 @@ __device__ __forceinline__ int base_bit(const Layer& L, const ECtl& C) {
 // Work of CTA cta: lanes 0..1 of the calling warp compute ga / gb in parallel.
 __device__ __forceinline__ void build_work_warp(const Op& O, const ECtl& C, int cta, int G, Work& W) {
   const int lane = threadIdx.x & 31;
-  int nb[kMaxOpLayers];
-  int wsum = 0;
-  for (int li = 0; li < O.n_layers; ++li) {
-    nb[li] = base_bit(O.L[li], C);
-    wsum += O.L[li].n_tiles * nb[li];
+  // base bits straight into the (shared-memory) work record: a dynamically
+  // indexed local array would live in local memory
+  const int nbl = lane < O.n_layers ? base_bit(O.L[lane], C) : 0;
+  if (lane < O.n_layers) {
+    W.nb[lane] = nbl;
+    W.fin[lane] = nbl;
   }
-  const unsigned N = (unsigned)wsum * (unsigned)O.n_win;   // host guarantees N * G < 2^32
+  const int wtot = wsum(lane < O.n_layers ? O.L[lane].n_tiles * nbl : 0);
+  __syncwarp();
+  const int* nb = W.nb;
+  const unsigned N = (unsigned)wtot * (unsigned)O.n_win;   // host guarantees N * G < 2^32
   if (lane < 2) {
     int item;
     if (O.n_win <= G) {
@@ -424,44 +428,15 @@ __device__ __forceinline__ void build_work_warp(const Op& O, const ECtl& C, int 
       const int w = (int)((unsigned)cta * (unsigned)O.n_win / (unsigned)G);
       const int cb = (w * G + O.n_win - 1) / O.n_win, ce = ((w + 1) * G + O.n_win - 1) / O.n_win;
       const int m = ce - cb, idx = cta - cb + lane;
-      item = w * wsum + (int)((unsigned)idx * (unsigned)wsum / (unsigned)m);
+      item = w * wtot + (int)((unsigned)idx * (unsigned)wtot / (unsigned)m);
     } else {
       item = (int)(N * (unsigned)(cta + lane) / (unsigned)G);
     }
-    const int g = group_at(O, nb, wsum, item);
+    const int g = group_at(O, nb, wtot, item);
     if (lane == 0) W.ga = g;
     else W.gb = g;
   }
-  if (lane < O.n_layers) {
-    W.nb[lane] = nb[lane];
-    W.fin[lane] = nb[lane];
-  }
 }
-
-// Run list of work W (one thread; decision independent).
-__device__ void build_runs(const Op& O, const Work& W, RunList& R) {
-  R.n = 0;
-  if (W.ga >= W.gb) return;
-  const int nt = O.n_tiles;
-  const int wa = W.ga / nt, wb = (W.gb - 1) / nt;
-  for (int w = wa; w <= wb; ++w) {
-    const int lo = max(W.ga - w * nt, 0), hi = min(W.gb - w * nt, nt);
-    for (int li = 0; li < O.n_layers; ++li) {
-      const Layer& L = O.L[li];
-      const int t0 = max(lo, L.tile_off), t1 = min(hi, L.tile_off + L.n_tiles);
-      for (int t = t0; t < t1; t += kSlotTiles) {
-        if (R.n >= kMaxRuns) __trap();       // host sizing guarantees this cannot happen
-        Run& r = R.r[R.n++];
-        r.li = (short)li;
-        r.w = (short)w;
-        r.t0 = (short)t;
-        r.nt = (short)min(kSlotTiles, t1 - t);
-        r.k0 = (short)(w * nt + t - W.ga);
-      }
-    }
-  }
-}
-
 
 // Warp-parallel run list + base FIFO offsets + task -> run table of work W
 // (the serial loops were a dependent chain of shared-memory round trips,
