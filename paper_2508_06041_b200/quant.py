@@ -60,7 +60,7 @@ class DeviceStore:
 
     @staticmethod
     def from_device_codes(specs, device=None):
-        """Build from device-resident codes: specs = [(codes_dev(uint16 tensor),
+        """Build from device-resident codes: specs = [(codes_dev(uint16 or uint8 tensor),
         lo(np f32), hi(np f32), n_bits, b_min)] (large synthetic models)."""
         import torch
         self = DeviceStore.__new__(DeviceStore)
@@ -72,8 +72,8 @@ class DeviceStore:
             hi = np.ascontiguousarray(hi, dtype=np.float32)
             keep += [lo, hi]
             rows, cols = codes.shape
-            descs[i] = _lib.LayerDesc(rows, cols, n_bits, b_min, 2, 1, codes.data_ptr(),
-                                      lo.ctypes.data, hi.ctypes.data)
+            descs[i] = _lib.LayerDesc(rows, cols, n_bits, b_min, codes.element_size(), 1,
+                                      codes.data_ptr(), lo.ctypes.data, hi.ctypes.data)
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             _lib.call("dpq_store_create", self.device.index, len(specs), descs, C.byref(h))
