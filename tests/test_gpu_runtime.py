@@ -427,3 +427,29 @@ def test_engine_long_context_chunked_attention(d_model, n_heads):
     lg, lo = np.array(lg), np.array(lo)
     assert np.max(np.abs(lg - lo)) <= 1e-4 * np.max(np.abs(lo))
     assert np.max(np.abs(lg[250:] - lo[250:])) <= 1e-4 * np.max(np.abs(lo))   # the chunked positions
+
+
+def test_trace_pulled_lazily_keeps_positions(report_setup):
+    """The trace is pulled from the device on access (not per step): records
+    keep the positions of the dynamic steps, also around non-dynamic steps and
+    device-loop launches, and mid-run reads do not change the result."""
+    S = report_setup
+    plan = R.load_plan(plan_path("dp_t3.5"), S.store)
+    prompt = S.tokens[:4]
+
+    def run(peek):
+        eng = R.DecodeEngine(S.weights, S.store, plan, S.store_hash)
+        eng.prefill(prompt)
+        for t in S.tokens[4:7]:
+            eng.step(int(t), dynamic=True, want_logits=False)
+            if peek:
+                assert len(eng.trace.steps) == eng.position - len(prompt)
+        eng.step(int(S.tokens[7]), dynamic=False, want_logits=False)
+        eng.decode_greedy(2)
+        return eng.trace
+
+    a, b = run(True), run(False)
+    assert [s.step for s in a.steps] == [4, 5, 6, 8, 9]
+    assert [s.step for s in b.steps] == [4, 5, 6, 8, 9]
+    assert [s.bits for s in a.steps] == [s.bits for s in b.steps]
+    assert a.estimator_ops == b.estimator_ops > 0
