@@ -154,6 +154,24 @@ def empirical_quantile(sorted_vals, r: float) -> float:
     return float(sorted_vals[idx])
 
 
+def translate_threshold(err_list, p: float, l: int):
+    """Threshold of a (l, l+1) layer from an error list (estimator.py:106-121):
+    r = 1 - (p - l); r >= 1 -> +inf (always low), r <= 0 -> -inf (always
+    high), else the empirical r-quantile. Returns (T, r). The list is used in
+    the order given, like the reference (callers pass it sorted)."""
+    err_list = np.asarray(err_list, dtype=np.float64)
+    if len(err_list) == 0:
+        raise ValueError("empty error list")
+    if not (l <= p <= l + 1):
+        raise ValueError(f"p={p} outside [{l}, {l + 1}]")
+    r = 1.0 - (p - l)
+    if r >= 1.0:
+        return math.inf, r
+    if r <= 0.0:
+        return -math.inf, r
+    return empirical_quantile(err_list, r), r
+
+
 def build_projection(delta_rows_fn, rows: int, k: int, seed: int, A=None) -> np.ndarray:
     """G = A @ dW with A ~ N(0,1)/sqrt(k) (estimator.py:190-200). ``delta_rows_fn``
     returns dW as a float64 (rows, cols) array or a CUDA tensor; the product

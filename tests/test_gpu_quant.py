@@ -195,3 +195,23 @@ def test_select_precision_api_matches_oracle(toy_store):
     assert R.select_precision(R.PlanLayer(lid, 6, 3.5, (3, 4), err * 2, 0.5, est), x)[0] == 3
     bit, e, cost = R.select_precision(R.PlanLayer(lid, 6, 3.5, (3, 4), err / 2, 0.5, est), x)
     assert bit == 4 and e == pytest.approx(err, rel=1e-5) and cost == 32 * 32
+
+
+@pytest.mark.parametrize("shape,pair", [((200, 700), (3, 4)), ((1000, 96), (4, 6))])
+def test_build_projection_on_device_matches_oracle(shape, pair):
+    """estimator.py:190-200 with dW dequantized on the device (fp64) and the
+    A @ dW product formed by the GPU: equals the oracle's host product."""
+    rng = np.random.default_rng(shape[0])
+    q = Q.quantize_layer(rng.normal(0, 1 / np.sqrt(shape[1]), shape), 6, 3)
+    l, h = pair
+    ds, i = q.device_handle()
+
+    def dW():
+        d = ds.dequantize(i, h)
+        d -= ds.dequantize(i, l)
+        return d
+
+    G = E.build_projection(dW, shape[0], 64, seed=9)
+    G_ref = O.build_projection_G(O.as_layer(q), l, h, 64, 9)
+    assert G.shape == (64, shape[1])
+    np.testing.assert_allclose(G, G_ref, rtol=1e-10, atol=1e-12 * np.abs(G_ref).max())

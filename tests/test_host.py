@@ -224,3 +224,43 @@ def test_qos_and_trace_helpers(tmp_path):
     p = str(tmp_path / "t.csv")
     traces[0].export_csv(p)
     assert open(p).read().splitlines() == ["step,layer,bit,estimate", "0,block0.q,3,"]
+
+
+def test_translate_threshold_matches_oracle():
+    """estimator.py:94-121 (threshold translation for offline calibration):
+    lattice quantiles, the +/-inf sentinels at r = 1 / r = 0, argument errors."""
+    from paper_2508_06041_b200 import estimator as E
+    rng = np.random.default_rng(4)
+    for n in (1, 7, 10, 64, 257):
+        errs = np.sort(rng.random(n))
+        for l in (3, 4):
+            for frac in (0.0, 0.1, 0.3, 0.5, 1 / 3, 0.7, 0.99, 1.0):
+                p = l + frac
+                assert E.translate_threshold(errs, p, l) == O.translate_threshold(errs, p, l)
+    assert E.translate_threshold([0.5], 3.0, 3)[0] == np.inf
+    assert E.translate_threshold([0.5], 4.0, 3)[0] == -np.inf
+    with pytest.raises(ValueError):
+        E.translate_threshold([], 3.5, 3)
+    with pytest.raises(ValueError):
+        E.translate_threshold([0.1], 4.5, 3)
+
+
+def test_threshold_oracle_pinned_to_reference():
+    """The oracle's quantile / translation equal the reference's own functions
+    (run here only, where /root/reference exists)."""
+    import importlib
+    import sys
+    src = "/root/reference/pkg/src"
+    if not os.path.isdir(src):
+        pytest.skip("reference not present")
+    sys.path.insert(0, src)
+    try:
+        ref = importlib.import_module("dpq.estimator")
+    finally:
+        sys.path.remove(src)
+    rng = np.random.default_rng(5)
+    for n in (1, 10, 33):
+        errs = np.sort(rng.random(n))
+        for frac in (0.0, 0.3, 0.5, 0.7, 1.0):
+            e = ref.translate_threshold(errs, 3 + frac, 3)
+            assert (e.T, e.r_quantile) == O.translate_threshold(errs, 3 + frac, 3)
