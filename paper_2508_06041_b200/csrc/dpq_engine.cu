@@ -15,14 +15,17 @@
 //    depends on;
 //  * the any-precision GEMV streams only planes 0..b-1 of the nested store
 //    (quant.py:74): base planes (known before the decision) are split evenly
-//    over the grid at (tile, window) granularity, decision-dependent extra
-//    planes are split evenly again after the decision; per item a warp does
-//    64 conflict-free byte-LUT lookups (8 weight bits per LDS);
-//  * every warp keeps a DEPTH-deep register ring of plane loads that runs
-//    ahead across op boundaries (the next op's base planes are issued before
-//    the barrier), and each CTA prefetches its next-op share into L2;
-//  * the last contributor of a (tile | up-gate tile pair) reduces it over
-//    windows in fixed order and applies the affine epilogue
+//    over the grid at (tile, window) granularity; a layer that decides high
+//    adds its extra planes [nb, fin) for the same groups of the same CTA;
+//    per item a warp does 64 conflict-free byte-LUT lookups (8 weight bits
+//    per LDS);
+//  * one TMA producer warp per CTA streams (run, plane) bulk copies into a
+//    shared-memory ring (mbarrier full / empty per slot) that runs ahead
+//    across op boundaries: the next op's base planes are issued before the
+//    barrier, its extra planes once the decision is published;
+//  * reduce unit u (a tile, or an up|gate tile pair) belongs to CTA u mod G,
+//    which sums its window partials in fixed window order and applies the
+//    affine epilogue
 //    y = s_in * (lo * sum x + span 2^-b (S + sum x / 2)) (exact restatement of
 //    quant.py:74-78 @ x), residual add / SiLU(gate)*up (runtime.py:364-370),
 //    and feeds the next estimators.
