@@ -348,20 +348,23 @@ def run_ours(args):
     achieved = alg / (ms * 1e-3) / 1e9
     peak, peak_kind = measured_peak()
 
-    # per-op GB/s (critical path from stage stamps) on a separate instrumented session
-    os.environ["DPQ_DEBUG_TIMES"] = "1"
-    eng2 = R.DecodeEngine(weights, store, plan, g_dtype=args.g_dtype)
-    del os.environ["DPQ_DEBUG_TIMES"]
-    eng2.prefill(prompt)
-    eng2.decode_greedy(8)
-    op_t, op_b, crit = op_stage_times(eng2, store, plan, ids, g_bytes)
-    eng2.close()
-    per_op = {}
-    for nm, i0 in (("qkv", 0), ("o", 1), ("upgate", 2), ("down", 3)):
-        t = op_t[i0::4].sum()
-        b = op_b[i0::4].sum()
-        per_op[nm] = {"us": float(t / (len(op_t) // 4)), "GBps": float(b / (t * 1e-6) / 1e9)}
-    gemv_gbs = float(op_b.sum() / (op_t.sum() * 1e-6) / 1e9)
+    # per-op GB/s (critical path from stage stamps) on a separate instrumented
+    # session; only the TMA engine (session kind 2) records stage stamps
+    per_op, gemv_gbs = None, None
+    if engine_kind == 2:
+        os.environ["DPQ_DEBUG_TIMES"] = "1"
+        eng2 = R.DecodeEngine(weights, store, plan, g_dtype=args.g_dtype)
+        del os.environ["DPQ_DEBUG_TIMES"]
+        eng2.prefill(prompt)
+        eng2.decode_greedy(8)
+        op_t, op_b, crit = op_stage_times(eng2, store, plan, ids, g_bytes)
+        eng2.close()
+        per_op = {}
+        for nm, i0 in (("qkv", 0), ("o", 1), ("upgate", 2), ("down", 3)):
+            t = op_t[i0::4].sum()
+            b = op_b[i0::4].sum()
+            per_op[nm] = {"us": float(t / (len(op_t) // 4)), "GBps": float(b / (t * 1e-6) / 1e9)}
+        gemv_gbs = float(op_b.sum() / (op_t.sum() * 1e-6) / 1e9)
 
     # selector overhead: sentinel-static plans at l and h, interpolated at the
     # realized effective bits (same engine, same decode loop)
@@ -417,11 +420,12 @@ def run_ours(args):
                        "per_op": per_op, "gemv_stage_GBps": gemv_gbs, "build_s": build_s},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "engine_kernel (whole decode step: fused selector + bitplane GEMVs, "
-                                   "attention, lm_head; one launch per timed region)",
+                         "kernel": ("engine_kernel (whole decode step: fused selector + bitplane GEMVs, "
+                                    "attention, lm_head; one launch per timed region)") if engine_kind == 2
+                         else "session step kernels (the TMA engine declined this shape)",
                          "alg_bytes_per_step": alg / args.steps},
             "clocks": clk,
-            "gpu_launches": 1,
+            "gpu_launches": 1 if engine_kind == 2 else None,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 12,
                     "d2h_bytes_per_step": 4 * cfg.vocab}}
     if rank == 0 and not args.no_cpu_baseline and host:
@@ -429,7 +433,8 @@ def run_ours(args):
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                                 "sample": sample}
     traffic_path = os.path.join(ROOT, "profiles", "engine_traffic.json")
-    if os.path.exists(traffic_path):
+    # the committed ncu DRAM figure is of the default workload only
+    if os.path.exists(traffic_path) and engine_kind == 2 and args.config == "llama3_8b" and args.target == 3.5:
         try:
             line["roofline"]["traffic"] = json.load(open(traffic_path)).get("bytes_per_step")
         except Exception:

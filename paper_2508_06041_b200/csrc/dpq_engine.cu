@@ -478,7 +478,7 @@ __device__ int build_runs_warp(const Op& O, const Work& W, RunList& R, short* fo
   const int n_runs = __shfl_sync(0xffffffffu, rb, 31), n_items = __shfl_sync(0xffffffffu, ib, 31);
   rb -= nr;
   ib -= items;
-  if (n_runs > kMaxRuns) __trap();
+  if (n_runs > kMaxRuns || W.gb - W.ga > kMaxTiles) __trap();   // host sizing (engine_eligible) violated
   for (int q = 0; q < nr; ++q) {
     Run& r = R.r[rb + q];
     r.li = (short)li;

@@ -365,20 +365,51 @@ def test_engine_matches_multi_kernel_and_is_deterministic(gqa):
 
 
 @pytest.mark.gpu
-def test_engine_llama_width_two_blocks():
-    """The engine at the bench's layer widths (d 4096, 32 heads / 8 KV, d_ff
-    14336: 8 and 28 column windows, window-aligned CTA split, several runs per
-    CTA, extra planes across windows) against the per-op kernel graph under
-    forced-bits replay, and bit-identical across runs."""
+@pytest.mark.parametrize("width", ["llama3_8b", "llama2_70b"])
+def test_engine_llama_width_two_blocks(width):
+    """The engine at the bench's layer widths (8B: d 4096, 32 heads / 8 KV,
+    d_ff 14336, 8 and 28 column windows; 70B: d 8192, 64 heads / 8 KV, d_ff
+    28672, 16 and 56 windows, a 6-bit overlay with mixed (3,4) / (4,5) pairs;
+    window-aligned CTA split, several runs per CTA, extra planes across
+    windows) against the per-op kernel graph under forced-bits replay, and
+    bit-identical across runs."""
     import paper_2508_06041_b200.synth as S
-    cfg = M.ModelConfig(n_blocks=2, d_model=4096, n_heads=32, d_ff=14336, vocab=256, seq_cap=64,
-                        n_kv_heads=8)
-    w, store, _ = S.random_device_model(cfg, 4, 3, seed=77)
+    if width == "llama3_8b":
+        cfg = M.ModelConfig(n_blocks=2, d_model=4096, n_heads=32, d_ff=14336, vocab=256, seq_cap=64,
+                            n_kv_heads=8)
+        n_bits = 4
+    else:
+        cfg = M.ModelConfig(n_blocks=1, d_model=8192, n_heads=64, d_ff=28672, vocab=256, seq_cap=64,
+                            n_kv_heads=8)
+        n_bits = 6
+    w, store, _ = S.random_device_model(cfg, n_bits, 3, seed=77)
     ids = store.ordered_ids()
-    pairs = {l: (3, 4) for l in ids}
-    plan = S.projection_plan(store, pairs, {l: 4 for l in ids}, k=64, seed=3, target=3.5)
+    pairs = {l: ((3, 4) if n_bits == 4 or i % 2 == 0 else (4, 5)) for i, l in enumerate(ids)}
+    plan = S.projection_plan(store, pairs, {l: pairs[l][1] for l in ids}, k=64, seed=3, target=3.5)
     toks = np.random.default_rng(12).integers(0, 256, 14)
     S.calibrate_thresholds(w, store, plan, toks[:6], high_rate=0.5)
+    if width == "llama2_70b":
+        # more (tile, window) groups per CTA than the engine's task tables
+        # hold: the session must decline the engine (not overrun shared
+        # memory) and decode on the per-op kernel graph
+        from paper_2508_06041_b200 import _lib
+        outs = []
+        for _ in range(2):
+            eng = R.DecodeEngine(w, store, plan)
+            assert _lib.load().dpq_session_is_persistent(eng._h) != 2     # not the TMA engine
+            lg = [eng.step(int(toks[0]), dynamic=False)]
+            lg += [eng.step(int(t), dynamic=True) for t in toks[1:5]]
+            outs.append((np.array(lg), [s.bits for s in eng.trace.steps]))
+            eng.close()
+        assert np.all(np.isfinite(outs[0][0]))
+        assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
+        old = R.DecodeEngine(w, store, plan, use_persistent=False)
+        lg = [old.step(int(toks[0]), dynamic=False)]
+        for t, bits in zip(toks[1:5], outs[0][1]):
+            lg.append(old.step(int(t), dynamic=True, forced_bits=bits))
+        lg = np.array(lg)
+        assert np.max(np.abs(lg - outs[0][0])) <= 1e-4 * np.max(np.abs(lg))
+        return
     runs = []
     for _ in range(2):
         eng = R.DecodeEngine(w, store, plan)
@@ -389,7 +420,7 @@ def test_engine_llama_width_two_blocks():
         runs.append((np.array(lg), [s.bits for s in eng.trace.steps]))
         eng.close()
     assert np.array_equal(runs[0][0], runs[1][0]) and runs[0][1] == runs[1][1]
-    highs = np.mean([[b[l] == 4 for l in ids] for b in runs[0][1]])
+    highs = np.mean([[b[l] == pairs[l][1] for l in ids] for b in runs[0][1]])
     assert 0.05 < highs < 0.95                    # both precisions exercised
     old = R.DecodeEngine(w, store, plan, use_persistent=False)
     lg = [old.step(int(toks[0]), dynamic=False)]
