@@ -44,7 +44,9 @@ constexpr int kSlotTiles = 8;      // tiles per ring slot (one plane of up to 8 
 constexpr int kSlotBytes = kSlotTiles * 2048;
 constexpr int kMaxSlots = 8;       // ring slots (power of two: index arithmetic by shifts)
 constexpr int kMaxRuns = 96;       // (layer, window, <= 8 tiles) runs per op per CTA
-constexpr int kMaxTiles = 128;
+constexpr int kMaxTiles = 128;     // tasks whose parked base sums live in shared memory
+constexpr int kMaxTasks = 384;     // (tile, window) groups per CTA and op; parked sums of tasks
+                                   // [kMaxTiles, kMaxTasks) go to a per-CTA global scratch (Prog.park)
 
 constexpr int kDbgRec = 128;   // debug record per (stage, CTA): [0,8) phase stamps, [8,88) 5 per consumer warp, [88,96) producer, [96,128) clock64 sub-stamps
 constexpr double kFxSum = 4294967296.0;       // 2^32: sum v
@@ -118,6 +120,7 @@ struct Prog {
   int slot_stride;
   int slot_max_win;
   float* attn_part;        // [H][max_chunks][hd + 2]
+  float* park;             // [G][kMaxTasks - kMaxTiles][32] parked base sums beyond the shared table
   unsigned* attn_cnt;      // [KV]
   int attn_max_chunks;
   int attn_emit;           // attention emits its heads' tiles (head_dim % 32 == 0), else an EMIT stage
@@ -359,7 +362,7 @@ struct Smem {
   Work pw;                 // producer work
   RunList pruns;           // producer run list
   short pfo[kMaxRuns];     // producer scratch (FIFO offsets / task table it does not need)
-  unsigned char ptask[kMaxTiles];
+  unsigned char ptask[kMaxTasks];
   unsigned long long full[kMaxSlots], empty[kMaxSlots];   // ring mbarriers
   volatile int seq[kMaxSlots];       // FIFO index armed in each slot (phase disambiguation)
   unsigned slot_off[kMaxSlots];      // slot byte offset from the dynamic smem base
@@ -379,7 +382,7 @@ struct Smem {
   int head_i[NW];
   float sbuf[kMaxTiles][32];         // base-pass S of tiles whose layer has extra planes
   short fo_bo[kMaxRuns], fo_eo[kMaxRuns], fo_xt[kMaxRuns];
-  unsigned char task_rb[kMaxTiles], task_rx[kMaxTiles];   // run of each base / extra task (kMaxRuns <= 255)
+  unsigned char task_rb[kMaxTasks], task_rx[kMaxTasks];   // run of each base / extra task (kMaxRuns <= 255)
   int vtile[kMaxTiles];              // reduce: emit tile of the CTA's i-th unit (values in sbuf)
 };
 
@@ -478,7 +481,7 @@ __device__ int build_runs_warp(const Op& O, const Work& W, RunList& R, short* fo
   const int n_runs = __shfl_sync(0xffffffffu, rb, 31), n_items = __shfl_sync(0xffffffffu, ib, 31);
   rb -= nr;
   ib -= items;
-  if (n_runs > kMaxRuns || W.gb - W.ga > kMaxTiles) __trap();   // host sizing (engine_eligible) violated
+  if (n_runs > kMaxRuns || W.gb - W.ga > kMaxTasks) __trap();   // host sizing (engine_eligible) violated
   for (int q = 0; q < nr; ++q) {
     Run& r = R.r[rb + q];
     r.li = (short)li;
@@ -1093,7 +1096,10 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
         const int nb = W.nb[q.li], fin = W.fin[q.li];
         const int p0 = kind ? nb : 0, p1 = kind ? fin : nb;
         const int jr = sm.cons_j + (kind ? sm.fo_eo[r] : sm.fo_bo[r]);   // FIFO base from shared memory (no spill reload)
-        float S = kind ? sm.sbuf[q.k0 + i][lane] : 0.f;
+        const int pk = q.k0 + i;                                   // task (group) index in [ga, gb)
+        float S = 0.f;
+        if (kind) S = pk < kMaxTiles ? sm.sbuf[pk][lane]
+                                     : __ldcg(P.park + ((size_t)cta * (kMaxTasks - kMaxTiles) + pk - kMaxTiles) * 32 + lane);
         for (int p = p0; p < p1; ++p) {
           const int j = jr + (p - p0);
           const int slot = j & (kMaxSlots - 1);
@@ -1128,7 +1134,8 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
         }
         const int t = q.t0 + i;
         if (!kind && fin > nb) {
-          sm.sbuf[q.k0 + i][lane] = S;                              // park the base part
+          if (pk < kMaxTiles) sm.sbuf[pk][lane] = S;                // park the base part
+          else __stcg(P.park + ((size_t)cta * (kMaxTasks - kMaxTiles) + pk - kMaxTiles) * 32 + lane, S);
         } else {
           __stcg(P.slot + (size_t)q.w * P.slot_stride + (size_t)t * 32 + lane,
                  (unsigned long long)epoch << 32 | __float_as_uint(S));

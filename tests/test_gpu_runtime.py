@@ -371,8 +371,10 @@ def test_engine_llama_width_two_blocks(width):
     d_ff 14336, 8 and 28 column windows; 70B: d 8192, 64 heads / 8 KV, d_ff
     28672, 16 and 56 windows, a 6-bit overlay with mixed (3,4) / (4,5) pairs;
     window-aligned CTA split, several runs per CTA, extra planes across
-    windows) against the per-op kernel graph under forced-bits replay, and
-    bit-identical across runs."""
+    windows; at 70B widths a CTA owns up to ~270 groups of up|gate, so parked
+    base sums overflow the shared table into the global scratch) against the
+    per-op kernel graph under forced-bits replay, and bit-identical across
+    runs."""
     import paper_2508_06041_b200.synth as S
     if width == "llama3_8b":
         cfg = M.ModelConfig(n_blocks=2, d_model=4096, n_heads=32, d_ff=14336, vocab=256, seq_cap=64,
@@ -388,32 +390,11 @@ def test_engine_llama_width_two_blocks(width):
     plan = S.projection_plan(store, pairs, {l: pairs[l][1] for l in ids}, k=64, seed=3, target=3.5)
     toks = np.random.default_rng(12).integers(0, 256, 14)
     S.calibrate_thresholds(w, store, plan, toks[:6], high_rate=0.5)
-    if width == "llama2_70b":
-        # more (tile, window) groups per CTA than the engine's task tables
-        # hold: the session must decline the engine (not overrun shared
-        # memory) and decode on the per-op kernel graph
-        from paper_2508_06041_b200 import _lib
-        outs = []
-        for _ in range(2):
-            eng = R.DecodeEngine(w, store, plan)
-            assert _lib.load().dpq_session_is_persistent(eng._h) != 2     # not the TMA engine
-            lg = [eng.step(int(toks[0]), dynamic=False)]
-            lg += [eng.step(int(t), dynamic=True) for t in toks[1:5]]
-            outs.append((np.array(lg), [s.bits for s in eng.trace.steps]))
-            eng.close()
-        assert np.all(np.isfinite(outs[0][0]))
-        assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
-        old = R.DecodeEngine(w, store, plan, use_persistent=False)
-        lg = [old.step(int(toks[0]), dynamic=False)]
-        for t, bits in zip(toks[1:5], outs[0][1]):
-            lg.append(old.step(int(t), dynamic=True, forced_bits=bits))
-        lg = np.array(lg)
-        assert np.max(np.abs(lg - outs[0][0])) <= 1e-4 * np.max(np.abs(lg))
-        return
     runs = []
     for _ in range(2):
         eng = R.DecodeEngine(w, store, plan)
-        assert eng.persistent
+        from paper_2508_06041_b200 import _lib
+        assert _lib.load().dpq_session_is_persistent(eng._h) == 2      # the TMA engine
         lg = [eng.step(int(toks[0]), dynamic=False)]
         for t in toks[1:]:
             lg.append(eng.step(int(t), dynamic=True))
