@@ -365,7 +365,7 @@ def test_engine_matches_multi_kernel_and_is_deterministic(gqa):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("width", ["llama3_8b", "llama2_70b"])
+@pytest.mark.parametrize("width", ["llama3_8b", "llama2_7b", "llama2_70b"])
 def test_engine_llama_width_two_blocks(width):
     """The engine at the bench's layer widths (8B: d 4096, 32 heads / 8 KV,
     d_ff 14336, 8 and 28 column windows; 70B: d 8192, 64 heads / 8 KV, d_ff
@@ -379,6 +379,9 @@ def test_engine_llama_width_two_blocks(width):
     if width == "llama3_8b":
         cfg = M.ModelConfig(n_blocks=2, d_model=4096, n_heads=32, d_ff=14336, vocab=256, seq_cap=64,
                             n_kv_heads=8)
+        n_bits = 4
+    elif width == "llama2_7b":             # MHA; d_ff 11008 = 21.5 windows (ragged last window)
+        cfg = M.ModelConfig(n_blocks=2, d_model=4096, n_heads=32, d_ff=11008, vocab=256, seq_cap=64)
         n_bits = 4
     else:
         cfg = M.ModelConfig(n_blocks=1, d_model=8192, n_heads=64, d_ff=28672, vocab=256, seq_cap=64,
