@@ -44,7 +44,11 @@ constexpr int kSlotTiles = 8;      // tiles per ring slot (one plane of up to 8 
 constexpr int kSlotBytes = kSlotTiles * 2048;
 constexpr int kMaxSlots = 8;       // ring slots (power of two: index arithmetic by shifts)
 constexpr int kMaxRuns = 96;       // (layer, window, <= 8 tiles) runs per op per CTA
-constexpr int kMaxTiles = 128;     // tasks whose parked base sums live in shared memory
+constexpr int kMaxTiles = 128;
+// Estimator accumulator element i of a set lives at word i * kAccSpread: one
+// 128-byte L2 line per element, so the fixed-point red.adds every output tile
+// sends to the same k + 1 elements do not serialize on a handful of lines.
+constexpr int kAccSpread = 16;     // tasks whose parked base sums live in shared memory
 constexpr int kMaxTasks = 384;     // (tile, window) groups per CTA and op; parked sums of tasks
                                    // [kMaxTiles, kMaxTasks) go to a per-CTA global scratch (Prog.park)
 
@@ -679,13 +683,13 @@ __device__ __forceinline__ void emit_feed(const Prog& P, const ECtl& C, int fi, 
         }
       }
       const int k0 = sub * 64 + 2 * lane;
-      if (k0 < F.k) red_add64(acc + k0, fx((double)g0, sc));
-      if (k0 + 1 < F.k) red_add64(acc + k0 + 1, fx((double)g1, sc));
+      if (k0 < F.k) red_add64(acc + (size_t)k0 * kAccSpread, fx((double)g0, sc));
+      if (k0 + 1 < F.k) red_add64(acc + (size_t)(k0 + 1) * kAccSpread, fx((double)g1, sc));
     }
   }
   const double dv = (double)v;
   const double q = wsum(dv * dv);
-  if (lane == 0) red_add64(acc + F.k, fx(q, kFxSq));
+  if (lane == 0) red_add64(acc + (size_t)F.k * kAccSpread, fx(q, kFxSq));
 }
 
 // Statistics + every feed of one tile (one warp).
@@ -976,8 +980,8 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
     const long long* acc = P.acc + (size_t)slot * P.acc_stride + Ld.acc;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      if (lane + 32 * q < Ld.k) ga[q] = __ldcg(acc + lane + 32 * q);
-    gsq = __ldcg(acc + Ld.k);
+      if (lane + 32 * q < Ld.k) ga[q] = __ldcg(acc + (size_t)(lane + 32 * q) * kAccSpread);
+    gsq = __ldcg(acc + (size_t)Ld.k * kAccSpread);
   }
   long long vs1 = 0, vs2 = 0;
   if (warp == kStatW + 1) prefetch_own_feeds(P, C, O, cta, G);
@@ -1588,7 +1592,10 @@ __device__ __forceinline__ void begin_stage(const Prog& P, const ECtl& C, int ct
     long long* a = P.acc + (size_t)nxt * P.acc_stride;
     long long* z = P.acc + (size_t)(2 + C.prev_z) * P.acc_stride;
     long long* vs = P.vstat + (size_t)nxt * P.n_inst * 2;
-    for (int i = cta * NT + tid; i < P.acc_stride; i += G * NT) { a[i] = 0; z[i] = 0; }
+    for (int i = cta * NT + tid; i < P.acc_stride / kAccSpread; i += G * NT) {   // the used words only
+      a[(size_t)i * kAccSpread] = 0;
+      z[(size_t)i * kAccSpread] = 0;
+    }
     for (int i = cta * NT + tid; i < P.n_inst * 2; i += G * NT) vs[i] = 0;
   }
   const int n_t = (P.d + 31) / 32;
