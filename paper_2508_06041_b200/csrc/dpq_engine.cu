@@ -44,11 +44,13 @@ constexpr int kSlotTiles = 8;      // tiles per ring slot (one plane of up to 8 
 constexpr int kSlotBytes = kSlotTiles * 2048;
 constexpr int kMaxSlots = 8;       // ring slots (power of two: index arithmetic by shifts)
 constexpr int kMaxRuns = 96;       // (layer, window, <= 8 tiles) runs per op per CTA
-constexpr int kMaxTiles = 128;
-// Estimator accumulator element i of a set lives at word i * kAccSpread: one
-// 128-byte L2 line per element, so the fixed-point red.adds every output tile
-// sends to the same k + 1 elements do not serialize on a handful of lines.
-constexpr int kAccSpread = 16;     // tasks whose parked base sums live in shared memory
+constexpr int kMaxTiles = 128;     // tasks whose parked base sums live in shared memory
+// Estimator accumulator element i of a set (and each input-statistics word)
+// lives at word i * kAccSpread: one 128-byte L2 line per element, so the
+// fixed-point red.adds every output tile sends to the same k + 1 elements do
+// not serialize on a handful of lines. (Replicas per element, summed by the
+// deciding warps, measured slower: the decision's loads are on the critical path.)
+constexpr int kAccSpread = 16;
 constexpr int kMaxTasks = 384;     // (tile, window) groups per CTA and op; parked sums of tasks
                                    // [kMaxTiles, kMaxTasks) go to a per-CTA global scratch (Prog.park)
 
@@ -609,9 +611,9 @@ __device__ __forceinline__ void emit_stats(const Prog& P, const ECtl& C, int ins
   const double dv = (double)v;
   const double s = wsum(dv), q = wsum(dv * dv);
   if (lane == 0) {
-    long long* vs = P.vstat + ((size_t)(C.n_steps_done & 1) * P.n_inst + inst) * 2;
+    long long* vs = P.vstat + ((size_t)(C.n_steps_done & 1) * P.n_inst + inst) * 2 * kAccSpread;
     red_add64(vs, fx(s, kFxSum));
-    red_add64(vs + 1, fx(q, kFxSq));
+    red_add64(vs + kAccSpread, fx(q, kFxSq));
   }
 }
 
@@ -994,9 +996,9 @@ __device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& 
     for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
   }
   if (warp == kStatW && lane == 0) {
-    const long long* vs = P.vstat + ((size_t)cur * P.n_inst + O.in_inst) * 2;
+    const long long* vs = P.vstat + ((size_t)cur * P.n_inst + O.in_inst) * 2 * kAccSpread;
     vs1 = __ldcg(vs);
-    vs2 = __ldcg(vs + 1);
+    vs2 = __ldcg(vs + kAccSpread);
   }
   if (tid == 0) CSTAMP(stamp, 1);
   float* lut = reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLut - smem_u32(&sm)));
@@ -1513,7 +1515,8 @@ __device__ __forceinline__ void head_stage(const Prog& P, const ECtl& C, Smem& s
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cur = C.n_steps_done & 1;
   const int fin_inst = 4 * P.n_blocks;
-  const double s2 = (double)__ldcg(P.vstat + ((size_t)cur * P.n_inst + fin_inst) * 2 + 1) * (1.0 / kFxSq);
+  const double s2 =
+      (double)__ldcg(P.vstat + (((size_t)cur * P.n_inst + fin_inst) * 2 + 1) * kAccSpread) * (1.0 / kFxSq);
   const float inv = (float)(1.0 / sqrt(s2 / (double)P.d + (double)P.eps));
   for (int v = cta * NW + warp; v < P.vocab; v += G * NW) {
     const float* row = P.lm + (size_t)v * P.d;
@@ -1591,12 +1594,12 @@ __device__ __forceinline__ void begin_stage(const Prog& P, const ECtl& C, int ct
   {
     long long* a = P.acc + (size_t)nxt * P.acc_stride;
     long long* z = P.acc + (size_t)(2 + C.prev_z) * P.acc_stride;
-    long long* vs = P.vstat + (size_t)nxt * P.n_inst * 2;
+    long long* vs = P.vstat + (size_t)nxt * P.n_inst * 2 * kAccSpread;
     for (int i = cta * NT + tid; i < P.acc_stride / kAccSpread; i += G * NT) {   // the used words only
       a[(size_t)i * kAccSpread] = 0;
       z[(size_t)i * kAccSpread] = 0;
     }
-    for (int i = cta * NT + tid; i < P.n_inst * 2; i += G * NT) vs[i] = 0;
+    for (int i = cta * NT + tid; i < P.n_inst * 2; i += G * NT) vs[(size_t)i * kAccSpread] = 0;
   }
   const int n_t = (P.d + 31) / 32;
   for (int tt = cta * NW + warp; tt < n_t; tt += G * NW) {
