@@ -26,6 +26,7 @@ extern "C" {
 #define DPQ_ERR_ARG -1      /* bad argument (QuantError / ValueError class)   */
 #define DPQ_ERR_CUDA -2     /* CUDA runtime error                             */
 #define DPQ_ERR_STATE -3    /* handle misuse (e.g. sequence cap exceeded)     */
+#define DPQ_ERR_RANGE -4    /* engine fixed-point accumulator range exceeded  */
 
 typedef struct dpq_store dpq_store;
 typedef struct dpq_plan dpq_plan;

@@ -187,9 +187,7 @@ struct dpq_plan {
   std::vector<dpq_sel_desc> host;    // copy of the descriptors (G pointers cleared)
   Arena arena;
   int any_prev = 0;
-  // engine layout of G^T (tile-blocked, see dpq_engine.cu emit_tile)
-  std::vector<const uint4*> gt;      // per layer, nullptr if none
-  std::vector<int> gt_f16, gt_kpad, gt_fb;
+  std::vector<int> gt_fb;            // per layer: fixed-point fraction bits of the engine's G.x sums
 };
 
 struct OpStep {
@@ -249,6 +247,8 @@ struct dpq_session {
   int eng_smem = 0;
   int eng_grid = 0;
   unsigned long long* eng_dbg = nullptr;
+  std::vector<unsigned long long*> eng_vec;   // tagged vectors (reset to "no epoch")
+  std::vector<size_t> eng_vec_len;
 };
 
 // ---------------------------------------------------------------------------
@@ -628,61 +628,19 @@ extern "C" int dpq_plan_create(dpq_store* s, int n_layers, const dpq_sel_desc* s
       }
       S.G = gdev;
     }
-    p->gt.push_back(nullptr);
-    p->gt_f16.push_back(0);
-    p->gt_kpad.push_back(0);
     p->gt_fb.push_back(0);
-    if (S.sentinel == 0 && d.est_kind == EST_PROJECTION && (d.g_dtype == G_F16 || d.g_dtype == G_F32)) {
-      const int kpad = (d.k + 63) / 64 * 64, nsub = kpad / 64;
-      const int ntile = cdiv(L.cols, 32);
+    if (S.sentinel == 0 && d.est_kind == EST_PROJECTION) {
+      // fixed-point fraction bits of the engine's G.x accumulators:
+      // |G_k . x| <= maxl1 * 2^16 must fit in int64 after scaling by 2^fb
+      // (larger inputs raise the engine's range flag, DPQ_ERR_RANGE)
       double maxl1 = 0.0;
       for (int r = 0; r < d.k; ++r) {
         double a = 0.0;
         for (int c = 0; c < L.cols; ++c) a += std::fabs(d.G[(size_t)r * L.cols + c]);
         maxl1 = std::max(maxl1, a);
       }
-      // |G_k . v| <= maxl1 * 2^16 must fit in int64 after scaling by 2^fb
       int fb = 62 - (int)std::ceil(std::log2(std::max(maxl1, 1e-30) * 65536.0));
-      fb = std::min(52, std::max(8, fb));
-      auto g = [&](int k, int c) -> double {
-        return (k < d.k && c < L.cols) ? d.G[(size_t)k * L.cols + c] : 0.0;
-      };
-      void* dev = nullptr;
-      if (d.g_dtype == G_F16) {
-        std::vector<__half> h((size_t)ntile * nsub * 256 * 8);
-        for (int T = 0; T < ntile; ++T)
-          for (int sb = 0; sb < nsub; ++sb)
-            for (int ch = 0; ch < 8; ++ch)
-              for (int ln = 0; ln < 32; ++ln)
-                for (int rr = 0; rr < 4; ++rr) {
-                  const size_t o = ((((size_t)T * nsub + sb) * 256 + ch * 32 + ln) * 8) + rr * 2;
-                  const int col = 32 * T + 4 * ch + rr, k0 = 64 * sb + 2 * ln;
-                  h[o] = __float2half_rn((float)g(k0, col));
-                  h[o + 1] = __float2half_rn((float)g(k0 + 1, col));
-                }
-        if (p->arena.alloc(&dev, h.size() * 2) ||
-            cudaMemcpy(dev, h.data(), h.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess)
-          return fail(set_err(DPQ_ERR_CUDA, "G^T upload"));
-      } else {
-        std::vector<float> h((size_t)ntile * nsub * 512 * 4);
-        for (int T = 0; T < ntile; ++T)
-          for (int sb = 0; sb < nsub; ++sb)
-            for (int ch = 0; ch < 16; ++ch)
-              for (int ln = 0; ln < 32; ++ln)
-                for (int rr = 0; rr < 2; ++rr) {
-                  const size_t o = ((((size_t)T * nsub + sb) * 512 + ch * 32 + ln) * 4) + rr * 2;
-                  const int col = 32 * T + 2 * ch + rr, k0 = 64 * sb + 2 * ln;
-                  h[o] = (float)g(k0, col);
-                  h[o + 1] = (float)g(k0 + 1, col);
-                }
-        if (p->arena.alloc(&dev, h.size() * 4) ||
-            cudaMemcpy(dev, h.data(), h.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
-          return fail(set_err(DPQ_ERR_CUDA, "G^T upload"));
-      }
-      p->gt.back() = reinterpret_cast<const uint4*>(dev);
-      p->gt_f16.back() = d.g_dtype == G_F16;
-      p->gt_kpad.back() = kpad;
-      p->gt_fb.back() = fb;
+      p->gt_fb.back() = std::min(52, std::max(8, fb));
     }
     if (S.sentinel == 0 && d.prev_residual) p->any_prev = 1;
     p->sel.push_back(S);

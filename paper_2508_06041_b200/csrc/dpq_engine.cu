@@ -1,34 +1,40 @@
 // Persistent decode-step engine for sm_100a (the fast path of dpq_session).
 //
 // One cooperative kernel runs whole decode steps (reference DecodeEngine.step,
-// runtime.py:330-381) on one CTA per SM. A step is a fixed list of stages
-//   BEGIN | per block: QKV  ATTN  O  UPGATE  DOWN | HEAD
-// separated by a grid barrier (monotonic arrival counter). Per op:
+// runtime.py:330-381) on one CTA per SM. A step is the stage list
+//   BEGIN | per block: QKV  O  UPGATE  DOWN | HEAD
+// with NO grid barrier between stages: every vector a stage publishes (the
+// residual stream, q|k|v, SiLU(gate)*up) and every cross-window partial sum
+// is a 64-bit word {float value, u32 epoch} (single-copy atomic, so no fence),
+// and a consumer waits only for the words it reads, tagged with the epoch of
+// the stage that produces them. A relaxed stage counter (arrive after each
+// stage, wait for stage E-2 before writing the buffers of stage E) bounds the
+// skew between CTAs so double-buffered state is never overwritten early.
 //
-//  * precision selection (runtime.py:184-193, estimator.py:35-60) costs no
-//    extra pass and no extra grid sync: the estimator's G.v partials and the
-//    input statistics (sum, sum of squares) are accumulated by the PRODUCER of
-//    the op's input, tile by tile, in its epilogue, into fixed-point int64
-//    accumulators (deterministic). Every CTA of the consuming op reads the
-//    completed accumulators after the barrier and takes the identical
-//    decision est > T (strict, runtime.py:192) before streaming any plane it
-//    depends on;
-//  * the any-precision GEMV streams only planes 0..b-1 of the nested store
-//    (quant.py:74): base planes (known before the decision) are split evenly
-//    over the grid at (tile, window) granularity; a layer that decides high
-//    adds its extra planes [nb, fin) for the same groups of the same CTA;
-//    per item a warp does 64 conflict-free byte-LUT lookups (8 weight bits
-//    per LDS);
-//  * one TMA producer warp per CTA streams (run, plane) bulk copies into a
-//    shared-memory ring (mbarrier full / empty per slot) that runs ahead
-//    across op boundaries: the next op's base planes are issued before the
-//    barrier, its extra planes once the decision is published;
-//  * reduce unit u (a tile, or an up|gate tile pair) belongs to CTA u mod G,
-//    which sums its window partials in fixed window order and applies the
-//    affine epilogue
-//    y = s_in * (lo * sum x + span 2^-b (S + sum x / 2)) (exact restatement of
-//    quant.py:74-78 @ x), residual add / SiLU(gate)*up (runtime.py:364-370),
-//    and feeds the next estimators.
+// Per op stage (layers sharing one input vector), CTA c owns one 512-column
+// window w of the input and a range of (32-row tile, window) groups:
+//  * input: the window's 512 values (tagged) -> shared memory; for the o op
+//    the window is the attention output of the 512 / head_dim heads it holds,
+//    computed in the prologue by every CTA of the window (RoPE, KV append by
+//    one CTA, causal softmax over the KV cache; runtime.py:351-362);
+//  * byte LUT of the window (257 x 64 fp32) from shared memory;
+//  * precision selection (runtime.py:184-193, estimator.py:35-60), fused into
+//    the prologue: the CTAs of window w split the estimator rows; each row is
+//    a G[w] . x[w] partial (G in f32 / f16 / e4m3), added in fixed point
+//    (deterministic) to the layer's accumulator with a release count; the
+//    window's first CTA adds sum x, sum x^2. The TMA producer warp of every
+//    CTA waits for the counts once it has queued the op's base planes,
+//    computes est > T (strict, runtime.py:192) from the same integers, and
+//    only then queues the extra planes of the layers that decided high;
+//  * the any-precision GEMV streams planes 0..b-1 of the nested store
+//    (quant.py:74) through a TMA ring (8 x 16 KB slots, mbarrier full/empty),
+//    64 conflict-free byte-LUT lookups (8 weight bits per LDS) per 2 KB item,
+//    Horner over planes, the per-(tile, window) sum published as a tagged word;
+//  * reduce unit u (a tile, or an up|gate tile pair) belongs to CTA u mod G:
+//    it sums its window partials in fixed window order, applies the affine
+//    epilogue y = s_in (lo sum x + span 2^-b (S + sum x / 2)) (an exact
+//    restatement of quant.py:74-78 @ x), the residual add / SiLU(gate)*up
+//    (runtime.py:364-370), and publishes the output tile.
 #include "dpq_common.cuh"
 
 // Consumer-only CTA barrier (the producer warp never joins).
@@ -37,30 +43,31 @@
 namespace dpq {
 namespace eng {
 
-constexpr int NT = 480;            // consumer threads per CTA (warps 0..14): 16 warps in all -> 128 registers
+constexpr int NT = 480;            // consumer threads per CTA (warps 0..14); 16 warps -> 128 registers
 constexpr int NW = NT / 32;        // consumer warps
-constexpr int NTB = NT + 32;       // block: consumers + one TMA producer warp (warp 15)
+constexpr int NTB = NT + 32;       // + one TMA producer warp (warp 15)
 constexpr int kSlotTiles = 8;      // tiles per ring slot (one plane of up to 8 consecutive tiles)
 constexpr int kSlotBytes = kSlotTiles * 2048;
-constexpr int kMaxSlots = 8;       // ring slots (power of two: index arithmetic by shifts)
+constexpr int kMaxSlots = 8;       // ring slots (power of two)
 constexpr int kMaxRuns = 96;       // (layer, window, <= 8 tiles) runs per op per CTA
-constexpr int kMaxTiles = 128;     // tasks whose parked base sums live in shared memory
-// Estimator accumulator element i of a set (and each input-statistics word)
-// lives at word i * kAccSpread: one 128-byte L2 line per element, so the
-// fixed-point red.adds every output tile sends to the same k + 1 elements do
-// not serialize on a handful of lines. (Replicas per element, summed by the
-// deciding warps, measured slower: the decision's loads are on the critical path.)
-constexpr int kAccSpread = 16;
-constexpr int kMaxTasks = 384;     // (tile, window) groups per CTA and op; parked sums of tasks
-                                   // [kMaxTiles, kMaxTasks) go to a per-CTA global scratch (Prog.park)
+constexpr int kMaxTiles = 128;     // groups whose parked base sums live in shared memory
+constexpr int kMaxTasks = 384;     // (tile, window) groups per CTA and op (the rest park in Prog.park)
+constexpr int kCurSlots = 4;       // accumulator slots of the current step (step % 4)
+constexpr int kPrevSlots = 4;      // previous-step slots (rotation % 4)
+constexpr int kAccSlots = kCurSlots + kPrevSlots;
+constexpr int kStatSpread = 16;    // statistics words: one 128-byte line each
+constexpr int kDbgRec = 8;         // debug stamps per (stage, CTA): [0] start .. [7] end
+constexpr double kFxSum = 4294967296.0;   // 2^32: sum x
+constexpr double kFxSq = 16777216.0;      // 2^24: sum x^2
+constexpr uint32_t kLut = 0x20000;        // the window LUT (absolute shared address)
 
-constexpr int kDbgRec = 128;   // debug record per (stage, CTA): [0,8) phase stamps, [8,88) 5 per consumer warp, [88,96) producer, [96,128) clock64 sub-stamps
-constexpr double kFxSum = 4294967296.0;       // 2^32: sum v
-constexpr double kFxSq = 16777216.0;          // 2^24: sum v^2
-
-enum { ST_BEGIN = 0, ST_OP = 1, ST_ATTN = 2, ST_HEAD = 3, ST_EMIT = 4 };
+enum { ST_BEGIN = 0, ST_OP = 1, ST_HEAD = 3 };
 enum { SRC_IMM = 0, SRC_PREV_STEP = 1, SRC_PREV_BLOCK = 2 };
 enum { FEED_CUR = 0, FEED_CURFB = 1, FEED_PREV = 2 };
+enum { IN_VEC = 0, IN_ATTN = 1 };
+enum { ERR_RANGE = 1 };
+
+typedef unsigned long long u64;
 
 struct Layer {
   const uint4* planes;
@@ -72,11 +79,12 @@ struct Layer {
   int sentinel;            // 0 estimate, 1 low (T = +inf), 2 high (T = -inf)
   int est;                 // EST_NONE / EST_LINEAR / EST_PROJECTION
   int src;                 // SRC_*
-  int k, fb;               // projection rank, fixed-point fraction bits of G.v
-  int acc;                 // offset of the accumulator set (k + 1 int64) in an acc slot
+  int k;                   // projection rank (0: linear)
+  int acc;                 // accumulator set offset in a slot: [k values][sum x^2][count]
+  int cnt_expect;          // count of a complete set: n_win(cols) * (k + 1)
   int trace;               // trace column
   double T, slope, intercept;
-  double fbscale;          // 2^-fb
+  double fbscale;          // 2^-fb of the set's G.x values
 };
 
 struct alignas(16) Op {
@@ -84,26 +92,49 @@ struct alignas(16) Op {
   int n_layers;
   int cols, n_win, n_tiles;
   int rms;                 // input RMS-normalised (runtime.py:383-384)
-  int pair;                // up|gate SiLU pair epilogue -> h
-  int add;                 // residual add into out
-  int in_inst, out_inst;   // vector instances (stats, feeds); out_inst < 0: none
-  const float* in;
-  float* out;
+  int pair;                // up|gate SiLU pair epilogue
+  int add;                 // residual add: out = res_in + y
+  int in_kind;             // IN_VEC / IN_ATTN
+  int in_stage;            // stage (index in the step) publishing `in` (IN_ATTN: the q|k|v stage)
+  int res_stage;           // stage publishing res_in
+  int inst;                // input instance: statistics + estimator feeds
+  int block;
+  int feed_rows;           // projection rows of the input's feeds (split over the window's CTAs)
+  const u64* in;           // tagged input (IN_ATTN: q|k|v)
+  const u64* res_in;       // tagged residual input (add)
+  u64* out;                // tagged output
 };
-
 static_assert(sizeof(Op) % 16 == 0, "Op is copied to shared memory in 16-byte words");
 
-// Producer-side estimator feed of one vector instance.
+// Estimator feed of one input instance: G [n_win][k][512] (f32 / f16 / e4m3 +
+// per-row scale) applied to each window, into the accumulator set `acc`.
 struct Feed {
-  const uint4* Gt;         // tile-blocked G^T (see host), nullptr for linear
-  int f16, k, kpad, fb;
-  int acc;                 // accumulator set offset
+  const void* G;
+  const float* gscale;
+  int dtype, k, row0;      // row0: first row of this feed in the instance's row list
+  int acc;
   int kind;                // FEED_*
+  int pad;
+  double fxscale;          // 2^fb
+};
+
+struct ECtl {
+  int mode;                // MODE_PREFILL / MODE_DYNAMIC            (host-written)
+  int token;               //                                        (host-written)
+  int force;               // decisions replaced by forced_bits      (host-written)
+  int pos;
+  int trace_step;
+  int has_prev;
+  int prime;
+  int async_prev_block;
+  int n_steps_done;        // steps since reset: publish word of the step control
+  int rot;                 // previous-step slot rotations
+  const signed char* forced_bits;
 };
 
 struct Prog {
   int n_stages;
-  const int2* stages;      // (kind, index)
+  const int2* stages;      // (kind, op index)
   const Op* ops;
   const int* feed_begin;   // [n_inst + 1]
   const Feed* feeds;
@@ -114,131 +145,117 @@ struct Prog {
   const float* lm;
   const float* cosv;
   const float* sinv;
-  float* x;
-  float* qkv;
-  float* attn;
-  float* h;
+  u64* xe;                 // tagged x = embed[token]
+  const u64* xfinal;       // tagged residual after the last block
+  int final_stage;
   float* logits;
   float* const* kc;        // [n_blocks] -> [seq_cap][dkv]
   float* const* vc;
-  unsigned long long* slot;  // [max_win][slot_stride]: float S | epoch << 32 (single-copy atomic)
-  float* slot_extra;
-  int slot_stride;
-  int slot_max_win;
-  float* attn_part;        // [H][max_chunks][hd + 2]
+  u64* slot;               // [2][slot_half] tagged (tile, window) partial sums
+  long long slot_half;
   float* park;             // [G][kMaxTasks - kMaxTiles][32] parked base sums beyond the shared table
-  unsigned* attn_cnt;      // [KV]
-  int attn_max_chunks;
-  int attn_emit;           // attention emits its heads' tiles (head_dim % 32 == 0), else an EMIT stage
-  unsigned* head_cnt;
-  long long* acc;          // [5][acc_stride]: cur0 cur1 prev0 prev1 prev2
+  long long* acc;          // [kAccSlots][acc_stride]
   int acc_stride;
-  long long* vstat;        // [2][n_inst][2]
-  unsigned long long* bar;
+  long long* vstat;        // [kCurSlots][n_inst][3 (sum, sumsq, count)][kStatSpread]
+  u64* bar;                // stage arrivals (G per stage)
+  unsigned* head_cnt;
+  unsigned* err;           // sticky error flags (ERR_RANGE: fixed-point range exceeded)
   signed char* tr_bits;
   float* tr_est;
   int n_trace, max_steps;
   int* tok_log;
-  struct ECtl* ctl;
-  int smem_dyn;             // dynamic shared memory bytes of the launch
-  int upper_slots;          // ring slots above the LUT too
-  unsigned long long* dbg; // optional per-stage timestamps [stages][grid][kDbgRec]
-};
-
-struct ECtl {
-  int mode;                // MODE_PREFILL / MODE_DYNAMIC
-  int token;
-  int force;
-  int pos;
-  int trace_step;
-  int has_prev;
-  int prime;
-  int async_prev_block;
-  int n_steps_done;        // all steps since reset (cur slot parity)
-  int prev_w, prev_r, prev_z;
-  const signed char* forced_bits;
-  unsigned long long bar_base;   // barrier arrivals completed before this launch / CTA count
+  ECtl* ctl;
+  int smem_dyn;
+  u64* dbg;                // optional [n_stages][G][kDbgRec] %globaltimer stamps
 };
 
 // ---------------------------------------------------------------------------
 // PTX helpers
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint4 ld_nc(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
+__device__ __forceinline__ u64 ld_relaxed64(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
-__device__ __forceinline__ void l1_prefetch(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" :: "l"(p));
-}
-__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acq64(const unsigned long long* p) {
-  unsigned long long v;
+__device__ __forceinline__ u64 ld_acq64(const u64* p) {
+  u64 v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void red_rel64(unsigned long long* p, unsigned long long v) {
-  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+__device__ __forceinline__ long long ld_acq_s64(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_acq_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ void red_add64(long long* p, long long v) {
   asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long gclock() {
-  unsigned long long t;
+__device__ __forceinline__ void red_rel_add64(long long* p, long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_rel_addu64(u64* p, u64 v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+// tagged word {float v, u32 epoch}: one 64-bit store, single-copy atomic
+__device__ __forceinline__ void st_tag(u64* p, float v, unsigned e) {
+  __stcg(p, ((u64)e << 32) | __float_as_uint(v));
+}
+__device__ __forceinline__ uint4 ld_tag2(const u64* p) {   // two tagged words (16-byte aligned)
+  uint4 r;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ u64 gclock() {
+  u64 t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// Spin-wait watchdog: a wait beyond 4 s records (line, block, thread, a, b)
-// in mapped host memory (dpq_engine_diag) and traps (a launch error instead of
-// a hang). No call, so nothing is spilled around the polling loops.
-__device__ unsigned long long* g_diag = nullptr;
-__device__ volatile int* g_prog = nullptr;     // optional mapped progress words [grid][4] (debug)
-#ifdef DPQ_PROFILE_WARPS
-#define CSTAMP(st, i) do { if (st) (st)[96 + (i)] = clock64(); } while (0)
-#else
-#define CSTAMP(st, i) do { } while (0)
-#endif
-#ifdef DPQ_ENGINE_TRACE
-#define PROGRESS(slot, v) do { if (g_prog) g_prog[blockIdx.x * 4 + (slot)] = (v); } while (0)
-#define WSTATE(v) do { if (lane == 0) sm.wstate[warp] = (v); } while (0)
-#else
-#define PROGRESS(slot, v) do { } while (0)
-#define WSTATE(v) do { } while (0)
-#endif
+// Spin-wait watchdog: a wait beyond its limit records (line, block, thread, a,
+// b) in mapped host memory (dpq_engine_diag) and traps: a launch error, not a
+// hang. No call, so nothing is spilled around the polling loops.
+__device__ u64* g_diag = nullptr;
 #define hang(what, a, b)                                                                   \
   do {                                                                                     \
     if (g_diag) {                                                                          \
-      volatile unsigned long long* d_ = g_diag;                                            \
-      d_[1] = (unsigned long long)__LINE__; d_[2] = blockIdx.x; d_[3] = threadIdx.x;       \
-      d_[4] = (unsigned long long)(long long)(a); d_[5] = (unsigned long long)(long long)(b); \
+      volatile u64* d_ = g_diag;                                                           \
+      d_[1] = (u64)__LINE__; d_[2] = blockIdx.x; d_[3] = threadIdx.x;                      \
+      d_[4] = (u64)(long long)(a); d_[5] = (u64)(long long)(b);                            \
       __threadfence_system(); d_[0] = 1ull; __threadfence_system();                        \
     }                                                                                      \
     __trap();                                                                              \
   } while (0)
-// Poll cheaply; read the (slow) global timer only every 4096 polls.
 #define SPIN_UNTIL_NS(cond, what, a, b, NS)                                                \
   do {                                                                                     \
     unsigned n_ = 0;                                                                       \
-    unsigned long long t0_ = 0;                                                            \
+    u64 t0_ = 0;                                                                           \
     while (!(cond)) {                                                                      \
-      if ((++n_ & 4095u) == 0) {                                                           \
-        const unsigned long long t_ = gclock();                                            \
+      if ((++n_ & 1023u) == 0) {                                                           \
+        const u64 t_ = gclock();                                                           \
         if (t0_ == 0) t0_ = t_;                                                            \
-        else if (t_ - t0_ > (NS)) hang(what, a, b);                                         \
+        else if (t_ - t0_ > (NS)) hang(what, a, b);                                        \
       }                                                                                    \
     }                                                                                      \
   } while (0)
 #define SPIN_UNTIL(cond, what, a, b) SPIN_UNTIL_NS(cond, what, a, b, 4000000000ull)
+
 template <typename T>
 __device__ __forceinline__ T wsum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ long long fx(double v, double scale) { return llrint(v * scale); }
+// fixed point with a range check (sticky error flag instead of a silent wrap)
+__device__ __forceinline__ long long fx(double v, double scale, unsigned* err) {
+  const double s = v * scale;
+  if (!(fabs(s) < 4.0e18)) { atomicOr(err, (unsigned)ERR_RANGE); return 0; }
+  return llrint(s);
+}
 // 1/sqrt(x) in double without library slow paths (MUFU seed + two Newton steps).
 __device__ __forceinline__ double rsqrt_d(double x) {
   double r = (double)rsqrtf((float)x);
@@ -273,36 +290,17 @@ __device__ __forceinline__ float plane_sum(const uint4 d0, const uint4 d1, const
   return (a0 + a1) + (a2 + a3);
 }
 
-// LUT of one 512-column window: row e, slot g = sum_{t: bit t of e} x[8g + t];
-// row 256 = 0 (target of the wrapped "e - 1" encoding for e = 0). Thread u <
-// 256 builds rows [64 q, 64 q + 64) of group g (u = 64 q + g) straight from
-// the input in global memory (lut_load issues the loads, lut_store writes
-// the rows once they arrived; no staging, no barrier in between).
-struct LutSrc { float4 a, b; };
-__device__ __forceinline__ LutSrc lut_load(const float* x, int cols, int w) {
-  LutSrc r;
-  r.a = r.b = make_float4(0.f, 0.f, 0.f, 0.f);
-  const int u = threadIdx.x;
-  if (u < 256) {
-    const int c0 = w * kWinCols + 8 * (u & 63);
-    if (c0 + 8 <= cols) {
-      r.a = __ldcg(reinterpret_cast<const float4*>(x + c0));
-      r.b = __ldcg(reinterpret_cast<const float4*>(x + c0 + 4));
-    } else {
-      float t[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) t[j] = c0 + j < cols ? __ldcg(x + c0 + j) : 0.f;
-      r.a = make_float4(t[0], t[1], t[2], t[3]);
-      r.b = make_float4(t[4], t[5], t[6], t[7]);
-    }
-  }
-  return r;
-}
-__device__ __forceinline__ void lut_store(float* lut, const LutSrc& x) {
+// LUT of one 512-column window from the staged window xw: row e, slot g =
+// sum_{t: bit t of e} x[8g + t]; row 256 = 0 (target of the wrapped "e - 1"
+// encoding for e = 0). Thread u < 256 builds rows [64 q, 64 q + 64) of group
+// g (u = 64 q + g).
+__device__ __forceinline__ void lut_build(float* lut, const float* xw) {
   const int u = threadIdx.x;
   if (u >= 256) return;
   const int g = u & 63, q = u >> 6;
-  const float xs[4] = {x.a.x, x.a.y, x.a.z, x.a.w};
+  const float4 xa = *reinterpret_cast<const float4*>(xw + 8 * g);
+  const float4 xb = *reinterpret_cast<const float4*>(xw + 8 * g + 4);
+  const float xs[4] = {xa.x, xa.y, xa.z, xa.w};
   float L[16];
   L[0] = 0.f;
 #pragma unroll
@@ -314,10 +312,10 @@ __device__ __forceinline__ void lut_store(float* lut, const LutSrc& x) {
   for (int mm = 0; mm < 4; ++mm) {
     const int m = 4 * q + mm;
     float H = 0.f;
-    if (m & 1) H += x.b.x;
-    if (m & 2) H += x.b.y;
-    if (m & 4) H += x.b.z;
-    if (m & 8) H += x.b.w;
+    if (m & 1) H += xb.x;
+    if (m & 2) H += xb.y;
+    if (m & 4) H += xb.z;
+    if (m & 8) H += xb.w;
 #pragma unroll
     for (int i = 0; i < 16; ++i) lut[(16 * m + i) * kGroups + g] = L[i] + H;
   }
@@ -327,22 +325,20 @@ __device__ __forceinline__ void lut_store(float* lut, const LutSrc& x) {
 // ---------------------------------------------------------------------------
 // Per-op work of one CTA.
 // A group is (32-row tile t, 512-column window w), linear index g = w * n_tiles
-// + t (window-major). Groups are split over the grid by their base planes
-// (known before the decision), CTA c owning [ga, gb) starting at the first
-// group at or after item c*N/G. The range is cut into runs of <= 8 tiles of
-// one layer inside one window. The TMA producer warp streams, per run and
-// plane, one bulk copy of the run's tiles into a 16 KB ring slot: base planes
-// [0, nb) of all runs (window ascending), then - once the decision is
-// published - extra planes [nb, fin) of the runs whose layer decided high
-// (window descending, so the LUT changes at most three times). Consumer task
-// (run, tile) goes to warp k % NW; S is accumulated per tile by Horner over
-// planes (S_{p+1} = 2 S_p + P_p), the base part parked in shared memory.
+// + t (window-major). Window w gets CTAs [ceil(w G / n_win), ceil((w+1) G /
+// n_win)) (host guarantees n_win <= G), its groups split among them evenly by
+// base planes (known before the decision). The range is cut into runs of <= 8
+// tiles of one layer. The TMA producer streams, per run and plane, one bulk
+// copy of the run's tiles into a 16 KB ring slot: base planes [0, nb) of all
+// runs, then - once the decision is taken - extra planes [nb, fin) of the runs
+// whose layer decided high (reverse run order). Consumer task (run, tile) goes
+// to warp k % NW; S is accumulated per tile by Horner over planes (S_{p+1} =
+// 2 S_p + P_p), the base part parked in shared memory.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kLut = 0x20000;   // the window LUT (absolute shared address)
-
 struct Work {
-  int nb[kMaxOpLayers], fin[kMaxOpLayers];
+  int nb[kMaxOpLayers];
   int ga, gb;
+  int w, cb, m;            // window, its first CTA, CTA count of the window
   int valid;
 };
 
@@ -359,37 +355,36 @@ struct RunList {
 };
 
 struct Smem {
-  Prog prog;               // program descriptor (kernel parameter copy)
-  ECtl ctl;                // control block of the current step (read at BEGIN)
-  Op op[2];                // consumer copies of the current / next op descriptors
-  Work work[2];            // consumer work of the current / next op
-  RunList runs;            // consumer run list of the current op
-  Op pop;                  // producer copy of the op it streams
-  Work pw;                 // producer work
-  RunList pruns;           // producer run list
-  short pfo[kMaxRuns];     // producer scratch (FIFO offsets / task table it does not need)
+  Prog prog;
+  ECtl ctl;                          // control block of the current step
+  Op op[2];                          // consumer copies of the current / next op descriptors
+  Work work[2];
+  RunList runs;                      // consumer run list of the current op
+  Op pop;                            // producer copy of the op it streams
+  Work pw;
+  RunList pruns;
+  short pfo[kMaxRuns];
   unsigned char ptask[kMaxTasks];
   unsigned long long full[kMaxSlots], empty[kMaxSlots];   // ring mbarriers
   volatile int seq[kMaxSlots];       // FIFO index armed in each slot (phase disambiguation)
-  unsigned slot_off[kMaxSlots];      // slot byte offset from the dynamic smem base
-  int n_slots;
-  volatile int dec_op;               // op counter whose decision is published
-  int runs_op;                       // op counter whose base runs / FIFO offsets are in runs, fo_bo, last
-  volatile int step_ready;           // step whose control block consumers have loaded
-  volatile int cons_op, cons_j;      // consumer progress (watchdog diagnostics)
-  unsigned long long* stamp;         // current stage's timestamps (profiling) or nullptr
-  volatile int wstate[NW];           // per consumer warp: item it waits for * 16 + state
-  int dec_fin[2][kMaxOpLayers];      // published final bits (op counter parity)
-  float scale, sx;         // op input scale (1/rms or 1) and sum of raw input
-  int last;                // base FIFO items of the current op (op stage) / last-arriver flag
-  int n_ext_items, t_ext;  // extra FIFO items / extra tasks of the current op (after the decision)
-  double red[32];
+  unsigned slot_off[kMaxSlots];
+  volatile int dec_op;               // op counter whose decision and extra tables are published
+  volatile int cons_done;            // ops the consumers have finished (tables of op n - 2 are free)
+  int runs_op;                       // op counter whose base runs are in runs / fo_bo / task_rb
+  volatile int step_ready;           // step whose control block the consumers have loaded
+  int dec_fin[2][kMaxOpLayers];      // final bits (op parity)
+  short fo_bo[kMaxRuns];
+  short fo_eo[2][kMaxRuns], fo_xt[2][kMaxRuns];
+  unsigned char task_rb[kMaxTasks];
+  unsigned char task_rx[2][kMaxTasks];
+  int n_ext_items[2], t_ext[2];
+  int last;                          // base items of the current op
+  int head_last;
   float head_v[NW];
   int head_i[NW];
-  float sbuf[kMaxTiles][32];         // base-pass S of tiles whose layer has extra planes
-  short fo_bo[kMaxRuns], fo_eo[kMaxRuns], fo_xt[kMaxRuns];
-  unsigned char task_rb[kMaxTasks], task_rx[kMaxTasks];   // run of each base / extra task (kMaxRuns <= 255)
-  int vtile[kMaxTiles];              // reduce: emit tile of the CTA's i-th unit (values in sbuf)
+  double red[32];
+  float sbuf[kMaxTiles][32];         // base-pass S of groups whose layer has extra planes
+  float xw[kWinCols];                // the op's input window
 };
 
 __device__ __forceinline__ int layer_of(const Op& O, int t) {
@@ -398,10 +393,8 @@ __device__ __forceinline__ int layer_of(const Op& O, int t) {
   return li;
 }
 
-// First group whose first base item is >= item i.
-__device__ __forceinline__ int group_at(const Op& O, const int* nb, int wsum, int i) {
-  const int w = i / wsum;
-  int r = i - w * wsum;
+// First group whose first base item is >= item i (window-local item index).
+__device__ __forceinline__ int group_at(const Op& O, const int* nb, int wsum_, int w, int r) {
   for (int li = 0; li < O.n_layers; ++li) {
     const int seg = O.L[li].n_tiles * nb[li];
     if (r < seg) return w * O.n_tiles + O.L[li].tile_off + (r + nb[li] - 1) / nb[li];
@@ -418,43 +411,29 @@ __device__ __forceinline__ int base_bit(const Layer& L, const ECtl& C) {
   return L.l;
 }
 
-// Work of CTA cta: lanes 0..1 of the calling warp compute ga / gb in parallel.
+// Work of CTA cta (one warp).
 __device__ __forceinline__ void build_work_warp(const Op& O, const ECtl& C, int cta, int G, Work& W) {
   const int lane = threadIdx.x & 31;
-  // base bits straight into the (shared-memory) work record: a dynamically
-  // indexed local array would live in local memory
   const int nbl = lane < O.n_layers ? base_bit(O.L[lane], C) : 0;
-  if (lane < O.n_layers) {
-    W.nb[lane] = nbl;
-    W.fin[lane] = nbl;
-  }
+  if (lane < O.n_layers) W.nb[lane] = nbl;
   const int wtot = wsum(lane < O.n_layers ? O.L[lane].n_tiles * nbl : 0);
   __syncwarp();
-  const int* nb = W.nb;
-  const unsigned N = (unsigned)wtot * (unsigned)O.n_win;   // host guarantees N * G < 2^32
+  const int w = (int)((unsigned)cta * (unsigned)O.n_win / (unsigned)G);
+  const int cb = (w * G + O.n_win - 1) / O.n_win, ce = ((w + 1) * G + O.n_win - 1) / O.n_win;
+  const int m = ce - cb;
   if (lane < 2) {
-    int item;
-    if (O.n_win <= G) {
-      // window-aligned: CTAs [ceil(w G / n_win), ceil((w + 1) G / n_win)) share
-      // window w (one LUT per CTA, no rebuild), its items split evenly
-      const int w = (int)((unsigned)cta * (unsigned)O.n_win / (unsigned)G);
-      const int cb = (w * G + O.n_win - 1) / O.n_win, ce = ((w + 1) * G + O.n_win - 1) / O.n_win;
-      const int m = ce - cb, idx = cta - cb + lane;
-      item = w * wtot + (int)((unsigned)idx * (unsigned)wtot / (unsigned)m);
-    } else {
-      item = (int)(N * (unsigned)(cta + lane) / (unsigned)G);
-    }
-    const int g = group_at(O, nb, wtot, item);
+    const int idx = cta - cb + lane;
+    const int item = (int)((unsigned)idx * (unsigned)wtot / (unsigned)m);
+    const int g = group_at(O, W.nb, wtot, w, item);
     if (lane == 0) W.ga = g;
     else W.gb = g;
   }
+  if (lane == 0) { W.w = w; W.cb = cb; W.m = m; }
+  __syncwarp();
 }
 
 // Warp-parallel run list + base FIFO offsets + task -> run table of work W
-// (the serial loops were a dependent chain of shared-memory round trips,
-// ~1-3 us per op). Segments = (window, layer) pieces of [ga, gb), one per
-// lane (<= 32: host sizing keeps CTA ranges within a few windows); runs of
-// <= kSlotTiles tiles per segment; returns the number of base items.
+// (one window; segments = layers, one per lane). Returns the base item count.
 __device__ int build_runs_warp(const Op& O, const Work& W, RunList& R, short* fo_bo, unsigned char* task_r) {
   const int lane = threadIdx.x & 31;
   const int nt = O.n_tiles;
@@ -463,21 +442,17 @@ __device__ int build_runs_warp(const Op& O, const Work& W, RunList& R, short* fo
     __syncwarp();
     return 0;
   }
-  const int wa = W.ga / nt, wb = (W.gb - 1) / nt;
-  const int S = (wb - wa + 1) * O.n_layers;
-  if (S > 32) __trap();                 // host sizing guarantees this cannot happen
-  int lo = 0, len = 0, nr = 0, items = 0, li = 0, w = wa;
-  if (lane < S) {
-    w = wa + lane / O.n_layers;
-    li = lane - (lane / O.n_layers) * O.n_layers;
+  const int w = W.w;
+  int lo = 0, len = 0, nr = 0, items = 0;
+  const int li = lane;
+  if (lane < O.n_layers) {
     const Layer& L = O.L[li];
-    lo = max(max(W.ga - w * nt, 0), L.tile_off);
-    const int hi = min(min(W.gb - w * nt, nt), L.tile_off + L.n_tiles);
+    lo = max(W.ga - w * nt, L.tile_off);
+    const int hi = min(W.gb - w * nt, L.tile_off + L.n_tiles);
     len = max(hi - lo, 0);
     nr = (len + kSlotTiles - 1) / kSlotTiles;
     items = nr * W.nb[li];
   }
-  // exclusive prefix sums over the segments (lane order = window-major, layer order)
   int rb = nr, ib = items;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -497,15 +472,13 @@ __device__ int build_runs_warp(const Op& O, const Work& W, RunList& R, short* fo
     r.k0 = (short)(w * nt + lo + q * kSlotTiles - W.ga);
     fo_bo[rb + q] = (short)(ib + q * W.nb[li]);
   }
-  // task kt = tile ga + kt -> its run
-  for (int k0 = 0; k0 < W.gb - W.ga; k0 += 32) {   // uniform trip count: the shuffles need every lane
+  for (int k0 = 0; k0 < W.gb - W.ga; k0 += 32) {
     const int kt = k0 + lane;
     const bool ok = kt < W.gb - W.ga;
-    const int g = W.ga + (ok ? kt : 0), ww = g / nt, t = g - ww * nt;
+    const int t = W.ga + (ok ? kt : 0) - w * nt;
     int l2 = 0;
     while (l2 + 1 < O.n_layers && t >= O.L[l2 + 1].tile_off) ++l2;
-    const int sg = (ww - wa) * O.n_layers + l2;
-    const int slo = __shfl_sync(0xffffffffu, lo, sg & 31), srb = __shfl_sync(0xffffffffu, rb, sg & 31);
+    const int slo = __shfl_sync(0xffffffffu, lo, l2), srb = __shfl_sync(0xffffffffu, rb, l2);
     if (ok) task_r[kt] = (unsigned char)(srb + (t - slo) / kSlotTiles);
   }
   if (lane == 0) R.n = n_runs;
@@ -516,16 +489,16 @@ __device__ int build_runs_warp(const Op& O, const Work& W, RunList& R, short* fo
 // Warp-parallel FIFO offsets of the extra planes [nb, fin) once the decision
 // is known: runs in reverse order (the producer's issue order), exclusive
 // prefix sums of items and tasks, and the extra task -> run table.
-__device__ void extra_fifo_warp(const Op& O, const Work& W, const RunList& R, int base_items, short* fo_eo,
+__device__ void extra_fifo_warp(const Work& W, const int* fin, const RunList& R, int base_items, short* fo_eo,
                                 short* fo_xt, unsigned char* task_rx, int& n_items, int& n_tasks) {
   const int lane = threadIdx.x & 31;
   int carry_i = base_items, carry_t = 0;
   for (int c0 = 0; c0 < R.n; c0 += 32) {
-    const int idx = c0 + lane;                  // position in the reversed order
+    const int idx = c0 + lane;
     const int r = R.n - 1 - idx;
     int ex = 0, nt = 0;
     if (idx < R.n) {
-      ex = W.fin[R.r[r].li] - W.nb[R.r[r].li];
+      ex = fin[R.r[r].li] - W.nb[R.r[r].li];
       nt = ex > 0 ? R.r[r].nt : 0;
     }
     int si = ex, st = nt;
@@ -559,19 +532,15 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
 __device__ __forceinline__ void mbar_arrive_n(unsigned long long* bar, unsigned n) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(n) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  const uint32_t a = smem_u32(bar);
-  unsigned ok = 0;
-  auto test = [&]() {
-    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                 : "=r"(ok) : "r"(a), "r"(parity) : "memory");
-    return ok != 0;
-  };
-  SPIN_UNTIL_NS(test(), "ring slot", (long long)a, (long long)parity, 1000000000ull);
+__device__ __forceinline__ bool mbar_test(uint32_t a, unsigned parity) {
+  unsigned ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+               : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+  return ok != 0;
 }
-// Bitplanes are streamed once per step (GBs >> L2): marked evict-first so they
-// do not push the small, re-read state (vectors, window slots, accumulators,
-// G^T, KV rows) out of L2.
+// Bitplanes are streamed once per step (GBs >> L2): evict-first so they do not
+// push the small, re-read state (vectors, partials, accumulators, G, KV rows)
+// out of L2.
 __device__ __forceinline__ unsigned long long l2_evict_first_policy() {
   unsigned long long pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -588,10 +557,10 @@ __device__ __forceinline__ float4 ld_keep(const float* p, unsigned long long pol
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(policy));
   return r;
 }
-__device__ __forceinline__ uint4 ld_stream(const uint4* p, unsigned long long policy) {
+__device__ __forceinline__ uint4 ld_nc16(const void* p) {
   uint4 r;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(policy));
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
@@ -601,211 +570,350 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 }
 
 // ---------------------------------------------------------------------------
-// Vector emission: statistics + estimator feeds of one 32-row tile (a warp;
-// lane = row). v = value (0 for padding rows).
+// Epochs, the stage counter and the step control
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned stage_epoch(const Prog& P, int step_no, int si) {
+  return (unsigned)step_no * (unsigned)P.n_stages + (unsigned)si + 1u;
+}
+// every CTA arrives once per stage after its last read of that stage's inputs
+__device__ __forceinline__ void stage_arrive(const Prog& P) {
+  CSYNC();
+  if (threadIdx.x == 0) red_rel_addu64(P.bar, 1ull);
+}
+// before writing the double-buffered state of stage E: all CTAs are done with E - 2
+__device__ __forceinline__ bool stage_done(const Prog& P, unsigned E) {
+  if (E <= 2) return true;
+  return ld_acq64(P.bar) >= (u64)(E - 2) * gridDim.x;
+}
 
-// Statistics of one 32-row tile of vector instance inst: sum v, sum v^2.
-__device__ __forceinline__ void emit_stats(const Prog& P, const ECtl& C, int inst, float v) {
+// ---------------------------------------------------------------------------
+// Estimator accumulators (fixed point, per step slot) and statistics
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ long long* acc_slot(const Prog& P, int slot) { return P.acc + (size_t)slot * P.acc_stride; }
+__device__ __forceinline__ long long* stat_words(const Prog& P, int cur, int inst) {
+  return P.vstat + ((size_t)cur * P.n_inst + inst) * 3 * kStatSpread;
+}
+
+// Feed rows of the op's input window (consumer prologue). Rows of all feeds
+// of the instance are numbered 0..feed_rows-1; CTA j of the window's m takes
+// rows j, j + m, ...; its i-th row goes to warp kFeedW0 + i % kFeedWarps.
+// Row r of feed F: partial G_F[w][r] . x[w] in fp32 lanes + double warp sum,
+// fixed point at 2^fb, added to the set's accumulator, then a release count.
+constexpr int kFeedW0 = 8, kFeedWarps = 6;      // warps 8..13 (warps 0..7 build the LUT)
+constexpr int kStatW = 14;                       // statistics warp
+
+struct FeedSel {      // the feed a row belongs to and where it accumulates
+  const Feed* F;
+  long long* acc;
+  int r;
+};
+
+__device__ __forceinline__ bool feed_active(const Feed& F, const ECtl& C) {
+  const bool dyn = C.mode == MODE_DYNAMIC;
+  if (F.kind == FEED_PREV) return dyn || C.prime;
+  if (F.kind == FEED_CURFB) return dyn && !C.has_prev;
+  return dyn;
+}
+__device__ __forceinline__ long long* feed_acc(const Prog& P, const ECtl& C, const Feed& F) {
+  const int slot = F.kind == FEED_PREV ? kCurSlots + (C.rot & (kPrevSlots - 1)) : (C.n_steps_done & (kCurSlots - 1));
+  return acc_slot(P, slot) + F.acc;
+}
+
+// Window partial of G row r (lanes: 16 columns each) against xw.
+__device__ __forceinline__ double feed_row_dot(const Feed& F, int w, int r, const float* xw) {
   const int lane = threadIdx.x & 31;
-  const double dv = (double)v;
-  const double s = wsum(dv), q = wsum(dv * dv);
-  if (lane == 0) {
-    long long* vs = P.vstat + ((size_t)(C.n_steps_done & 1) * P.n_inst + inst) * 2 * kAccSpread;
-    red_add64(vs, fx(s, kFxSum));
-    red_add64(vs + kAccSpread, fx(q, kFxSq));
+  const float* xl = xw + 16 * lane;
+  float s = 0.f;
+  const size_t base = ((size_t)w * F.k + r) * kWinCols + 16 * lane;
+  if (F.dtype == G_F16) {
+    const uint4* g = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(F.G) + base);
+    const uint4 a = ld_nc16(g), b = ld_nc16(g + 1);
+    const __half2* ha = reinterpret_cast<const __half2*>(&a);
+    const __half2* hb = reinterpret_cast<const __half2*>(&b);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 u = __half22float2(ha[i]), v = __half22float2(hb[i]);
+      s = fmaf(u.x, xl[2 * i], s);
+      s = fmaf(u.y, xl[2 * i + 1], s);
+      s = fmaf(v.x, xl[8 + 2 * i], s);
+      s = fmaf(v.y, xl[8 + 2 * i + 1], s);
+    }
+  } else if (F.dtype == G_F32) {
+    const uint4* g = reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(F.G) + base);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 a = ld_nc16(g + q);
+      s = fmaf(__uint_as_float(a.x), xl[4 * q], s);
+      s = fmaf(__uint_as_float(a.y), xl[4 * q + 1], s);
+      s = fmaf(__uint_as_float(a.z), xl[4 * q + 2], s);
+      s = fmaf(__uint_as_float(a.w), xl[4 * q + 3], s);
+    }
+  } else {   // e4m3 with a per-row scale
+    const uint4 a = ld_nc16(reinterpret_cast<const unsigned char*>(F.G) + base);
+    const unsigned wd[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        __nv_fp8_e4m3 e;
+        e.__x = (unsigned char)(wd[q] >> (8 * j));
+        s = fmaf((float)e, xl[4 * q + j], s);
+      }
+    s *= __ldg(F.gscale + r);
+  }
+  return wsum((double)s);
+}
+
+// The feed row list: row q of the instance -> its feed (linear scan; <= a few feeds).
+__device__ __forceinline__ const Feed* feed_of_row(const Prog& P, int inst, int q) {
+  const int f0 = P.feed_begin[inst], f1 = P.feed_begin[inst + 1];
+  const Feed* F = P.feeds + f0;
+  for (int f = f0; f < f1; ++f) {
+    const Feed* G = P.feeds + f;
+    if (G->k > 0 && q >= G->row0 && q < G->row0 + G->k) return G;
+  }
+  return F;
+}
+
+// Statistics + feeds of the op's input window (warps kFeedW0.. / kStatW), after
+// the LUT build started (xw complete).
+__device__ __forceinline__ void window_feeds(const Prog& P, const ECtl& C, const Op& O, const Work& W,
+                                             const float* xw) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cta = blockIdx.x;
+  const int j = cta - W.cb, m = W.m;
+  if (warp >= kFeedW0 && warp < kFeedW0 + kFeedWarps) {
+    // projection rows: this CTA's i-th row -> warp kFeedW0 + i % kFeedWarps
+    for (int i = warp - kFeedW0;; i += kFeedWarps) {
+      const int q = j + i * m;
+      if (q >= O.feed_rows) break;
+      const Feed* F = feed_of_row(P, O.inst, q);
+      if (!feed_active(*F, C)) continue;
+      const int r = q - F->row0;
+      const double v = feed_row_dot(*F, W.w, r, xw);
+      if (lane == 0) {
+        long long* a = feed_acc(P, C, *F);
+        red_add64(a + r, fx(v, F->fxscale, P.err));
+        red_rel_add64(a + F->k + 1, 1);          // count (release: the value above is visible first)
+      }
+    }
+  } else if (warp == kStatW && j == 0) {
+    // sum x, sum x^2 of the window: op statistics + the feeds' sum x^2 words
+    double s = 0.0, q = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const double v = (double)xw[16 * lane + i];
+      s += v;
+      q += v * v;
+    }
+    s = wsum(s);
+    q = wsum(q);
+    if (lane == 0) {
+      long long* st = stat_words(P, C.n_steps_done & (kCurSlots - 1), O.inst);
+      red_add64(st, fx(s, kFxSum, P.err));
+      red_add64(st + kStatSpread, fx(q, kFxSq, P.err));
+      red_rel_add64(st + 2 * kStatSpread, 1);
+    }
+    const long long qf = fx(q, kFxSq, P.err);
+    for (int f = P.feed_begin[O.inst] + lane; f < P.feed_begin[O.inst + 1]; f += 32) {
+      const Feed& F = P.feeds[f];
+      if (!feed_active(F, C)) continue;
+      long long* a = feed_acc(P, C, F);
+      red_add64(a + F.k, qf);
+      red_rel_add64(a + F.k + 1, 1);
+    }
   }
 }
 
-// Feed fi (an estimator reading the vector) with tile `tile`: G_tile^T v
-// partials and sum v^2 into its fixed-point accumulators (a warp, lane = row).
-
-__device__ __forceinline__ void emit_feed(const Prog& P, const ECtl& C, int fi, int tile, float v,
-                                          const uint4 (*pre)[8] = nullptr) {
-  const int lane = threadIdx.x & 31;
-  Feed F;
-  {
-    const int4* fp = reinterpret_cast<const int4*>(P.feeds + fi);
-    int4* fd = reinterpret_cast<int4*>(&F);
-#pragma unroll
-    for (int q = 0; q < (int)(sizeof(Feed) / 16); ++q) fd[q] = __ldg(fp + q);
-  }
-  const int cur = C.n_steps_done & 1;
-  const bool dyn = C.mode == MODE_DYNAMIC;
-  long long* acc;
-  if (F.kind == FEED_PREV) {
-    if (!(dyn || C.prime)) return;
-    acc = P.acc + (size_t)(2 + C.prev_w) * P.acc_stride + F.acc;
+// ---------------------------------------------------------------------------
+// Input window: the tagged vector's 512 values -> xw (threads < 128, 4 each),
+// waiting for the producing stage's epoch.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void load_window(const u64* in, int cols, int w, unsigned epoch, float* xw) {
+  const int t = threadIdx.x;
+  if (t >= 128) return;
+  const int c0 = w * kWinCols + 4 * t;
+  float v[4] = {0.f, 0.f, 0.f, 0.f};
+  if (c0 + 4 <= cols) {
+    uint4 a, b;
+    bool ok;
+    SPIN_UNTIL((a = ld_tag2(in + c0), b = ld_tag2(in + c0 + 2),
+                ok = a.y == epoch && a.w == epoch && b.y == epoch && b.w == epoch), "input window", c0, epoch);
+    v[0] = __uint_as_float(a.x); v[1] = __uint_as_float(a.z);
+    v[2] = __uint_as_float(b.x); v[3] = __uint_as_float(b.z);
   } else {
-    if (!dyn) return;
-    if (F.kind == FEED_CURFB && C.has_prev) return;
-    acc = P.acc + (size_t)cur * P.acc_stride + F.acc;
+    for (int j = 0; j < 4; ++j)
+      if (c0 + j < cols) {
+        u64 x;
+        SPIN_UNTIL((x = ld_relaxed64(in + c0 + j), (unsigned)(x >> 32) == epoch), "input window", c0 + j, epoch);
+        v[j] = __uint_as_float((unsigned)x);
+      }
   }
-  if (F.Gt) {
-    // block of tile: [sub][chunk][lane][16 B]; f16 chunk = 4 rows x half2,
-    // f32 chunk = 2 rows x float2; lane owns k pair (2 lane, 2 lane + 1) of sub.
-    const int nsub = F.kpad / 64;
-    const double sc = ldexp(1.0, F.fb);
-    const unsigned long long pol = l2_evict_first_policy();   // G^T (~150 MB/step at 8B) streams like the planes
-    for (int sub = 0; sub < nsub; ++sub) {
-      float g0 = 0.f, g1 = 0.f;
-      if (F.f16) {
-        const uint4* blk = F.Gt + ((size_t)tile * nsub + sub) * 256 + lane;
-        uint4 c[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) c[i] = pre ? (*pre)[i] : ld_stream(blk + 32 * i, pol);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const __half2* hh = reinterpret_cast<const __half2*>(&c[i]);
-#pragma unroll
-          for (int rr = 0; rr < 4; ++rr) {
-            const float xr = __shfl_sync(0xffffffffu, v, 4 * i + rr);
-            const float2 gg = __half22float2(hh[rr]);
-            g0 = fmaf(gg.x, xr, g0);
-            g1 = fmaf(gg.y, xr, g1);
-          }
-        }
-      } else {
-        const uint4* blk = F.Gt + ((size_t)tile * nsub + sub) * 512 + lane;
-#pragma unroll
-        for (int hb = 0; hb < 2; ++hb) {
-          uint4 c[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) c[i] = ld_stream(blk + 32 * (8 * hb + i), pol);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float* ff = reinterpret_cast<const float*>(&c[i]);
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-              const float xr = __shfl_sync(0xffffffffu, v, 2 * (8 * hb + i) + rr);
-              g0 = fmaf(ff[2 * rr], xr, g0);
-              g1 = fmaf(ff[2 * rr + 1], xr, g1);
-            }
-          }
+  *reinterpret_cast<float4*>(xw + 4 * t) = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// ---------------------------------------------------------------------------
+// Attention for the o op's window (runtime.py:351-362): the 512 / head_dim
+// heads whose outputs are columns of window w, computed by every CTA of the
+// window (identical code and data, so identical results). Unit = (head, sub)
+// takes positions sub, sub + nsub, ... with an online softmax in registers
+// (lane = 4 consecutive dims); units are merged per head in fixed order. The
+// window's first CTA appends k_t / v_t of the window's KV groups
+// (runtime.py:355-356); position t itself is taken from registers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float4 tag4(const u64* p, unsigned epoch) {
+  uint4 a, b;
+  bool ok;
+  SPIN_UNTIL((a = ld_tag2(p), b = ld_tag2(p + 2), ok = a.y == epoch && a.w == epoch && b.y == epoch && b.w == epoch),
+             "q|k|v", 0, epoch);
+  return make_float4(__uint_as_float(a.x), __uint_as_float(a.z), __uint_as_float(b.x), __uint_as_float(b.z));
+}
+// RoPE (half split, runtime.py:288-298) of dims [i0, i0 + 4) of a head vector.
+__device__ __forceinline__ float4 rope4(const u64* v, int i0, int hd, float4 c, float4 s, unsigned e) {
+  const int half = hd / 2;
+  const bool lo = i0 < half;
+  const float4 a = tag4(v + i0, e);
+  const float4 b = tag4(v + (lo ? i0 + half : i0 - half), e);
+  float4 r;
+  if (lo) {   // x_i c_i - x_{i+half} s_i
+    r.x = a.x * c.x - b.x * s.x; r.y = a.y * c.y - b.y * s.y;
+    r.z = a.z * c.z - b.z * s.z; r.w = a.w * c.w - b.w * s.w;
+  } else {    // x_{i-half} s_j + x_i c_j
+    r.x = b.x * s.x + a.x * c.x; r.y = b.y * s.y + a.y * c.y;
+    r.z = b.z * s.z + a.z * c.z; r.w = b.w * s.w + a.w * c.w;
+  }
+  return r;
+}
+__device__ __forceinline__ float dot4(float4 a, float4 b) { return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w; }
+
+__device__ __noinline__ void attn_window(const Prog& P, const ECtl& C, const Op& O, const Work& W, float* scratch,
+                                         float* xw, unsigned e_qkv) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int hd = P.hd, qh = P.H / P.KV, b = O.block;
+  const int t = C.pos;
+  const int h0 = W.w * kWinCols / hd;
+  const int nh = min(kWinCols / hd, P.H - h0);
+  const int nsub = max(1, NW / nh);
+  const int units = nh * nsub;
+  const float scale = 1.0f / sqrtf((float)hd);
+  const int i0 = 4 * lane;
+  const bool act = i0 < hd;
+  const int jj = i0 < hd / 2 ? i0 : i0 - hd / 2;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 c4 = act ? __ldg(reinterpret_cast<const float4*>(P.cosv + (size_t)t * (hd / 2) + jj)) : z4;
+  const float4 s4 = act ? __ldg(reinterpret_cast<const float4*>(P.sinv + (size_t)t * (hd / 2) + jj)) : z4;
+  float* kc = P.kc[b];
+  float* vc = P.vc[b];
+  const unsigned long long kvpol = l2_evict_last_policy();   // the KV cache is re-read every step
+  const int ps = hd + 4;
+  bool wrote = false;
+  for (int u = warp; u < units; u += NW) {
+    const int hh = u % nh, sub = u / nh;
+    const int h = h0 + hh, g = h / qh;
+    const float4 q4 = act ? rope4(O.in + (size_t)h * hd, i0, hd, c4, s4, e_qkv) : z4;
+    float4 kt = z4, vt = z4;
+    const bool own_t = (t % nsub) == sub;
+    if (own_t && act) {
+      kt = rope4(O.in + P.d + (size_t)g * hd, i0, hd, c4, s4, e_qkv);      // RoPE'd k of this step
+      vt = tag4(O.in + P.d + P.dkv + (size_t)g * hd + i0, e_qkv);
+      if (W.cb == (int)blockIdx.x && h % qh == 0) {                        // KV append (runtime.py:355-356)
+        *reinterpret_cast<float4*>(kc + (size_t)t * P.dkv + g * hd + i0) = kt;
+        *reinterpret_cast<float4*>(vc + (size_t)t * P.dkv + g * hd + i0) = vt;
+        wrote = true;
+      }
+    }
+    float m = -CUDART_INF_F, l = 0.f;
+    float4 o = z4;
+    // cached positions s < t, 2-deep register pipeline
+    float4 k0 = z4, v0 = z4, k1 = z4, v1 = z4;
+    int s = sub;
+    const size_t goff = (size_t)g * hd + i0;
+    if (act && s < t) { k0 = ld_keep(kc + (size_t)s * P.dkv + goff, kvpol); v0 = ld_keep(vc + (size_t)s * P.dkv + goff, kvpol); }
+    if (act && s + nsub < t) {
+      k1 = ld_keep(kc + (size_t)(s + nsub) * P.dkv + goff, kvpol);
+      v1 = ld_keep(vc + (size_t)(s + nsub) * P.dkv + goff, kvpol);
+    }
+#define ATTN_UPDATE(K_, V_)                                                          \
+    {                                                                                \
+      const float a = wsum(dot4(q4, K_)) * scale;              /* runtime.py:358 */  \
+      const float mn = fmaxf(m, a);                                                  \
+      const float corr = expf(m - mn), p = expf(a - mn);       /* runtime.py:359-361 */ \
+      l = l * corr + p;                                                              \
+      o.x = o.x * corr + p * V_.x; o.y = o.y * corr + p * V_.y;                      \
+      o.z = o.z * corr + p * V_.z; o.w = o.w * corr + p * V_.w;                      \
+      m = mn;                                                                        \
+    }
+    for (; s < t; s += 2 * nsub) {
+      ATTN_UPDATE(k0, v0)
+      if (act && s + 2 * nsub < t) {
+        k0 = ld_keep(kc + (size_t)(s + 2 * nsub) * P.dkv + goff, kvpol);
+        v0 = ld_keep(vc + (size_t)(s + 2 * nsub) * P.dkv + goff, kvpol);
+      }
+      if (s + nsub < t) {
+        ATTN_UPDATE(k1, v1)
+        if (act && s + 3 * nsub < t) {
+          k1 = ld_keep(kc + (size_t)(s + 3 * nsub) * P.dkv + goff, kvpol);
+          v1 = ld_keep(vc + (size_t)(s + 3 * nsub) * P.dkv + goff, kvpol);
         }
       }
-      const int k0 = sub * 64 + 2 * lane;
-      if (k0 < F.k) red_add64(acc + (size_t)k0 * kAccSpread, fx((double)g0, sc));
-      if (k0 + 1 < F.k) red_add64(acc + (size_t)(k0 + 1) * kAccSpread, fx((double)g1, sc));
     }
+    if (own_t) ATTN_UPDATE(kt, vt)
+#undef ATTN_UPDATE
+    float* pr = scratch + u * ps;
+    if (act) *reinterpret_cast<float4*>(pr + i0) = o;
+    if (lane == 0) { pr[hd] = m; pr[hd + 1] = l; }
   }
-  const double dv = (double)v;
-  const double q = wsum(dv * dv);
-  if (lane == 0) red_add64(acc + (size_t)F.k * kAccSpread, fx(q, kFxSq));
-}
-
-// Statistics + every feed of one tile (one warp).
-__device__ __forceinline__ void emit_tile(const Prog& P, const ECtl& C, int inst, int tile, float v) {
-  emit_stats(P, C, inst, v);
-  for (int fi = P.feed_begin[inst]; fi < P.feed_begin[inst + 1]; ++fi) emit_feed(P, C, fi, tile, v);
-}
-
-// ---------------------------------------------------------------------------
-// Grid barrier (monotonic 64-bit arrival counter)
-// ---------------------------------------------------------------------------
-// Grid barrier: monotonic arrival counter bar[0] (G arrivals per stage);
-// waiters poll it relaxed and fence after (cheapest variant measured by
-// tools/ubench_barrier.cu on B200: ~1.3 us for 148 CTAs).
-__device__ __forceinline__ void bar_arrive(const Prog& P, unsigned long long epoch, int G) {
+  if (wrote) __threadfence();        // the appended rows are read by other CTAs in later steps
   CSYNC();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" :: "l"(P.bar) : "memory");
-  }
-}
-__shared__ unsigned long long s_bar_seen;     // last barrier epoch seen released (zeroed at kernel start)
-__device__ __forceinline__ void bar_wait(const Prog& P, unsigned long long epoch) {
-  // lane 0 of warps 0..kPollers-1 poll, staggered by a fraction of the L2
-  // round trip; the first to see the release publishes it in shared memory
-  constexpr int kPollers = 4;
-  volatile unsigned long long& s_seen = s_bar_seen;
-  const int warp = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0 && warp < kPollers) {
-    const unsigned long long target = epoch * (unsigned long long)gridDim.x;
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(P.bar) : "memory");
-    if (v < target && s_seen < epoch) {
-      if (warp) __nanosleep(120u * (unsigned)warp);
-      auto poll = [&]() {
-        if (s_seen >= epoch) return true;
-        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(P.bar) : "memory");
-        return v >= target;
-      };
-      SPIN_UNTIL_NS(poll(), "grid barrier", 0, (long long)epoch, 3000000000ull);
+  // merge the nsub units of each head in fixed order -> xw
+  for (int q = tid; q < kWinCols; q += NT) {
+    const int hh = q / hd, i = q - hh * hd;
+    float r = 0.f;
+    if (hh < nh) {
+      float M = -CUDART_INF_F;
+      for (int sb = 0; sb < nsub; ++sb) M = fmaxf(M, scratch[(sb * nh + hh) * ps + hd]);
+      float L = 0.f, acc = 0.f;
+      for (int sb = 0; sb < nsub; ++sb) {
+        const float* pr = scratch + (sb * nh + hh) * ps;
+        const float mw = pr[hd];
+        const float e = mw == -CUDART_INF_F ? 0.f : expf(mw - M);
+        L += e * pr[hd + 1];
+        acc += e * pr[i];
+      }
+      r = acc / L;                                             // runtime.py:362
     }
-    if (v >= target && s_seen < epoch) s_seen = epoch;
-    __threadfence();
-  }
-  CSYNC();
-}
-
-__device__ __forceinline__ void read_ctl(const Prog& P, ECtl& C) {
-  const int* src = reinterpret_cast<const int*>(P.ctl);
-  int* dst = reinterpret_cast<int*>(&C);
-  CSYNC();
-  if (threadIdx.x < (int)(sizeof(ECtl) / 4)) dst[threadIdx.x] = __ldcg(src + threadIdx.x);
-  CSYNC();
-}
-
-// ---------------------------------------------------------------------------
-// Op stage
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void load4(uint4* dst, const uint4* a) {
-  dst[0] = ld_nc(a);
-  dst[1] = ld_nc(a + 32);
-  dst[2] = ld_nc(a + 64);
-  dst[3] = ld_nc(a + 96);
-}
-
-
-// L2 prefetch of the G^T blocks this CTA's reduce units will feed (one 4 KB
-// block per (unit, feed) for f16, k <= 64), issued in the prologue so the
-// feed loads at the end of the stage hit L2.
-__device__ __forceinline__ void prefetch_own_feeds(const Prog& P, const ECtl& C, const Op& O, int cta, int G) {
-  if (O.out_inst < 0 || (C.mode != MODE_DYNAMIC && !C.prime)) return;
-  const int lane = threadIdx.x & 31;
-  const int f0 = P.feed_begin[O.out_inst], nf = P.feed_begin[O.out_inst + 1] - f0;
-  const int n_units = O.pair ? O.L[0].n_tiles : O.n_tiles;
-  const int mine = n_units > cta ? (n_units - cta + G - 1) / G : 0;
-  for (int q = lane; q < mine * nf; q += 32) {
-    const int i = q / nf, u = cta + i * G;
-    const Feed* F = P.feeds + f0 + (q - i * nf);
-    if (!F->Gt) continue;
-    const int li = layer_of(O, u);
-    const int et = O.pair ? u : (O.L[li].out_off >> 5) + (u - O.L[li].tile_off);
-    const int blk = (F->kpad / 64) * (F->f16 ? 4096 : 8192);
-    l2_prefetch(reinterpret_cast<const char*>(F->Gt) + (size_t)et * blk, (unsigned)blk);
+    xw[q] = r;
   }
 }
 
 // ---------------------------------------------------------------------------
 // Tile reduction + epilogue (one warp, lane = row of the tile)
 // ---------------------------------------------------------------------------
-// S of op tile t: sum of the window slots in fixed window order, each slot
-// awaited until it carries this op's epoch (no fence / counter needed: the
-// 64-bit slot store is single-copy atomic).
-__device__ __forceinline__ float tile_S(const Prog& P, const Op& O, int t, unsigned epoch) {
+// S of op tile t: sum of the window partials in fixed window order, each
+// awaited until it carries this stage's epoch.
+__device__ __forceinline__ float tile_S(const u64* slot, const Op& O, int t, unsigned epoch) {
   const int lane = threadIdx.x & 31;
-  const unsigned long long* base = P.slot + (size_t)t * 32 + lane;
+  const int rows = O.n_tiles * 32;
+  const u64* base = slot + (size_t)t * 32 + lane;
   float acc = 0.f;
   for (int w0 = 0; w0 < O.n_win; w0 += 8) {
     const int nw = min(8, O.n_win - w0);
-    unsigned long long v[8];
+    u64 v[8];
     bool ok;
     unsigned n_ = 0;
-    unsigned long long t0 = 0;
+    u64 t0 = 0;
     do {
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (j < nw) v[j] = __ldcg(base + (size_t)(w0 + j) * P.slot_stride);
+        if (j < nw) v[j] = ld_relaxed64(base + (size_t)(w0 + j) * rows);
       ok = true;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (j < nw) ok &= (unsigned)(v[j] >> 32) == epoch;
       if ((++n_ & 1023u) == 0) {
-        const unsigned long long t_ = gclock();
+        const u64 t_ = gclock();
         if (t0 == 0) t0 = t_;
-        else if (t_ - t0 > 4000000000ull) hang("window slots", t, 0);
+        else if (t_ - t0 > 4000000000ull) hang("window partials", t, epoch);
       }
     } while (!__all_sync(0xffffffffu, ok));
 #pragma unroll
@@ -815,368 +923,75 @@ __device__ __forceinline__ float tile_S(const Prog& P, const Op& O, int t, unsig
   return acc;
 }
 
-// y of op tile t (layer li) at the final plane count; valid = row exists.
-__device__ __forceinline__ float tile_y(const Prog& P, const Op& O, const Work& W, const Smem& sm, int t,
+struct Epi { float scale, sx; };
+
+// op input statistics (sum x, sum x^2) once every window has added them
+__device__ __forceinline__ Epi op_epi(const Prog& P, const ECtl& C, const Op& O) {
+  const long long* st = stat_words(P, C.n_steps_done & (kCurSlots - 1), O.inst);
+  SPIN_UNTIL(ld_acq_s64(st + 2 * kStatSpread) >= O.n_win, "statistics", O.inst, 0);
+  const double s = (double)__ldcg(st) * (1.0 / kFxSum);
+  const double q = (double)__ldcg(st + kStatSpread) * (1.0 / kFxSq);
+  Epi e;
+  e.sx = (float)s;
+  e.scale = O.rms ? (float)rsqrt_d(q / (double)O.cols + (double)P.eps) : 1.f;
+  return e;
+}
+
+__device__ __forceinline__ float tile_y(const u64* slot, const Op& O, const int* fin, const Epi& E, int t,
                                         unsigned epoch, int& li, int& r, bool& valid) {
   const int lane = threadIdx.x & 31;
   li = layer_of(O, t);
   const Layer& L = O.L[li];
-  const int fin = W.fin[li];
-  const float S = tile_S(P, O, t, epoch);
+  const float S = tile_S(slot, O, t, epoch);
   r = (t - L.tile_off) * 32 + lane;
   valid = r < L.rows;
   if (!valid) return 0.f;
   const float lo = __ldg(L.lo + r), span = __ldg(L.span + r);
-  return sm.scale * (lo * sm.sx + ldexpf(span, -fin) * (S + 0.5f * sm.sx));
-}
-
-// Reduce unit u (tile, or up|gate tile pair) of op O: window sum, affine
-// epilogue, residual add / SiLU (runtime.py:364-370), output store. Returns the
-// value the output instance is fed with (0 for padding rows) and its tile.
-__device__ __forceinline__ float reduce_unit(const Prog& P, const Op& O, const Work& W, const Smem& sm, int u,
-                                          unsigned epoch, int& etile) {
-  const int lane = threadIdx.x & 31;
-  // independent operands first (they do not wait for the window slots)
-  {
-    const int t = u, li = layer_of(O, t);
-    const Layer& L = O.L[li];
-    const int r = (t - L.tile_off) * 32 + lane;
-    if (r < L.rows) { l1_prefetch(L.lo + r); l1_prefetch(L.span + r); }
-    if (O.pair) {
-      const int t2 = u + O.L[0].n_tiles, li2 = layer_of(O, t2);
-      const Layer& L2 = O.L[li2];
-      const int r2 = (t2 - L2.tile_off) * 32 + lane;
-      if (r2 < L2.rows) { l1_prefetch(L2.lo + r2); l1_prefetch(L2.span + r2); }
-    } else if (O.add && r < L.rows) {
-      l1_prefetch(O.out + L.out_off + r);
-    }
-  }
-  unsigned long long* stp = (threadIdx.x == 0 && u == blockIdx.x) ? sm.stamp : nullptr;
-  if (stp) stp[2] = gclock();
-  CSTAMP(stp, 11);
-  float v = 0.f;
-  if (O.pair) {
-    const int half = O.L[0].n_tiles;
-    int li, r, li2, r2;
-    bool ok, ok2;
-    const float up = tile_y(P, O, W, sm, u, epoch, li, r, ok);
-    const float gt = tile_y(P, O, W, sm, u + half, epoch, li2, r2, ok2);
-    v = ok ? up * (gt / (1.0f + expf(-gt))) : 0.f;                 // runtime.py:368
-    if (ok) O.out[r] = v;
-    etile = u;
-  } else {
-    int li, r;
-    bool ok;
-    const float y = tile_y(P, O, W, sm, u, epoch, li, r, ok);
-    const int o = O.L[li].out_off + r;
-    if (ok) {
-      v = O.add ? O.out[o] + y : y;                                 // runtime.py:364, 370
-      O.out[o] = v;
-    }
-    etile = (O.L[li].out_off >> 5) + (u - O.L[li].tile_off);
-  }
-  if (stp) stp[3] = gclock();
-  CSTAMP(stp, 12);
-  return v;
-}
-
-// ---------------------------------------------------------------------------
-// The op stage (consumer warps 0..NW-1)
-// ---------------------------------------------------------------------------
-// Reduction of the op's units: unit u belongs to CTA u mod G (spread over the
-// grid so every CTA has at most a few), its i-th unit to warp i mod NW. Phase
-// A: window sums + epilogue per unit (values parked in shared memory); phase
-// B: the estimator feeds of the output instance, one (unit, feed) task per
-// warp in parallel (independent fixed-point sums). Warp NW - 1 first prepares
-// the next op's descriptor and work.
-__device__ __forceinline__ void reduce_duty(const Prog& P, const ECtl& C, const Op& O, const Work& W, Smem& sm,
-                                          int cta, int G, unsigned epoch, Op* On, Work* Wn, const Op* On_global,
-                                          int op_no) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n_units = O.pair ? O.L[0].n_tiles : O.n_tiles;
-  const int mine = n_units > cta ? (n_units - cta + G - 1) / G : 0;     // units of this CTA
-  if (warp == NW - 1 && On && !Wn->valid) {
-    // (descriptor copied into *On during the prologue)
-    build_work_warp(*On, C, cta, G, *Wn);
-    __syncwarp();
-    // the next op's base runs, FIFO offsets and task table (this op's are dead
-    // after its items): off the next stage's pre-barrier path
-    const int nbi = build_runs_warp(*On, *Wn, sm.runs, sm.fo_bo, sm.task_rb);
-    if (lane == 0) {
-      Wn->valid = 1;
-      sm.last = nbi;
-      sm.runs_op = op_no + 1;
-    }
-  }
-  const int f0 = O.out_inst >= 0 ? P.feed_begin[O.out_inst] : 0;
-  const int nf = O.out_inst >= 0 ? P.feed_begin[O.out_inst + 1] - f0 : 0;
-  for (int i = warp; i < mine; i += NW) {
-    int et;
-    const float v = reduce_unit(P, O, W, sm, cta + i * G, epoch, et);
-    if (O.out_inst >= 0) {
-      emit_stats(P, C, O.out_inst, v);
-      sm.sbuf[i][lane] = v;              // parked base sums are dead after the extra pass
-      if (lane == 0) sm.vtile[i] = et;
-    }
-  }
-  if (nf == 0) return;
-  CSYNC();
-  for (int q = warp; q < mine * nf; q += NW) {
-    const int i = q / nf;
-    emit_feed(P, C, f0 + (q - i * nf), sm.vtile[i], sm.sbuf[i][lane]);
-  }
-  if (threadIdx.x == 0) CSTAMP(sm.stamp, 13);
-}
-
-// FIFO layout of an op (relative to its first FIFO index): base items run by
-// run, planes [0, nb); then extra items for runs in reverse order, planes
-// [nb, fin). Returns the total and fills per-run offsets (lane-parallel).
-// Returns the number of ring items the op consumed (FIFO advance).
-__device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, Work& W, Op* On, Work* Wn,
-                                     const Op* On_global, Smem& sm, int cta, int G,
-                                     unsigned long long wait_target, bool do_wait, unsigned long long* stamp,
-                                     int op_no, int j_op) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned epoch = (unsigned)(wait_target + 1);     // this stage's epoch: tags the window slots
-  const int cur = C.n_steps_done & 1;
-  // ---- base work and run list (decision independent), before the barrier
-  // every thread reads W.valid before anyone can change it: the decision to
-  // join the CSYNC below must be uniform (a named-barrier count mismatch
-  // would silently misalign all later consumer barriers)
-  const bool built = W.valid != 0;
-  CSYNC();
-  if (!built) {
-    if (warp == 0) build_work_warp(O, C, cta, G, W);
-    CSYNC();
-  }
-  if (warp == 0 && sm.runs_op != op_no) {   // not prepared during the previous op's reduce phase
-    const int nbi = build_runs_warp(O, W, sm.runs, sm.fo_bo, sm.task_rb);
-    if (lane == 0) sm.last = nbi;
-  }
-  if (tid == 0) {
-    sm.stamp = stamp;
-    sm.cons_op = op_no;
-    sm.cons_j = j_op;
-  }
-  if (do_wait) bar_wait(P, wait_target);
-  if (stamp && tid == 0) stamp[0] = gclock();
-  if (tid == 0) CSTAMP(stamp, 0);
-
-  // ---- prologue. Critical path: the first window's input -> LUT -> base
-  // items. The selector inputs (accumulators, statistics) are loaded in the
-  // same round trip and finished after the LUT build (runtime.py:184-193).
-  const int w_first = sm.runs.n > 0 ? sm.runs.r[0].w : -1;
-  const LutSrc xsrc = lut_load(O.in, O.cols, max(w_first, 0));
-  // decision warps: accumulator loads in flight (k <= 128: 4 per lane)
-  // roles: warps 0..7 build the LUT (lut_store: threads < 256), warps 8.. take
-  // the decisions (one per layer) and the input statistics
-  constexpr int kDecW = 8, kStatW = kDecW + kMaxOpLayers;
-  static_assert(kStatW + 2 < NW - 1, "prologue roles need more consumer warps");
-  const int li_d = warp - kDecW;
-  const bool dec_warp = li_d >= 0 && li_d < O.n_layers;
-  const Layer& Ld = O.L[dec_warp ? li_d : 0];
-  const bool estimating = dec_warp && C.mode == MODE_DYNAMIC && Ld.sentinel == 0 && Ld.est != EST_NONE;
-  long long ga[4] = {0, 0, 0, 0}, gsq = 0;
-  if (estimating) {
-    const int slot = (Ld.src == SRC_PREV_STEP && C.has_prev) ? 2 + C.prev_r : cur;
-    const long long* acc = P.acc + (size_t)slot * P.acc_stride + Ld.acc;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (lane + 32 * q < Ld.k) ga[q] = __ldcg(acc + (size_t)(lane + 32 * q) * kAccSpread);
-    gsq = __ldcg(acc + (size_t)Ld.k * kAccSpread);
-  }
-  long long vs1 = 0, vs2 = 0;
-  if (warp == kStatW + 1) prefetch_own_feeds(P, C, O, cta, G);
-  if (warp == kStatW + 2 && On && !Wn->valid) {
-    // the next op's descriptor -> shared memory now (its work and runs are
-    // built during this op's reduce phase, no global round trip there)
-    const int nw4 = (int)(sizeof(Op) / 16);
-    const int4* src = reinterpret_cast<const int4*>(On_global);
-    int4* dst = reinterpret_cast<int4*>(On);
-    for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
-  }
-  if (warp == kStatW && lane == 0) {
-    const long long* vs = P.vstat + ((size_t)cur * P.n_inst + O.in_inst) * 2 * kAccSpread;
-    vs1 = __ldcg(vs);
-    vs2 = __ldcg(vs + kAccSpread);
-  }
-  if (tid == 0) CSTAMP(stamp, 1);
-  float* lut = reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLut - smem_u32(&sm)));
-  int lut_w = -1;
-  if (w_first >= 0) {                 // LUT of the first window
-    lut_store(lut, xsrc);
-    lut_w = w_first;
-  }
-  if (tid == 0) CSTAMP(stamp, 2);
-  if (dec_warp) {
-    const int li = li_d;
-    int bit = W.nb[li];
-    double est = CUDART_NAN;
-    if (estimating) {
-      double q = 0.0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const double g = (double)ga[i] * Ld.fbscale;
-        q += g * g;
-      }
-      q = wsum(q);
-      const double sq = (double)gsq * (1.0 / kFxSq);
-      const double sc = O.rms ? rsqrt_d(sq / (double)O.cols + (double)P.eps) : 1.0;
-      if (Ld.est == EST_PROJECTION) est = q > 0.0 ? sc * q * rsqrt_d(q) : 0.0;
-      else est = Ld.slope * (sq > 0.0 ? sc * sq * rsqrt_d(sq) : 0.0) + Ld.intercept;
-      if (!C.force) bit = est > Ld.T ? Ld.h : Ld.l;                      // strict > (runtime.py:192)
-    }
-    if (lane == 0) {
-      CSTAMP(stamp, 4 + li);
-      W.fin[li] = bit;
-      sm.dec_fin[op_no & 1][li] = bit;
-      if (C.mode == MODE_DYNAMIC && cta == 0 && Ld.trace >= 0 && P.n_trace > 0 && C.trace_step < P.max_steps) {
-        const size_t o = (size_t)C.trace_step * P.n_trace + Ld.trace;
-        P.tr_bits[o] = (signed char)bit;
-        P.tr_est[o] = estimating ? (float)est : CUDART_NAN_F;
-      }
-    }
-  } else if (warp == kStatW && lane == 0) {
-    sm.sx = (float)((double)vs1 * (1.0 / kFxSum));
-    sm.scale = O.rms ? (float)rsqrt_d((double)vs2 * (1.0 / kFxSq) / (double)O.cols + (double)P.eps) : 1.f;
-    CSTAMP(stamp, 7);
-  }
-  CSYNC();                             // decisions and LUT visible
-  const RunList& R = sm.runs;
-  if (warp == NW - 1) {                 // last warp: fewest items (tasks go round-robin from warp 0)
-    if (lane == 0) {
-      __threadfence_block();
-      sm.dec_op = op_no + 1;          // the producer may now stream the extra planes
-    }
-    // FIFO offsets of the extra planes (base offsets were set before the barrier)
-    int ni, nt;
-    extra_fifo_warp(O, W, R, sm.last, sm.fo_eo, sm.fo_xt, sm.task_rx, ni, nt);
-    if (lane == 0) {
-      sm.n_ext_items = ni;
-      sm.t_ext = nt;
-    }
-  }
-  const int n_base = sm.last;
-  if (stamp && tid == 0) stamp[1] = gclock();
-  if (tid == 0) CSTAMP(stamp, 3);
-  if (tid == 0) PROGRESS(1, 1);
-  const int n_tasks_base = W.gb - W.ga;
-#ifdef DPQ_PROFILE_WARPS
-  unsigned long long w_first_t = 0, w_last_t = 0, w_seq = 0, w_mb = 0, w_task0 = 0;   // per-warp profiling (stamp != nullptr)
-  int w_planes = 0;
-#define WPROF(x) do { if (stamp) { x; } } while (0)
-#else
-#define WPROF(x) do { } while (0)
-#endif
-  // ---- stream: tasks (run, tile) in FIFO order, LUT rebuilt per window segment
-  const unsigned char* dyn0 = reinterpret_cast<const unsigned char*>(&sm);
-  for (int kind = 0; kind < 2; ++kind) {
-    const int n_tasks = kind ? sm.t_ext : n_tasks_base;
-    int k = 0;                          // task index at the segment start
-    int rr = kind ? R.n - 1 : 0;        // run index at the segment start
-    while (k < n_tasks) {
-      // segment: consecutive runs (task order) of one window
-      while (kind && W.fin[R.r[rr].li] == W.nb[R.r[rr].li]) --rr;
-      const int w = R.r[rr].w;
-      int k_end = k, re = rr;
-      while (kind ? re >= 0 : re < R.n) {
-        const Run& q = R.r[re];
-        if (q.w != w) break;
-        if (!kind || W.fin[q.li] > W.nb[q.li]) k_end += q.nt;
-        re += kind ? -1 : 1;
-      }
-      if (w != lut_w) {
-        const LutSrc xs2 = lut_load(O.in, O.cols, w);
-        CSYNC();                          // previous LUT users done
-        lut_store(lut, xs2);
-        CSYNC();
-        lut_w = w;
-      }
-      const uint32_t lanereg = kLut | ((uint32_t)lane * 4u);
-      for (int kt = k + warp; kt < k_end; kt += NW) {
-        WPROF(if (!w_task0) w_task0 = clock64());
-        // task kt -> run and tile (tables built with the FIFO offsets)
-        const int r = kind ? sm.task_rx[kt] : sm.task_rb[kt];
-        const Run& q = R.r[r];
-        const int i = kt - (kind ? sm.fo_xt[r] : q.k0);
-        const int nb = W.nb[q.li], fin = W.fin[q.li];
-        const int p0 = kind ? nb : 0, p1 = kind ? fin : nb;
-        const int jr = sm.cons_j + (kind ? sm.fo_eo[r] : sm.fo_bo[r]);   // FIFO base from shared memory (no spill reload)
-        const int pk = q.k0 + i;                                   // task (group) index in [ga, gb)
-        float S = 0.f;
-        if (kind) S = pk < kMaxTiles ? sm.sbuf[pk][lane]
-                                     : __ldcg(P.park + ((size_t)cta * (kMaxTasks - kMaxTiles) + pk - kMaxTiles) * 32 + lane);
-        for (int p = p0; p < p1; ++p) {
-          const int j = jr + (p - p0);
-          const int slot = j & (kMaxSlots - 1);
-          WSTATE(j * 16 + 1);
-#ifdef DPQ_PROFILE_WARPS
-          const unsigned long long tw0 = stamp ? clock64() : 0;
-#endif
-          if (lane == 0) SPIN_UNTIL_NS(sm.seq[slot] == j, "ring sequence", j, sm.seq[slot], 1000000000ull);
-          __syncwarp();
-          WSTATE(j * 16 + 2);
-#ifdef DPQ_PROFILE_WARPS
-          const unsigned long long tw1 = stamp ? clock64() : 0;
-#endif
-          mbar_wait(&sm.full[slot], (unsigned)((j / kMaxSlots) & 1));
-          WSTATE(j * 16 + 3);
-#ifdef DPQ_PROFILE_WARPS
-          if (stamp) {
-            const unsigned long long tn = clock64();
-            w_seq += tw1 - tw0;
-            w_mb += tn - tw1;
-            if (!w_first_t) w_first_t = tn;
-            w_last_t = tn;
-            ++w_planes;
-          }
-#endif
-          const uint4* d = reinterpret_cast<const uint4*>(dyn0 + sm.slot_off[slot] + i * kTileBytes) + lane;
-          const uint4 d0 = d[0], d1 = d[32], d2 = d[64], d3 = d[96];
-          S = 2.f * S + plane_sum(d0, d1, d2, d3, lanereg);       // Horner over planes
-          __syncwarp();                                            // every lane has used its slot data
-          if (lane == 0) mbar_arrive_n(&sm.empty[slot], i == q.nt - 1 ? (unsigned)(kSlotTiles + 1 - q.nt) : 1u);
-          WSTATE(j * 16 + 4);
-        }
-        const int t = q.t0 + i;
-        if (!kind && fin > nb) {
-          if (pk < kMaxTiles) sm.sbuf[pk][lane] = S;                // park the base part
-          else __stcg(P.park + ((size_t)cta * (kMaxTasks - kMaxTiles) + pk - kMaxTiles) * 32 + lane, S);
-        } else {
-          __stcg(P.slot + (size_t)q.w * P.slot_stride + (size_t)t * 32 + lane,
-                 (unsigned long long)epoch << 32 | __float_as_uint(S));
-        }
-      }
-      k = k_end;
-      rr = re;
-    }
-#ifdef DPQ_PROFILE_WARPS
-    if (stamp && lane == 0) {
-      unsigned long long* ws = stamp + 8 + warp * 5;
-      ws[0] = w_task0; ws[1] = w_first_t; ws[2] = w_last_t; ws[3] = clock64(); ws[4] = (unsigned long long)w_planes | (min(w_seq, 0xffffffull) << 16) | (min(w_mb, 0xffffffull) << 40);
-    }
-#endif
-    // kind 0: parked base sums visible before the extra pass; kind 1: every warp
-    // done with the runs before the reduce phase rebuilds them for the next op
-    if (!kind || n_tasks > 0) CSYNC();
-  }
-  if (tid == 0) PROGRESS(1, 2);
-  if (stamp && tid == 0) stamp[5] = gclock();
-  if (tid == 0) CSTAMP(stamp, 10);
-  reduce_duty(P, C, O, W, sm, cta, G, epoch, On, Wn, On_global, op_no);
-  if (tid == 0) PROGRESS(1, 3);
-  if (stamp && tid == 0) stamp[6] = gclock();
-  if (tid == 0) CSTAMP(stamp, 15);
-  CSYNC();
-  if (tid == 0) { W.valid = 0; CSTAMP(stamp, 16); }
-  return n_base + sm.n_ext_items;
+  return E.scale * (lo * E.sx + ldexpf(span, -fin[li]) * (S + 0.5f * E.sx));
 }
 
 // ---------------------------------------------------------------------------
 // The TMA producer warp: streams every op's planes into the ring, running
-// ahead of the consumers across stage barriers (bounded by ring space, and by
-// each op's decision for its extra planes).
+// ahead of the consumers (bounded by ring space), and takes each op's
+// decisions (runtime.py:184-193) once the base planes are queued.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op& O, const Work& W, int* fin,
+                                          int cta) {
+  const int lane = threadIdx.x & 31;
+  const bool dyn = C.mode == MODE_DYNAMIC;
+  for (int li = 0; li < O.n_layers; ++li) {
+    const Layer& L = O.L[li];
+    int bit = W.nb[li];
+    double est = CUDART_NAN;
+    const bool estimating = dyn && L.sentinel == 0 && L.est != EST_NONE;
+    if (estimating) {
+      const int slot = (L.src == SRC_PREV_STEP && C.has_prev) ? kCurSlots + ((C.rot - 1) & (kPrevSlots - 1))
+                                                              : (C.n_steps_done & (kCurSlots - 1));
+      const long long* a = acc_slot(P, slot) + L.acc;
+      if (lane == 0) SPIN_UNTIL(ld_acq_s64(a + L.k + 1) >= L.cnt_expect, "estimator feeds", L.trace, L.cnt_expect);
+      __syncwarp();
+      double q = 0.0;
+      for (int i = lane; i < L.k; i += 32) {
+        const double g = (double)__ldcg(a + i) * L.fbscale;
+        q += g * g;
+      }
+      q = wsum(q);
+      const double sq = (double)__ldcg(a + L.k) * (1.0 / kFxSq);
+      const double sc = O.rms ? rsqrt_d(sq / (double)O.cols + (double)P.eps) : 1.0;
+      if (L.est == EST_PROJECTION) est = q > 0.0 ? sc * q * rsqrt_d(q) : 0.0;                 // estimator.py:56-57
+      else est = L.slope * (sq > 0.0 ? sc * sq * rsqrt_d(sq) : 0.0) + L.intercept;           // estimator.py:41-42
+      if (!C.force) bit = est > L.T ? L.h : L.l;                                              // strict > (runtime.py:192)
+    }
+    fin[li] = bit;
+    if (lane == 0 && dyn && cta == 0 && L.trace >= 0 && P.n_trace > 0 && C.trace_step < P.max_steps) {
+      const size_t o = (size_t)C.trace_step * P.n_trace + L.trace;
+      P.tr_bits[o] = (signed char)bit;
+      P.tr_est[o] = estimating ? (float)est : CUDART_NAN_F;
+    }
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G, int n_steps) {
   const int lane = threadIdx.x & 31;
   int j = 0, op_no = 0;
@@ -1187,20 +1002,11 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
     if (j >= kMaxSlots) {
       const uint32_t a = smem_u32(&sm.empty[slot]);
       const unsigned par = (unsigned)(((j / kMaxSlots) - 1) & 1);
-      unsigned ok = 0;
-      auto test = [&]() {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                     : "=r"(ok) : "r"(a), "r"(par) : "memory");
-        return ok != 0;
-      };
-      SPIN_UNTIL_NS(test(), "producer slot", ((long long)j << 32) | (unsigned)op_no,
-                    ((long long)sm.cons_op << 32) | (unsigned)sm.cons_j, 12000000000ull);
+      SPIN_UNTIL_NS(mbar_test(a, par), "producer slot", j, op_no, 12000000000ull);
       // the consumers' generic reads of the slot precede this async-proxy write
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     sm.seq[slot] = j;
-    PROGRESS(2, j);
-    PROGRESS(3, op_no);
     const Layer& L = O.L[r.li];
     const uint4* src = L.planes + p * L.pstride + ((long long)r.w * L.n_tiles + (r.t0 - L.tile_off)) * (kTileBytes / 16);
     mbar_expect_tx(&sm.full[slot], (unsigned)r.nt * kTileBytes);
@@ -1216,42 +1022,40 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
     for (int si = 0; si < P.n_stages; ++si) {
       const int2 st = P.stages[si];
       if (st.x != ST_OP) continue;
-      const int nw4 = (int)(sizeof(Op) / 16);
-      const int4* src = reinterpret_cast<const int4*>(P.ops + st.y);
-      int4* dst = reinterpret_cast<int4*>(&sm.pop);
-      for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
+      {
+        const int nw4 = (int)(sizeof(Op) / 16);
+        const int4* src = reinterpret_cast<const int4*>(P.ops + st.y);
+        int4* dst = reinterpret_cast<int4*>(&sm.pop);
+        for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
+      }
       __syncwarp();
-      build_work_warp(sm.pop, C, cta, G, sm.pw);
-      __syncwarp();
-      // (no L2 bulk prefetch of the next op's planes: measured slower -- it
-      // competes with the current stage's loads; the ring alone runs ahead)
-      build_runs_warp(sm.pop, sm.pw, sm.pruns, sm.pfo, sm.ptask);   // same runs as the consumers'
-      if (lane == 0) {
-        unsigned long long* pd = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec + 8 + 5 * NW : nullptr;
-        const int j0 = j;
-        if (pd) pd[0] = gclock();
-        const Op& O = sm.pop;
-        const RunList& R = sm.pruns;
+      const Op& O = sm.pop;
+      build_work_warp(O, C, cta, G, sm.pw);
+      const int nbi = build_runs_warp(O, sm.pw, sm.pruns, sm.pfo, sm.ptask);   // same runs as the consumers'
+      const RunList& R = sm.pruns;
+      if (lane == 0)
         for (int r = 0; r < R.n; ++r)
-          for (int p = 0; p < sm.pw.nb[R.r[r].li]; ++p) {
-            issue(O, R.r[r], p);
-            if (pd && j == j0 + 1) pd[1] = gclock();
-          }
-        if (pd) pd[2] = gclock();
-        bool may_extra = false;
-        if (C.mode == MODE_DYNAMIC && !C.force)
-          for (int li = 0; li < O.n_layers; ++li) may_extra |= O.L[li].sentinel == 0 && O.L[li].l < O.L[li].h;
-        if (may_extra && R.n > 0) {
-          SPIN_UNTIL_NS(sm.dec_op >= op_no + 1, "producer decision", op_no, 0, 12000000000ull);
-          __threadfence_block();
-          if (pd) pd[3] = gclock();
-          for (int r = R.n - 1; r >= 0; --r) {
-            const int li = R.r[r].li;
-            const int fin = sm.dec_fin[op_no & 1][li];
-            for (int p = sm.pw.nb[li]; p < fin; ++p) issue(O, R.r[r], p);
-          }
+          for (int p = 0; p < sm.pw.nb[R.r[r].li]; ++p) issue(O, R.r[r], p);
+      __syncwarp();
+      const int par = op_no & 1;
+      int fin[kMaxOpLayers];
+      decide_op(P, C, O, sm.pw, fin, cta);
+      // the decision tables are double-buffered by op parity: the consumers
+      // must be done with op op_no - 2 before they are overwritten
+      if (lane == 0) SPIN_UNTIL_NS(sm.cons_done >= op_no - 1, "consumer progress", op_no, sm.cons_done, 12000000000ull);
+      __syncwarp();
+      if (lane < O.n_layers) sm.dec_fin[par][lane] = lane == 0 ? fin[0] : lane == 1 ? fin[1] : fin[2];
+      int ni, nt;
+      extra_fifo_warp(sm.pw, fin, R, nbi, sm.fo_eo[par], sm.fo_xt[par], sm.task_rx[par], ni, nt);
+      if (lane == 0) {
+        sm.n_ext_items[par] = ni;
+        sm.t_ext[par] = nt;
+        __threadfence_block();
+        sm.dec_op = op_no + 1;          // the consumers may now run the extra planes
+        for (int r = R.n - 1; r >= 0; --r) {
+          const int li = R.r[r].li;
+          for (int p = sm.pw.nb[li]; p < fin[li]; ++p) issue(O, R.r[r], p);
         }
-        if (pd) { pd[4] = gclock(); pd[5] = (unsigned long long)(j - j0); }
       }
       __syncwarp();
       ++op_no;
@@ -1260,295 +1064,220 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
 }
 
 // ---------------------------------------------------------------------------
-// Attention stage (runtime.py:351-362): RoPE, KV append, causal softmax.
+// The op stage (consumer warps 0..NW-1)
 // ---------------------------------------------------------------------------
-// Unit = (query head h, chunk of <= kAttnChunkE positions). Warp w takes the
-// chunk's positions s0 + w, s0 + w + NW, ... with a per-warp online softmax
-// (lane = 4 consecutive dims, float4 loads; RoPE half-split recomputed per
-// warp from the q / k outputs, runtime.py:351-352); the NW partial (m, l, o)
-// are merged in shared memory in fixed warp order. Chunk partials of a head
-// are merged by the last unit of the head. The unit holding position t of the
-// first query head of each KV group appends k_t / v_t (runtime.py:355-356).
-constexpr int kAttnPerWarp = 16;                 // positions per warp and chunk
-constexpr int kAttnStaged = 3;                   // of which staged in shared memory (LUT region)
-constexpr int kAttnChunkE = NW * kAttnPerWarp;   // positions per unit
-
-// RoPE of 4 consecutive dims [i0, i0 + 4) of a head vector v (i0 % 4 == 0,
-// hd % 8 == 0), with the position's cos / sin of those dims preloaded.
-__device__ __forceinline__ float4 rope4(const float* v, int i0, int hd, float4 c, float4 s) {
-  const int half = hd / 2;
-  const bool lo = i0 < half;
-  const float4 a = __ldcg(reinterpret_cast<const float4*>(v + i0));
-  const float4 b = __ldcg(reinterpret_cast<const float4*>(v + (lo ? i0 + half : i0 - half)));
-  float4 r;
-  if (lo) {   // x_i c_i - x_{i+half} s_i
-    r.x = a.x * c.x - b.x * s.x; r.y = a.y * c.y - b.y * s.y;
-    r.z = a.z * c.z - b.z * s.z; r.w = a.w * c.w - b.w * s.w;
-  } else {    // x_{i-half} s_j + x_i c_j
-    r.x = b.x * s.x + a.x * c.x; r.y = b.y * s.y + a.y * c.y;
-    r.z = b.z * s.z + a.z * c.z; r.w = b.w * s.w + a.w * c.w;
-  }
-  return r;
-}
-
-__device__ __forceinline__ float dot4(float4 a, float4 b) { return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w; }
-
-// Statistics + feeds of head h's output tiles (values in vals[hd]): one
-// (tile, feed) task per warp.
-__device__ __forceinline__ void attn_emit_head(const Prog& P, const ECtl& C, int inst, int h, const float* vals) {
+// Reduction of the op's units: unit u belongs to CTA u mod G, its i-th unit to
+// warp i mod NW. Warp NW - 1 first prepares the next op's work and runs.
+__device__ __forceinline__ void reduce_duty(const Prog& P, const ECtl& C, const Op& O, Smem& sm, int cta, int G,
+                                            unsigned epoch, const int* fin, const u64* slot, Op* On, Work* Wn,
+                                            int op_no, unsigned e_res) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nt = (P.hd + 31) / 32;
-  const int f0 = P.feed_begin[inst], nf = P.feed_begin[inst + 1] - f0;
-  for (int q = warp; q < nt * (nf + 1); q += NW) {
-    const int tt = q / (nf + 1), f = q - tt * (nf + 1);
-    const int i = tt * 32 + lane;
-    const float v = i < P.hd ? vals[i] : 0.f;
-    const int tile = (h * P.hd) / 32 + tt;
-    if (f == nf) emit_stats(P, C, inst, v);
-    else emit_feed(P, C, f0 + f, tile, v);
+  const int n_units = O.pair ? O.L[0].n_tiles : O.n_tiles;
+  const int mine = n_units > cta ? (n_units - cta + G - 1) / G : 0;
+  if (warp == NW - 1 && On && !Wn->valid) {
+    build_work_warp(*On, C, cta, G, *Wn);
+    const int nbi = build_runs_warp(*On, *Wn, sm.runs, sm.fo_bo, sm.task_rb);
+    if (lane == 0) {
+      Wn->valid = 1;
+      sm.last = nbi;
+      sm.runs_op = op_no + 1;
+    }
   }
-}
-
-__device__ __forceinline__ void attn_stage(const Prog& P, const ECtl& C, int b, float* sh, int cta, int G, int* s_last,
-                                       unsigned long long wait_target, bool do_wait, unsigned long long* stamp) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int t = C.pos, n = t + 1;
-  const int hd = P.hd, qh = P.H / P.KV, nv = hd / 4;
-  const int nch = (n + kAttnChunkE - 1) / kAttnChunkE;
-  const int units = P.H * nch;
-  const float scale = 1.0f / sqrtf((float)hd);
-  const float* cs = P.cosv + (size_t)t * (hd / 2);
-  const float* sn = P.sinv + (size_t)t * (hd / 2);
-  float* kc = P.kc[b];
-  float* vc = P.vc[b];
-  const int inst = 4 * b + 1;
-  // shared memory (LUT region): K / V staging [NW][kAttnStaged][2][hd], the
-  // per-warp partials [NW][hd + 4] and the merged head output [hd]
-  float* kvs = sh;
-  const int ps = hd + 4;                   // part row stride (16-byte aligned)
-  float* part = sh + NW * kAttnStaged * 2 * hd;
-  float* outv = part + NW * ps;
-  const bool act = lane < nv;
-  const int i0 = 4 * lane;
-  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  const unsigned long long kvpol = l2_evict_last_policy();   // the KV cache is re-read every step: keep it in L2
-  // Rows of unit positions s0 + warp + NW j: j < kAttnStaged are copied
-  // asynchronously into shared memory (for the CTA's first unit before the
-  // barrier: cached positions do not depend on this step; a lane copies and
-  // later reads only its own 16 bytes), the rest stream through a 4-deep
-  // register pipeline.
-#define ATTN_STAGE_ROWS(u_)                                                              \
-  do {                                                                                   \
-    const int h_ = (u_) / nch, g_ = h_ / qh;                                             \
-    const int s0_ = ((u_) - h_ * nch) * kAttnChunkE, lim_ = min(t, s0_ + kAttnChunkE);   \
-    _Pragma("unroll") for (int j = 0; j < kAttnStaged; ++j) {                            \
-      const int s_ = s0_ + warp + NW * j;                                                \
-      if (act && s_ < lim_) {                                                            \
-        const size_t off_ = (size_t)s_ * P.dkv + g_ * hd + i0;                           \
-        float* d_ = kvs + ((warp * kAttnStaged + j) * 2) * hd + i0;                      \
-        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(smem_u32(d_)), "l"(kc + off_), "l"(kvpol) : "memory"); \
-        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(smem_u32(d_ + hd)), "l"(vc + off_), "l"(kvpol) : "memory"); \
-      }                                                                                  \
-    }                                                                                    \
-  } while (0)
-#define ATTN_ROW(s_, lim_, g_, K_, V_)                                             \
-  do {                                                                             \
-    if (act && (s_) < (lim_)) {                                                    \
-      const size_t off_ = (size_t)(s_) * P.dkv + (g_) * hd + i0;                   \
-      K_ = ld_keep(kc + off_, kvpol);                                             \
-      V_ = ld_keep(vc + off_, kvpol);                                             \
-    }                                                                              \
-  } while (0)
-  if (cta < units) ATTN_STAGE_ROWS(cta);
-  const int j0 = i0 < hd / 2 ? i0 : i0 - hd / 2;
-  const float4 c4 = act ? __ldg(reinterpret_cast<const float4*>(cs + j0)) : z4;
-  const float4 s4 = act ? __ldg(reinterpret_cast<const float4*>(sn + j0)) : z4;
-  if (do_wait) bar_wait(P, wait_target);
-  if (stamp && tid == 0) stamp[0] = gclock();
-  if (tid == 0) CSTAMP(stamp, 0);
-  for (int u = cta; u < units; u += G) {
-    const int h = u / nch, ch = u - h * nch;
-    const int g = h / qh;
-    unsigned long long* stp = (tid == 0 && u == cta) ? stamp : nullptr;
-    const int s0 = ch * kAttnChunkE, s1 = min(n, s0 + kAttnChunkE);
-    const int lim = min(t, s1);            // cached rows of the chunk: [s0, lim)
-    if (u != cta) {
-      CSYNC();                             // previous unit's readers of the staging done
-      ATTN_STAGE_ROWS(u);
-    }
-    // per-warp online softmax (lane = dims 4 lane .. 4 lane + 3)
-    float m = -CUDART_INF_F, l = 0.f;
-    float4 o = z4;
-    const float4 q4 = act ? rope4(P.qkv + h * hd, i0, hd, c4, s4) : o;
-    float4 kt = o, vt = o;
-    const bool own_t = act && s1 == n && (t - s0) % NW == warp;   // this warp holds the new position t
-    if (own_t) {
-      kt = rope4(P.qkv + P.d + g * hd, i0, hd, c4, s4);      // RoPE'd k of this step
-      vt = __ldcg(reinterpret_cast<const float4*>(P.qkv + P.d + P.dkv + g * hd + i0));
-    }
-    // register pipeline rows (j = kAttnStaged ..., 2 deep), in flight with q / k_t / v_t
-    const int sr = s0 + warp + NW * kAttnStaged;
-    float4 k0 = z4, v0 = z4, k1 = z4, v1 = z4;
-    ATTN_ROW(sr, lim, g, k0, v0);
-    ATTN_ROW(sr + NW, lim, g, k1, v1);
-    if (own_t && h % qh == 0) {          // runtime.py:355-356 (KV append)
-      *reinterpret_cast<float4*>(kc + (size_t)t * P.dkv + g * hd + i0) = kt;
-      *reinterpret_cast<float4*>(vc + (size_t)t * P.dkv + g * hd + i0) = vt;
-    }
-#define ATTN_UPDATE(s_, K_, V_)                                                    \
-    {                                                                              \
-      const float4 k4 = (s_) == t ? kt : K_, v4 = (s_) == t ? vt : V_;             \
-      const float a = wsum(dot4(q4, k4)) * scale;            /* runtime.py:358 */  \
-      const float mn = fmaxf(m, a);                                                \
-      const float corr = expf(m - mn), p = expf(a - mn);     /* runtime.py:359-361 */ \
-      l = l * corr + p;                                                            \
-      o.x = o.x * corr + p * v4.x; o.y = o.y * corr + p * v4.y;                    \
-      o.z = o.z * corr + p * v4.z; o.w = o.w * corr + p * v4.w;                    \
-      m = mn;                                                                      \
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-#pragma unroll
-    for (int j = 0; j < kAttnStaged; ++j) {
-      const int s = s0 + warp + NW * j;
-      if (s < s1) {
-        const float* r_ = kvs + ((warp * kAttnStaged + j) * 2) * hd + i0;
-        const float4 ks = act ? *reinterpret_cast<const float4*>(r_) : z4;
-        const float4 vs = act ? *reinterpret_cast<const float4*>(r_ + hd) : z4;
-        ATTN_UPDATE(s, ks, vs)
-      }
-    }
-#define ATTN_STEP(s_, K_, V_)                                                      \
-    if ((s_) < s1) ATTN_UPDATE(s_, K_, V_)                                         \
-    ATTN_ROW((s_) + 2 * NW, lim, g, K_, V_);   /* refill this register slot */
-    for (int s = sr; s < s1; s += 2 * NW) {
-      ATTN_STEP(s, k0, v0)
-      ATTN_STEP(s + NW, k1, v1)
-    }
-    CSTAMP(stp, 2);
-    CSYNC();                                 // previous unit's readers of part / outv done
-    if (act) *reinterpret_cast<float4*>(part + warp * ps + i0) = o;
-    // warp weights (fixed order): lane w of every warp computes the global max M
-    // and e_w = exp(m_w - M); L = sum_w e_w l_w
-    if (lane == 0) { part[warp * ps + hd] = m; part[warp * ps + hd + 1] = l; }
-    CSYNC();
-    CSTAMP(stp, 7);
-    {
-      const float mw = lane < NW ? part[lane * ps + hd] : -CUDART_INF_F;
-      const float lw = lane < NW ? part[lane * ps + hd + 1] : 0.f;
-      float M = mw;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-      const float e = mw == -CUDART_INF_F ? 0.f : expf(mw - M);      // warps without positions: 0
-      // fixed-order sum over lanes 0..NW-1 (the shuffle tree is the same in every warp)
-      const float L = wsum(e * lw);
-      const int di = tid < hd ? tid : 0;
-      float acc = 0.f;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) acc += __shfl_sync(0xffffffffu, e, w) * part[w * ps + di];
-      CSTAMP(stp, 8);
-      if (tid < hd) {
-        if (nch == 1) {
-          const float r = acc / L;            // runtime.py:362
-          P.attn[h * hd + tid] = r;
-          outv[tid] = r;
-        } else {
-          float* pp = P.attn_part + ((size_t)h * P.attn_max_chunks + ch) * (hd + 2);
-          pp[tid] = acc;
-          if (tid == 0) { pp[hd] = M; pp[hd + 1] = L; }
+  if (mine == 0) return;
+  const Epi E = op_epi(P, C, O);
+  for (int i = warp; i < mine; i += NW) {
+    const int u = cta + i * G;
+    if (O.pair) {
+      const int half = O.L[0].n_tiles;
+      int li, r, li2, r2;
+      bool ok, ok2;
+      const float up = tile_y(slot, O, fin, E, u, epoch, li, r, ok);
+      const float gt = tile_y(slot, O, fin, E, u + half, epoch, li2, r2, ok2);
+      if (ok) st_tag(O.out + r, up * (gt / (1.0f + expf(-gt))), epoch);        // runtime.py:368
+    } else {
+      int li, r;
+      bool ok;
+      const float y = tile_y(slot, O, fin, E, u, epoch, li, r, ok);
+      if (ok) {
+        const int o = O.L[li].out_off + r;
+        float v = y;
+        if (O.add) {                                                            // runtime.py:364, 370
+          u64 x;
+          SPIN_UNTIL((x = ld_relaxed64(O.res_in + o), (unsigned)(x >> 32) == e_res), "residual", o, e_res);
+          v = __uint_as_float((unsigned)x) + y;
         }
+        st_tag(O.out + o, v, epoch);
       }
     }
-    if (nch == 1) {
-      CSYNC();
-      CSTAMP(stp, 4);
-      if (P.attn_emit) attn_emit_head(P, C, inst, h, outv);
-      CSTAMP(stp, 5);
-      continue;
-    }
-    __threadfence();
-    CSYNC();
-    if (tid == 0) *s_last = atomicAdd(P.attn_cnt + h, 1u) == (unsigned)nch - 1;
-    CSYNC();
-    if (!*s_last) continue;
-    __threadfence();
-    const float* base = P.attn_part + (size_t)h * P.attn_max_chunks * (hd + 2);
-    if (tid < hd) {
-      float M = -CUDART_INF_F;
-#pragma unroll 1
-      for (int c = 0; c < nch; ++c) M = fmaxf(M, __ldcg(base + c * (hd + 2) + hd));
-      float Ls = 0.f, acc = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < nch; ++c) {
-        const float e = expf(__ldcg(base + c * (hd + 2) + hd) - M);
-        Ls += __ldcg(base + c * (hd + 2) + hd + 1) * e;
-        acc += __ldcg(base + c * (hd + 2) + tid) * e;
-      }
-      const float r = acc / Ls;
-      P.attn[h * hd + tid] = r;
-      outv[tid] = r;
-    }
-    if (tid == 0) P.attn_cnt[h] = 0u;
-    CSYNC();
-    CSTAMP(stp, 4);
-    if (P.attn_emit) attn_emit_head(P, C, inst, h, outv);
-    CSTAMP(stp, 5);
   }
-  if (tid == 0) CSTAMP(stamp, 6);
 }
 
-// EMIT: statistics + feeds of a whole vector (attention output when heads
-// are not 32-aligned).
-__device__ __forceinline__ void emit_stage(const Prog& P, const ECtl& C, const float* v, int n, int inst, int cta, int G) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n_t = (n + 31) / 32;
-  for (int tt = cta * NW + warp; tt < n_t; tt += G * NW) {
-    const int i = tt * 32 + lane;
-    emit_tile(P, C, inst, tt, i < n ? __ldcg(v + i) : 0.f);
+__device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, Work& W, Op* On, Work* Wn,
+                                        const Op* On_global, Smem& sm, int cta, int G, unsigned epoch,
+                                        unsigned step_base, u64* dbg, int op_no, int j_op) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int par = op_no & 1;
+  // ---- work and base runs (decision independent)
+  const bool built = W.valid != 0;
+  CSYNC();
+  if (!built) {
+    if (warp == 0) build_work_warp(O, C, cta, G, W);
+    CSYNC();
   }
+  if (warp == 0 && sm.runs_op != op_no) {
+    const int nbi = build_runs_warp(O, W, sm.runs, sm.fo_bo, sm.task_rb);
+    if (lane == 0) sm.last = nbi;
+  }
+  if (dbg && tid == 0) dbg[0] = gclock();
+  // the next op's descriptor -> shared memory (its work is built in the reduce phase)
+  if (warp == NW - 1 && On && !Wn->valid) {
+    const int nw4 = (int)(sizeof(Op) / 16);
+    const int4* src = reinterpret_cast<const int4*>(On_global);
+    int4* dst = reinterpret_cast<int4*>(On);
+    for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
+  }
+  // ---- input window -> xw (skew bound checked on the way: stage E - 2 done)
+  float* lut = reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLut - smem_u32(&sm)));
+  if (tid == 32) SPIN_UNTIL(stage_done(P, epoch), "stage counter", epoch, 0);
+  if (O.in_kind == IN_ATTN) {
+    attn_window(P, C, O, W, lut, sm.xw, step_base + (unsigned)O.in_stage + 1u);
+  } else {
+    load_window(O.in, O.cols, W.w, step_base + (unsigned)O.in_stage + 1u, sm.xw);
+  }
+  CSYNC();
+  if (dbg && tid == 0) dbg[1] = gclock();
+  // ---- LUT (warps 0..7) | estimator feeds and statistics (warps 8..14)
+  lut_build(lut, sm.xw);
+  window_feeds(P, C, O, W, sm.xw);
+  CSYNC();
+  if (dbg && tid == 0) dbg[2] = gclock();
+  // ---- stream: tasks (run, tile) in FIFO order
+  const RunList& R = sm.runs;
+  const unsigned char* dyn0 = reinterpret_cast<const unsigned char*>(&sm);
+  const uint32_t lanereg = kLut | ((uint32_t)lane * 4u);
+  const int n_base = sm.last;
+  u64* slot = P.slot + (size_t)(epoch & 1u) * P.slot_half + (size_t)W.w * O.n_tiles * 32;
+  for (int kind = 0; kind < 2; ++kind) {
+    if (kind) {
+      if (lane == 0) SPIN_UNTIL_NS(sm.dec_op >= op_no + 1, "decision", op_no, 0, 8000000000ull);
+      __syncwarp();
+      __threadfence_block();
+    }
+    const int n_tasks = kind ? sm.t_ext[par] : W.gb - W.ga;
+    for (int kt = warp; kt < n_tasks; kt += NW) {
+      const int r = kind ? sm.task_rx[par][kt] : sm.task_rb[kt];
+      const Run& q = R.r[r];
+      const int i = kt - (kind ? sm.fo_xt[par][r] : q.k0);
+      const int nb = W.nb[q.li];
+      const int fin = kind ? sm.dec_fin[par][q.li] : nb;
+      const int p0 = kind ? nb : 0, p1 = kind ? fin : nb;
+      const int jr = j_op + (kind ? sm.fo_eo[par][r] : sm.fo_bo[r]);
+      const int pk = q.k0 + i;                                   // group index in [ga, gb)
+      float S = 0.f;
+      if (kind) S = pk < kMaxTiles ? sm.sbuf[pk][lane]
+                                   : __ldcg(P.park + ((size_t)cta * (kMaxTasks - kMaxTiles) + pk - kMaxTiles) * 32 + lane);
+      for (int p = p0; p < p1; ++p) {
+        const int j = jr + (p - p0);
+        const int sl = j & (kMaxSlots - 1);
+        if (lane == 0) SPIN_UNTIL_NS(sm.seq[sl] == j, "ring sequence", j, sm.seq[sl], 2000000000ull);
+        __syncwarp();
+        const uint32_t fa = smem_u32(&sm.full[sl]);
+        const unsigned fpar = (unsigned)((j / kMaxSlots) & 1);
+        SPIN_UNTIL_NS(mbar_test(fa, fpar), "ring slot", j, fpar, 2000000000ull);
+        const uint4* d = reinterpret_cast<const uint4*>(dyn0 + sm.slot_off[sl] + i * kTileBytes) + lane;
+        const uint4 d0 = d[0], d1 = d[32], d2 = d[64], d3 = d[96];
+        __syncwarp();
+        if (lane == 0) mbar_arrive_n(&sm.empty[sl], i == q.nt - 1 ? (unsigned)(kSlotTiles + 1 - q.nt) : 1u);
+        S = 2.f * S + plane_sum(d0, d1, d2, d3, lanereg);       // Horner over planes
+      }
+      const int t = q.t0 + i;
+      // base pass of a layer that may still add planes: park; else publish
+      const bool may_extra = !kind && C.mode == MODE_DYNAMIC && !C.force && O.L[q.li].sentinel == 0 &&
+                             O.L[q.li].est != EST_NONE && O.L[q.li].h > nb;
+      if (may_extra) {
+        if (pk < kMaxTiles) sm.sbuf[pk][lane] = S;
+        else __stcg(P.park + ((size_t)cta * (kMaxTasks - kMaxTiles) + pk - kMaxTiles) * 32 + lane, S);
+      }
+      if (!may_extra || kind) st_tag(slot + (size_t)t * 32 + lane, S, epoch);
+    }
+    if (!kind) {
+      CSYNC();          // parked base sums visible
+      // groups that parked but whose layer decided low: publish the base sum
+      if (lane == 0) SPIN_UNTIL_NS(sm.dec_op >= op_no + 1, "decision", op_no, 0, 8000000000ull);
+      __syncwarp();
+      __threadfence_block();
+      for (int kt = warp; kt < W.gb - W.ga; kt += NW) {
+        const int r = sm.task_rb[kt];
+        const Run& q = R.r[r];
+        const int nb = W.nb[q.li];
+        const bool may_extra = C.mode == MODE_DYNAMIC && !C.force && O.L[q.li].sentinel == 0 &&
+                               O.L[q.li].est != EST_NONE && O.L[q.li].h > nb;
+        if (!may_extra || sm.dec_fin[par][q.li] > nb) continue;
+        const int i = kt - q.k0, pk = kt;
+        const float S = pk < kMaxTiles ? sm.sbuf[pk][lane]
+                                       : __ldcg(P.park + ((size_t)cta * (kMaxTasks - kMaxTiles) + pk - kMaxTiles) * 32 + lane);
+        st_tag(slot + (size_t)(q.t0 + i) * 32 + lane, S, epoch);
+      }
+    }
+  }
+  CSYNC();              // every warp is done with the run tables (the reduce phase rebuilds them)
+  if (dbg && tid == 0) dbg[3] = gclock();
+  // ---- reduce this CTA's units of the op, then the stage is done
+  const int fin3[kMaxOpLayers] = {sm.dec_fin[par][0], sm.dec_fin[par][1], sm.dec_fin[par][2]};
+  const int n_ext = sm.n_ext_items[par];
+  const unsigned e_res = O.add ? step_base + (unsigned)O.res_stage + 1u : 0u;
+  reduce_duty(P, C, O, sm, cta, G, epoch, fin3, P.slot + (size_t)(epoch & 1u) * P.slot_half, On, Wn, op_no, e_res);
+  if (dbg && tid == 0) dbg[4] = gclock();
+  CSYNC();
+  if (tid == 0) {
+    W.valid = 0;
+    sm.cons_done = op_no + 1;
+  }
+  return n_base + n_ext;
 }
 
 // ---------------------------------------------------------------------------
 // Head stage: final RMSNorm + lm_head logits (runtime.py:372), greedy argmax
 // (runtime.py:405-408) and the end-of-step control update (runtime.py:373-380).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void head_stage(const Prog& P, const ECtl& C, Smem& sm, int cta, int G) {
+__device__ __noinline__ void head_stage(const Prog& P, const ECtl& C, Smem& sm, float* xs, int cta, int G,
+                                        unsigned e_final) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int cur = C.n_steps_done & 1;
-  const int fin_inst = 4 * P.n_blocks;
-  const double s2 =
-      (double)__ldcg(P.vstat + (((size_t)cur * P.n_inst + fin_inst) * 2 + 1) * kAccSpread) * (1.0 / kFxSq);
+  // the final residual (tagged) -> shared memory, sum of squares in fixed order
+  double q = 0.0;
+  for (int i = tid; i < P.d; i += NT) {
+    u64 x;
+    SPIN_UNTIL((x = ld_relaxed64(P.xfinal + i), (unsigned)(x >> 32) == e_final), "final x", i, e_final);
+    const float v = __uint_as_float((unsigned)x);
+    xs[i] = v;
+    q += (double)v * v;
+  }
+  q = wsum(q);
+  if (lane == 0) sm.red[warp] = q;
+  CSYNC();
+  double s2 = 0.0;
+  for (int w = 0; w < NW; ++w) s2 += sm.red[w];
   const float inv = (float)(1.0 / sqrt(s2 / (double)P.d + (double)P.eps));
   for (int v = cta * NW + warp; v < P.vocab; v += G * NW) {
     const float* row = P.lm + (size_t)v * P.d;
     float a = 0.f;
-    int i = lane * 4;
     if ((P.d & 3) == 0) {
-      for (; i + 7 * 128 < P.d; i += 8 * 128) {
-        float4 w4[8], x4[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          w4[u] = __ldg(reinterpret_cast<const float4*>(row + i + u * 128));
-          x4[u] = __ldcg(reinterpret_cast<const float4*>(P.x + i + u * 128));
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) a += w4[u].x * x4[u].x + w4[u].y * x4[u].y + w4[u].z * x4[u].z + w4[u].w * x4[u].w;
-      }
-      for (; i < P.d; i += 128) {
+      for (int i = lane * 4; i < P.d; i += 128) {
         const float4 w4 = __ldg(reinterpret_cast<const float4*>(row + i));
-        const float4 x4 = __ldcg(reinterpret_cast<const float4*>(P.x + i));
+        const float4 x4 = *reinterpret_cast<const float4*>(xs + i);
         a += w4.x * x4.x + w4.y * x4.y + w4.z * x4.z + w4.w * x4.w;
       }
     } else {
-      for (int k = lane; k < P.d; k += 32) a += row[k] * __ldcg(P.x + k);
+      for (int k = lane; k < P.d; k += 32) a += row[k] * xs[k];
     }
     a = wsum(a);
     if (lane == 0) P.logits[v] = a * inv;
   }
   __threadfence();
   CSYNC();
-  if (tid == 0) sm.last = atomicAdd(P.head_cnt, 1u) == (unsigned)G - 1;
+  if (tid == 0) sm.head_last = atomicAdd(P.head_cnt, 1u) == (unsigned)G - 1;
   CSYNC();
-  if (!sm.last) return;
+  if (!sm.head_last) return;
   __threadfence();
   float best = -CUDART_INF_F;
   int bi = 0x7fffffff;
@@ -1576,38 +1305,40 @@ __device__ __forceinline__ void head_stage(const Prog& P, const ECtl& C, Smem& s
     c->pos = C.pos + 1;
     if (dyn) c->trace_step = C.trace_step + 1;
     if (dyn || C.prime) {
-      c->prev_r = C.prev_w;
-      c->prev_w = C.prev_z;
-      c->prev_z = C.prev_r;
+      c->rot = C.rot + 1;
       c->has_prev = 1;
     }
-    c->n_steps_done = C.n_steps_done + 1;
     __threadfence();
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" :: "l"(&c->n_steps_done), "r"(C.n_steps_done + 1) : "memory");
   }
 }
 
-// BEGIN: zero the next step's accumulator slots, x = embed[token]
-// (runtime.py:345) with its statistics and block-0 estimator feeds.
-__device__ __forceinline__ void begin_stage(const Prog& P, const ECtl& C, int cta, int G) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nxt = (C.n_steps_done + 1) & 1;
+// BEGIN: the step's control block, zeroing of the accumulator slots used two
+// steps ahead, x = embed[token] (runtime.py:345) as a tagged vector.
+__device__ __forceinline__ void begin_stage(const Prog& P, Smem& sm, int cta, int G, int step, int expect_done,
+                                            unsigned epoch) {
+  const int tid = threadIdx.x;
+  if (tid == 0) SPIN_UNTIL(ld_acq_s32(&P.ctl->n_steps_done) >= expect_done, "step control", expect_done, 0);
+  CSYNC();
   {
-    long long* a = P.acc + (size_t)nxt * P.acc_stride;
-    long long* z = P.acc + (size_t)(2 + C.prev_z) * P.acc_stride;
-    long long* vs = P.vstat + (size_t)nxt * P.n_inst * 2 * kAccSpread;
-    for (int i = cta * NT + tid; i < P.acc_stride / kAccSpread; i += G * NT) {   // the used words only
-      a[(size_t)i * kAccSpread] = 0;
-      z[(size_t)i * kAccSpread] = 0;
-    }
-    for (int i = cta * NT + tid; i < P.n_inst * 2; i += G * NT) vs[(size_t)i * kAccSpread] = 0;
+    const int* src = reinterpret_cast<const int*>(P.ctl);
+    int* dst = reinterpret_cast<int*>(&sm.ctl);
+    if (tid < (int)(sizeof(ECtl) / 4)) dst[tid] = __ldcg(src + tid);
   }
-  const int n_t = (P.d + 31) / 32;
-  for (int tt = cta * NW + warp; tt < n_t; tt += G * NW) {
-    const int i = tt * 32 + lane;
-    const float v = i < P.d ? __ldg(P.embed + (size_t)C.token * P.d + i) : 0.f;
-    if (i < P.d) P.x[i] = v;
-    emit_tile(P, C, 0, tt, v);
+  CSYNC();
+  if (tid == 0) {
+    __threadfence_block();
+    sm.step_ready = step + 1;                   // the producer may stream this step
   }
+  const ECtl& C = sm.ctl;
+  {
+    long long* a = acc_slot(P, (C.n_steps_done + 2) & (kCurSlots - 1));
+    long long* z = acc_slot(P, kCurSlots + ((C.rot + 1) & (kPrevSlots - 1)));
+    long long* vs = stat_words(P, (C.n_steps_done + 2) & (kCurSlots - 1), 0);
+    for (int i = cta * NT + tid; i < P.acc_stride; i += G * NT) { a[i] = 0; z[i] = 0; }
+    for (int i = cta * NT + tid; i < P.n_inst * 3; i += G * NT) vs[(size_t)i * kStatSpread] = 0;
+  }
+  for (int i = cta * NT + tid; i < P.d; i += G * NT) st_tag(P.xe + i, __ldg(P.embed + (size_t)C.token * P.d + i), epoch);
 }
 
 // ---------------------------------------------------------------------------
@@ -1623,22 +1354,21 @@ extern "C" __global__ void __launch_bounds__(NTB, 1) engine_kernel(const Prog Pk
     sm.work[0].valid = 0;
     sm.work[1].valid = 0;
     sm.dec_op = 0;
+    sm.cons_done = 0;
     sm.runs_op = -1;
     sm.step_ready = 0;
-    s_bar_seen = 0;
     // ring slots: below the LUT (after Smem) and above its zero row
     const uint32_t base = smem_u32(smem_raw);
     uint32_t lo = (base + (uint32_t)sizeof(Smem) + 1023u) & ~1023u;
     int n = 0;
     while (lo + kSlotBytes <= kLut && n < kMaxSlots) { sm.slot_off[n++] = lo - base; lo += kSlotBytes; }
-    uint32_t hi = kLut + 256 * 256 + 256;
-    while (Pk.upper_slots && hi + kSlotBytes <= base + (uint32_t)Pk.smem_dyn && n < kMaxSlots) {
+    uint32_t hi = kLut + kLutBytes;
+    while (hi + kSlotBytes <= base + (uint32_t)Pk.smem_dyn && n < kMaxSlots) {
       sm.slot_off[n++] = hi - base;
       hi += kSlotBytes;
     }
     if (n < kMaxSlots) __trap();        // host sizing guarantees kMaxSlots ring slots
-    sm.n_slots = n;
-    for (int q = 0; q < n; ++q) {
+    for (int q = 0; q < kMaxSlots; ++q) {
       mbar_init(&sm.full[q], 1);
       mbar_init(&sm.empty[q], kSlotTiles);
       sm.seq[q] = -1;
@@ -1652,58 +1382,40 @@ extern "C" __global__ void __launch_bounds__(NTB, 1) engine_kernel(const Prog Pk
     return;
   }
   float* lut = reinterpret_cast<float*>(smem_raw + (kLut - smem_u32(smem_raw)));
-  __shared__ int s_last;
+  const int s0 = __ldcg(&P.ctl->n_steps_done);   // steps completed before this launch
   int wi = 0, op_no = 0, j_op = 0;
-  // barrier epochs continue from previous launches (counter = G x stages so far)
-  const unsigned long long e0 = ld_acq64(P.bar) / (unsigned long long)G;   // stages completed before
-  unsigned long long k = 0;     // stages completed in this launch
-  ECtl& C = sm.ctl;
   for (int step = 0; step < n_steps; ++step) {
+    const unsigned step_base = (unsigned)(s0 + step) * (unsigned)P.n_stages;
     for (int si = 0; si < P.n_stages; ++si) {
       const int2 st = P.stages[si];
-      const bool wait = k > 0;
-      const unsigned long long target = e0 + k;        // epoch of the previous stage
-      if (tid == 0) PROGRESS(0, (step << 16) | si);
+      const unsigned epoch = step_base + (unsigned)si + 1u;
+      u64* dbg = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr;
       if (st.x == ST_OP) {
         int nsi = si + 1;
         while (nsi < P.n_stages && P.stages[nsi].x != ST_OP) ++nsi;
         const bool has_next = nsi < P.n_stages;
-        const bool have_desc = sm.work[wi].valid != 0;
-        if (!have_desc) {
+        if (sm.work[wi].valid == 0) {
+          CSYNC();
           const int nw4 = (int)(sizeof(Op) / 16);
           const int4* src = reinterpret_cast<const int4*>(P.ops + st.y);
           int4* dst = reinterpret_cast<int4*>(&sm.op[wi]);
           for (int q = tid; q < nw4; q += NT) dst[q] = __ldg(src + q);
           CSYNC();
         }
-        j_op += op_stage(P, C, sm.op[wi], sm.work[wi], has_next ? &sm.op[wi ^ 1] : nullptr, &sm.work[wi ^ 1],
-                         has_next ? P.ops + P.stages[nsi].y : nullptr, sm, cta, G, target, wait,
-                         P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr, op_no, j_op);
+        j_op += op_stage(P, sm.ctl, sm.op[wi], sm.work[wi], has_next ? &sm.op[wi ^ 1] : nullptr, &sm.work[wi ^ 1],
+                         has_next ? P.ops + P.stages[nsi].y : nullptr, sm, cta, G, epoch, step_base, dbg, op_no,
+                         j_op);
         ++op_no;
         wi ^= 1;
+      } else if (st.x == ST_BEGIN) {
+        if (dbg && tid == 0) dbg[0] = gclock();
+        begin_stage(P, sm, cta, G, step, s0 + step, epoch);
       } else {
-        if (wait && st.x != ST_ATTN) bar_wait(P, target);     // attention waits after its K/V prefetch
-        if (P.dbg && tid == 0 && st.x != ST_ATTN) P.dbg[((size_t)si * G + cta) * kDbgRec] = gclock();
-        if (st.x == ST_BEGIN) {
-          read_ctl(P, C);
-          if (tid == 0) {
-            __threadfence_block();
-            sm.step_ready = step + 1;                   // the producer may stream this step
-          }
-          begin_stage(P, C, cta, G);
-        } else if (st.x == ST_ATTN) {
-          attn_stage(P, C, st.y, lut, cta, G, &s_last, target, wait,
-                     P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr);
-        } else if (st.x == ST_EMIT) {
-          emit_stage(P, C, P.attn, P.d, 4 * st.y + 1, cta, G);
-        } else {
-          head_stage(P, C, sm, cta, G);
-        }
+        if (dbg && tid == 0) dbg[0] = gclock();
+        head_stage(P, sm.ctl, sm, lut, cta, G, step_base + (unsigned)P.final_stage + 1u);
       }
-      if (P.dbg && tid == 0) P.dbg[((size_t)si * G + cta) * kDbgRec + 7] = gclock();
-      bar_arrive(P, e0 + k + 1, G);
-      if (tid == 0) CSTAMP(P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr, 17);
-      ++k;
+      if (dbg && tid == 0) dbg[7] = gclock();
+      stage_arrive(P);
     }
   }
 }
