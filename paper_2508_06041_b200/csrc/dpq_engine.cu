@@ -4,59 +4,62 @@
 // runtime.py:330-381) on one CTA per SM. A step is the stage list
 //   BEGIN | per block: QKV  O  UPGATE  DOWN | HEAD
 // with NO grid barrier between stages: every vector a stage publishes (the
-// residual stream, q|k|v, SiLU(gate)*up) and every cross-window partial sum
-// is a 64-bit word {float value, u32 epoch} (single-copy atomic, so no fence),
-// and a consumer waits only for the words it reads, tagged with the epoch of
-// the stage that produces them. A relaxed stage counter (arrive after each
-// stage, wait for stage E-2 before writing the buffers of stage E) bounds the
-// skew between CTAs so double-buffered state is never overwritten early.
+// residual stream, q|k|v, the attention chunk states, SiLU(gate)*up) and every
+// cross-window partial sum is a 64-bit word {float value, u32 epoch} (single-
+// copy atomic, so no fence), and a reader waits only for the words it reads,
+// tagged with the epoch of the stage that produces them. A relaxed arrival
+// counter (one arrival per CTA and stage, in stage order) bounds the skew: a
+// stage writes its double-buffered state only after every CTA has finished
+// stage E - 2.
 //
-// Per op stage (layers sharing one input vector), CTA c owns one 512-column
-// window w of the input and a range of (32-row tile, window) groups:
-//  * input: the window's 512 values (tagged) -> shared memory; for the o op
-//    the window is the attention output of the 512 / head_dim heads it holds,
-//    computed in the prologue by every CTA of the window (RoPE, KV append by
-//    one CTA, causal softmax over the KV cache; runtime.py:351-362);
-//  * byte LUT of the window (257 x 64 fp32) from shared memory;
-//  * precision selection (runtime.py:184-193, estimator.py:35-60), fused into
-//    the prologue: the CTAs of window w split the estimator rows; each row is
-//    a G[w] . x[w] partial (G in f32 / f16 / e4m3), added in fixed point
-//    (deterministic) to the layer's accumulator with a release count; the
-//    window's first CTA adds sum x, sum x^2. The TMA producer warp of every
-//    CTA waits for the counts once it has queued the op's base planes,
-//    computes est > T (strict, runtime.py:192) from the same integers, and
-//    only then queues the extra planes of the layers that decided high;
-//  * the any-precision GEMV streams planes 0..b-1 of the nested store
-//    (quant.py:74) through a TMA ring (8 x 16 KB slots, mbarrier full/empty),
-//    64 conflict-free byte-LUT lookups (8 weight bits per LDS) per 2 KB item,
-//    Horner over planes, the per-(tile, window) sum published as a tagged word;
-//  * reduce unit u (a tile, or an up|gate tile pair) belongs to CTA u mod G:
-//    it sums its window partials in fixed window order, applies the affine
-//    epilogue y = s_in (lo sum x + span 2^-b (S + sum x / 2)) (an exact
-//    restatement of quant.py:74-78 @ x), the residual add / SiLU(gate)*up
-//    (runtime.py:364-370), and publishes the output tile.
+// Warp roles of a CTA (NCW consumer warps, one reducer warp, one TMA producer
+// warp), all walking the same stage list:
+//  * producer: streams the CTA's bitplane items (one (tile, plane) = 2 KB,
+//    cp.async.bulk into a ring of 2 KB slots, mbarrier full/empty) for every op
+//    as far ahead as the ring allows: base planes [0, nb) of the CTA's tasks,
+//    then - once the op's precision decisions are taken from the estimator
+//    accumulators (runtime.py:184-193, estimator.py:35-60) - the extra planes
+//    [nb, h) of the layers that decided high;
+//  * consumers: per op, the input window (512 columns) -> shared memory, the
+//    estimator feeds of that window (G[w] . x[w] rows, fixed point, into the
+//    layer accumulators) and the window's byte LUT (257 x 64 fp32), then the
+//    CTA's tasks: task k (one 32-row tile of one layer) goes to warp k mod NCW,
+//    Horner over its planes (S_{p+1} = 2 S_p + P_p, quant.py:74), 64 conflict-
+//    free byte-LUT lookups per 2 KB item; the base sum and the extra-plane sum
+//    of a (tile, window) are published as separate tagged words (no parking);
+//  * reducer: unit u of an op (a tile, or an up|gate tile pair) belongs to CTA
+//    u mod G; the warp waits for its units' window partials as they arrive
+//    (concurrently with the consumers), S = 2^(h - nb) S_base + S_extra in fixed
+//    window order, the affine epilogue y = s_in (lo sum x + span 2^-b (S +
+//    sum x / 2)) (an exact restatement of quant.py:74-78 @ x), the residual add
+//    / SiLU(gate)*up (runtime.py:364-370), and publishes the output tile.
+// Per (op, CTA) the work is static (host-built): the CTA's window w (CTAs are
+// split into window-aligned sets) and its tasks, every m-th tile of the op
+// (m = CTAs of the window), so each layer of the op is spread evenly whatever
+// bits it selects. Attention (runtime.py:351-362) runs in the o op's prologue
+// on (head, 64-position chunk) units; o's input windows merge the chunk states.
 #include "dpq_common.cuh"
 
-// Consumer-only CTA barrier (the producer warp never joins).
+// Consumer-only CTA barrier (the producer and reducer warps never join).
 #define CSYNC() asm volatile("bar.sync 1, %0;" :: "n"(dpq::eng::NT) : "memory")
 
 namespace dpq {
 namespace eng {
 
-constexpr int NT = 480;            // consumer threads per CTA (warps 0..14); 16 warps -> 128 registers
-constexpr int NW = NT / 32;        // consumer warps
-constexpr int NTB = NT + 32;       // + one TMA producer warp (warp 15)
-constexpr int kSlotTiles = 8;      // tiles per ring slot (one plane of up to 8 consecutive tiles)
-constexpr int kSlotBytes = kSlotTiles * 2048;
-constexpr int kMaxSlots = 8;       // ring slots (power of two)
-constexpr int kMaxRuns = 96;       // (layer, window, <= 8 tiles) runs per op per CTA
-constexpr int kMaxTiles = 128;     // groups whose parked base sums live in shared memory
-constexpr int kMaxTasks = 384;     // (tile, window) groups per CTA and op (the rest park in Prog.park)
+constexpr int NCW = 10;            // consumer warps (12 warps per CTA: 3 per SMSP -> 168 registers)
+constexpr int NW = NCW;
+constexpr int NT = NCW * 32;       // consumer threads
+constexpr int kRedWarp = NCW;      // reducer warp
+constexpr int kProdWarp = NCW + 1; // TMA producer warp
+constexpr int NTB = NT + 64;
+constexpr int kItemBytes = 2048;   // one (tile, plane) item = kTileBytes
+constexpr int kMaxSlots = 64;      // ring slots (2 KB); the host checks they fit
+constexpr int kDecRing = 4;        // op decision entries in flight
 constexpr int kCurSlots = 4;       // accumulator slots of the current step (step % 4)
 constexpr int kPrevSlots = 4;      // previous-step slots (rotation % 4)
 constexpr int kAccSlots = kCurSlots + kPrevSlots;
 constexpr int kStatSpread = 16;    // statistics words: one 128-byte line each
-constexpr int kDbgRec = 8;         // debug stamps per (stage, CTA): [0] start .. [7] end
+constexpr int kDbgRec = 16;        // debug stamps per (stage, CTA)
 constexpr double kFxSum = 4294967296.0;   // 2^32: sum x
 constexpr double kFxSq = 16777216.0;      // 2^24: sum x^2
 constexpr uint32_t kLut = 0x20000;        // the window LUT (absolute shared address)
@@ -64,7 +67,6 @@ constexpr uint32_t kLut = 0x20000;        // the window LUT (absolute shared add
 enum { ST_BEGIN = 0, ST_OP = 1, ST_HEAD = 3 };
 enum { SRC_IMM = 0, SRC_PREV_STEP = 1, SRC_PREV_BLOCK = 2 };
 enum { FEED_CUR = 0, FEED_CURFB = 1, FEED_PREV = 2 };
-enum { IN_VEC = 0, IN_ATTN = 1 };
 enum { ERR_RANGE = 1 };
 
 typedef unsigned long long u64;
@@ -87,6 +89,17 @@ struct Layer {
   double fbscale;          // 2^-fb of the set's G.x values
 };
 
+// Static work of one CTA in one op (host-built): window w (CTA j of the m
+// sharing it), tasks [task0, task0 + n_tasks) of Prog.tasks, and the CTA's
+// task count per layer.
+struct alignas(16) CtaWork {
+  int task0;
+  short n_tasks, w, j, m;
+  short cnt[kMaxOpLayers];
+  short pad;
+};
+static_assert(sizeof(CtaWork) == 32, "CtaWork is 32 bytes");
+
 struct alignas(16) Op {
   Layer L[kMaxOpLayers];
   int n_layers;
@@ -94,15 +107,18 @@ struct alignas(16) Op {
   int rms;                 // input RMS-normalised (runtime.py:383-384)
   int pair;                // up|gate SiLU pair epilogue
   int add;                 // residual add: out = res_in + y
-  int in_kind;             // IN_VEC / IN_ATTN
-  int in_stage;            // stage (index in the step) publishing `in` (IN_ATTN: the q|k|v stage)
+  int attn_in;             // input = attention of the q|k|v op (out of stage in_stage)
+  int in_stage;            // stage (index in the step) publishing `in`
   int res_stage;           // stage publishing res_in
   int inst;                // input instance: statistics + estimator feeds
   int block;
   int feed_rows;           // projection rows of the input's feeds (split over the window's CTAs)
-  const u64* in;           // tagged input (IN_ATTN: q|k|v)
+  int n_units;             // reduce units (tiles, or up|gate pairs)
+  const u64* in;           // tagged input (attn_in: the q|k|v op's output)
   const u64* res_in;       // tagged residual input (add)
   u64* out;                // tagged output
+  const CtaWork* work;     // [G]
+  long long pad2;
 };
 static_assert(sizeof(Op) % 16 == 0, "Op is copied to shared memory in 16-byte words");
 
@@ -136,6 +152,7 @@ struct Prog {
   int n_stages;
   const int2* stages;      // (kind, op index)
   const Op* ops;
+  const uint2* tasks;      // (tile | layer << 16, per-layer task counts before it: 10 bits each)
   const int* feed_begin;   // [n_inst + 1]
   const Feed* feeds;
   int n_inst;
@@ -151,13 +168,13 @@ struct Prog {
   float* logits;
   float* const* kc;        // [n_blocks] -> [seq_cap][dkv]
   float* const* vc;
-  u64* slot;               // [2][slot_half] tagged (tile, window) partial sums
+  u64* slot;               // [2][slot_half] tagged (tile, window) base partial sums
+  u64* slotx;              // [2][slot_half] tagged extra-plane partial sums
   long long slot_half;
-  float* park;             // [G][kMaxTasks - kMaxTiles][32] parked base sums beyond the shared table
   long long* acc;          // [kAccSlots][acc_stride]
   int acc_stride;
   long long* vstat;        // [kCurSlots][n_inst][3 (sum, sumsq, count)][kStatSpread]
-  u64* bar;                // stage arrivals (G per stage)
+  u64* bar;                // stage arrivals (one per CTA and stage)
   unsigned* head_cnt;
   unsigned* err;           // sticky error flags (ERR_RANGE: fixed-point range exceeded)
   signed char* tr_bits;
@@ -167,6 +184,8 @@ struct Prog {
   ECtl* ctl;
   int smem_dyn;
   u64* dbg;                // optional [n_stages][G][kDbgRec] %globaltimer stamps
+  u64* attn_part;          // [H][attn_maxch][hd + 2] tagged chunk partials (o[hd], m, l)
+  int attn_maxch;
 };
 
 // ---------------------------------------------------------------------------
@@ -268,7 +287,7 @@ __device__ __forceinline__ double rsqrt_d(double x) {
 // LUT lookups: lane l, byte s of its 64-byte plane segment -> LUT row e, slot
 // (l + s) mod 64 (layout in dpq_common.cuh); address formed by one PRMT.
 // ---------------------------------------------------------------------------
-#define ENG_LDS(dst, addr, IMM) asm("ld.shared.f32 %0, [%1+%2];" : "=f"(dst) : "r"(addr), "n"(IMM))
+#define ENG_LDS(dst, addr, IMM) asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(dst) : "r"(addr), "n"(IMM))
 
 __device__ __forceinline__ float plane_sum(const uint4 d0, const uint4 d1, const uint4 d2, const uint4 d3,
                                            uint32_t lanereg) {
@@ -290,27 +309,23 @@ __device__ __forceinline__ float plane_sum(const uint4 d0, const uint4 d1, const
   return (a0 + a1) + (a2 + a3);
 }
 
-// LUT of one 512-column window from the staged window xw: row e, slot g =
+// Byte LUT of one 512-column window from the staged window xw: row e, slot g =
 // sum_{t: bit t of e} x[8g + t]; row 256 = 0 (target of the wrapped "e - 1"
-// encoding for e = 0). Thread u < 256 builds rows [64 q, 64 q + 64) of group
-// g (u = 64 q + g).
+// encoding for e = 0). Job q = (group g, 16-row block m) writes rows
+// [16 m, 16 m + 16) of slot g (low nibble subset sums + the high nibble's);
+// the 1024 jobs are spread over all consumer threads (conflict-free stores).
 __device__ __forceinline__ void lut_build(float* lut, const float* xw) {
-  const int u = threadIdx.x;
-  if (u >= 256) return;
-  const int g = u & 63, q = u >> 6;
-  const float4 xa = *reinterpret_cast<const float4*>(xw + 8 * g);
-  const float4 xb = *reinterpret_cast<const float4*>(xw + 8 * g + 4);
-  const float xs[4] = {xa.x, xa.y, xa.z, xa.w};
-  float L[16];
-  L[0] = 0.f;
+  for (int q = threadIdx.x; q < 1024; q += NT) {
+    const int g = q & 63, m = q >> 6;
+    const float4 xa = *reinterpret_cast<const float4*>(xw + 8 * g);
+    const float4 xb = *reinterpret_cast<const float4*>(xw + 8 * g + 4);
+    float L[16];
+    L[0] = 0.f;
 #pragma unroll
-  for (int n = 1; n < 16; ++n) {
-    const int low = n & (-n);
-    L[n] = L[n ^ low] + xs[__ffs(low) - 1];
-  }
-#pragma unroll
-  for (int mm = 0; mm < 4; ++mm) {
-    const int m = 4 * q + mm;
+    for (int n = 1; n < 16; ++n) {
+      const int low = n & (-n);
+      L[n] = L[n ^ low] + (low == 1 ? xa.x : low == 2 ? xa.y : low == 4 ? xa.z : xa.w);
+    }
     float H = 0.f;
     if (m & 1) H += xb.x;
     if (m & 2) H += xb.y;
@@ -319,72 +334,37 @@ __device__ __forceinline__ void lut_build(float* lut, const float* xw) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) lut[(16 * m + i) * kGroups + g] = L[i] + H;
   }
-  if (u < 64) lut[256 * kGroups + u] = 0.f;
+  if (threadIdx.x < 64) lut[256 * kGroups + threadIdx.x] = 0.f;
 }
 
-// ---------------------------------------------------------------------------
-// Per-op work of one CTA.
-// A group is (32-row tile t, 512-column window w), linear index g = w * n_tiles
-// + t (window-major). Window w gets CTAs [ceil(w G / n_win), ceil((w+1) G /
-// n_win)) (host guarantees n_win <= G), its groups split among them evenly by
-// base planes (known before the decision). The range is cut into runs of <= 8
-// tiles of one layer. The TMA producer streams, per run and plane, one bulk
-// copy of the run's tiles into a 16 KB ring slot: base planes [0, nb) of all
-// runs, then - once the decision is taken - extra planes [nb, fin) of the runs
-// whose layer decided high (reverse run order). Consumer task (run, tile) goes
-// to warp k % NW; S is accumulated per tile by Horner over planes (S_{p+1} =
-// 2 S_p + P_p), the base part parked in shared memory.
-// ---------------------------------------------------------------------------
-struct Work {
-  int nb[kMaxOpLayers];
-  int ga, gb;
-  int w, cb, m;            // window, its first CTA, CTA count of the window
-  int valid;
-};
-
-struct Run {
-  short li, w;
-  short t0, nt;            // op tiles [t0, t0 + nt)
-  short k0;                // first tile index inside the CTA range (parking slot)
-  short pad;
-};
-
-struct RunList {
-  int n;
-  Run r[kMaxRuns];
-};
+constexpr int kMaxTasks = 256;     // tasks (tiles) per CTA and op
 
 struct Smem {
   Prog prog;
-  ECtl ctl;                          // control block of the current step
-  Op op[2];                          // consumer copies of the current / next op descriptors
-  Work work[2];
-  RunList runs;                      // consumer run list of the current op
-  Op pop;                            // producer copy of the op it streams
-  Work pw;
-  RunList pruns;
-  short pfo[kMaxRuns];
-  unsigned char ptask[kMaxTasks];
+  ECtl ctl[2];                       // control block of the step, by step parity
+  Op cop[2];                         // consumer: current / next op (by op parity)
+  CtaWork cw[2];
+  Op pop;                            // producer copy
+  CtaWork pw;
+  Op rop[2];                         // reducer copies (current / prefetched next, by op parity)
   unsigned long long full[kMaxSlots], empty[kMaxSlots];   // ring mbarriers
   volatile int seq[kMaxSlots];       // FIFO index armed in each slot (phase disambiguation)
   unsigned slot_off[kMaxSlots];
-  volatile int dec_op;               // op counter whose decision and extra tables are published
-  volatile int cons_done;            // ops the consumers have finished (tables of op n - 2 are free)
-  int runs_op;                       // op counter whose base runs are in runs / fo_bo / task_rb
-  volatile int step_ready;           // step whose control block the consumers have loaded
-  int dec_fin[2][kMaxOpLayers];      // final bits (op parity)
-  short fo_bo[kMaxRuns];
-  short fo_eo[2][kMaxRuns], fo_xt[2][kMaxRuns];
-  unsigned char task_rb[kMaxTasks];
-  unsigned char task_rx[2][kMaxTasks];
-  int n_ext_items[2], t_ext[2];
-  int last;                          // base items of the current op
+  volatile int dec_op;               // decisions of ops < dec_op are published
+  int dec_fin[kDecRing][kMaxOpLayers];
+  volatile int cons_ops;             // ops finished by the consumers
+  volatile unsigned cons_gs;         // consumer stages finished (global stage number + 1)
+  volatile int step_ready;           // steps whose control block is in ctl[]
   int head_last;
   float head_v[NW];
   int head_i[NW];
   double red[32];
-  float sbuf[kMaxTiles][32];         // base-pass S of groups whose layer has extra planes
-  float xw[kWinCols];                // the op's input window
+  alignas(16) float attn_q[128];     // RoPE'd q of the current attention unit
+  alignas(16) float attn_m[4][132];  // per-warp (o[hd], m, l) of the unit
+  alignas(16) float xw[kWinCols];    // the op's input window
+  uint2 ctask[2][kMaxTasks];         // consumer task lists (by op parity)
+  uint2 ptask[kMaxTasks];            // producer task list
+  const uint4* psrc[kMaxTasks];      // producer: plane-0 address of each task's tile
 };
 
 __device__ __forceinline__ int layer_of(const Op& O, int t) {
@@ -393,15 +373,17 @@ __device__ __forceinline__ int layer_of(const Op& O, int t) {
   return li;
 }
 
-// First group whose first base item is >= item i (window-local item index).
-__device__ __forceinline__ int group_at(const Op& O, const int* nb, int wsum_, int w, int r) {
-  for (int li = 0; li < O.n_layers; ++li) {
-    const int seg = O.L[li].n_tiles * nb[li];
-    if (r < seg) return w * O.n_tiles + O.L[li].tile_off + (r + nb[li] - 1) / nb[li];
-    r -= seg;
+// Per-layer integers of an op (<= 3 layers) in registers: indexed by select,
+// never by a local-memory array.
+struct I3 {
+  int v0, v1, v2;
+  __device__ __forceinline__ int operator[](int i) const { return i == 0 ? v0 : (i == 1 ? v1 : v2); }
+  __device__ __forceinline__ void set(int i, int x) {
+    if (i == 0) v0 = x;
+    else if (i == 1) v1 = x;
+    else v2 = x;
   }
-  return (w + 1) * O.n_tiles;
-}
+};
 
 // Base planes per layer for the step mode (known before the decision).
 __device__ __forceinline__ int base_bit(const Layer& L, const ECtl& C) {
@@ -411,112 +393,48 @@ __device__ __forceinline__ int base_bit(const Layer& L, const ECtl& C) {
   return L.l;
 }
 
-// Work of CTA cta (one warp).
-__device__ __forceinline__ void build_work_warp(const Op& O, const ECtl& C, int cta, int G, Work& W) {
-  const int lane = threadIdx.x & 31;
-  const int nbl = lane < O.n_layers ? base_bit(O.L[lane], C) : 0;
-  if (lane < O.n_layers) W.nb[lane] = nbl;
-  const int wtot = wsum(lane < O.n_layers ? O.L[lane].n_tiles * nbl : 0);
-  __syncwarp();
-  const int w = (int)((unsigned)cta * (unsigned)O.n_win / (unsigned)G);
-  const int cb = (w * G + O.n_win - 1) / O.n_win, ce = ((w + 1) * G + O.n_win - 1) / O.n_win;
-  const int m = ce - cb;
-  if (lane < 2) {
-    const int idx = cta - cb + lane;
-    const int item = (int)((unsigned)idx * (unsigned)wtot / (unsigned)m);
-    const int g = group_at(O, W.nb, wtot, w, item);
-    if (lane == 0) W.ga = g;
-    else W.gb = g;
-  }
-  if (lane == 0) { W.w = w; W.cb = cb; W.m = m; }
-  __syncwarp();
+// Task k of a CTA's list: op tile, layer, and per-layer counts of the tasks before it.
+__device__ __forceinline__ int task_tile(uint2 t) { return (int)(t.x & 0xffffu); }
+__device__ __forceinline__ int task_layer(uint2 t) { return (int)(t.x >> 16); }
+__device__ __forceinline__ int task_before(uint2 t, const I3& per_layer) {
+  return (int)(t.y & 1023u) * per_layer.v0 + (int)((t.y >> 10) & 1023u) * per_layer.v1 +
+         (int)((t.y >> 20) & 1023u) * per_layer.v2;
+}
+__device__ __forceinline__ I3 base_bits(const Op& O, const ECtl& C) {
+  I3 r{0, 0, 0};
+  r.v0 = base_bit(O.L[0], C);
+  if (O.n_layers > 1) r.v1 = base_bit(O.L[1], C);
+  if (O.n_layers > 2) r.v2 = base_bit(O.L[2], C);
+  return r;
 }
 
-// Warp-parallel run list + base FIFO offsets + task -> run table of work W
-// (one window; segments = layers, one per lane). Returns the base item count.
-__device__ int build_runs_warp(const Op& O, const Work& W, RunList& R, short* fo_bo, unsigned char* task_r) {
+// Asynchronous warp-parallel copy of an op descriptor (cp.async; complete
+// after cp.async.wait_all of the issuing threads).
+__device__ __forceinline__ void load_op_async(const Prog& P, int oi, Op* O) {
   const int lane = threadIdx.x & 31;
-  const int nt = O.n_tiles;
-  if (W.ga >= W.gb) {
-    if (lane == 0) R.n = 0;
-    __syncwarp();
-    return 0;
-  }
-  const int w = W.w;
-  int lo = 0, len = 0, nr = 0, items = 0;
-  const int li = lane;
-  if (lane < O.n_layers) {
-    const Layer& L = O.L[li];
-    lo = max(W.ga - w * nt, L.tile_off);
-    const int hi = min(W.gb - w * nt, L.tile_off + L.n_tiles);
-    len = max(hi - lo, 0);
-    nr = (len + kSlotTiles - 1) / kSlotTiles;
-    items = nr * W.nb[li];
-  }
-  int rb = nr, ib = items;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int a = __shfl_up_sync(0xffffffffu, rb, o), b = __shfl_up_sync(0xffffffffu, ib, o);
-    if (lane >= o) { rb += a; ib += b; }
-  }
-  const int n_runs = __shfl_sync(0xffffffffu, rb, 31), n_items = __shfl_sync(0xffffffffu, ib, 31);
-  rb -= nr;
-  ib -= items;
-  if (n_runs > kMaxRuns || W.gb - W.ga > kMaxTasks) __trap();   // host sizing (engine_eligible) violated
-  for (int q = 0; q < nr; ++q) {
-    Run& r = R.r[rb + q];
-    r.li = (short)li;
-    r.w = (short)w;
-    r.t0 = (short)(lo + q * kSlotTiles);
-    r.nt = (short)min(kSlotTiles, len - q * kSlotTiles);
-    r.k0 = (short)(w * nt + lo + q * kSlotTiles - W.ga);
-    fo_bo[rb + q] = (short)(ib + q * W.nb[li]);
-  }
-  for (int k0 = 0; k0 < W.gb - W.ga; k0 += 32) {
-    const int kt = k0 + lane;
-    const bool ok = kt < W.gb - W.ga;
-    const int t = W.ga + (ok ? kt : 0) - w * nt;
-    int l2 = 0;
-    while (l2 + 1 < O.n_layers && t >= O.L[l2 + 1].tile_off) ++l2;
-    const int slo = __shfl_sync(0xffffffffu, lo, l2), srb = __shfl_sync(0xffffffffu, rb, l2);
-    if (ok) task_r[kt] = (unsigned char)(srb + (t - slo) / kSlotTiles);
-  }
-  if (lane == 0) R.n = n_runs;
-  __syncwarp();
-  return n_items;
+  const int nw4 = (int)(sizeof(Op) / 16);
+  const char* src = reinterpret_cast<const char*>(P.ops + oi);
+  for (int q = lane; q < nw4; q += 32)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"((uint32_t)__cvta_generic_to_shared(O) + 16u * q),
+                 "l"(src + 16 * q) : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// Warp-parallel FIFO offsets of the extra planes [nb, fin) once the decision
-// is known: runs in reverse order (the producer's issue order), exclusive
-// prefix sums of items and tasks, and the extra task -> run table.
-__device__ void extra_fifo_warp(const Work& W, const int* fin, const RunList& R, int base_items, short* fo_eo,
-                                short* fo_xt, unsigned char* task_rx, int& n_items, int& n_tasks) {
+// Warp-parallel copy of an op descriptor (+ this CTA's work and task list).
+__device__ __forceinline__ void load_op(const Prog& P, int oi, int cta, Op* O, CtaWork* W, uint2* tasks) {
   const int lane = threadIdx.x & 31;
-  int carry_i = base_items, carry_t = 0;
-  for (int c0 = 0; c0 < R.n; c0 += 32) {
-    const int idx = c0 + lane;
-    const int r = R.n - 1 - idx;
-    int ex = 0, nt = 0;
-    if (idx < R.n) {
-      ex = fin[R.r[r].li] - W.nb[R.r[r].li];
-      nt = ex > 0 ? R.r[r].nt : 0;
-    }
-    int si = ex, st = nt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, si, o), b = __shfl_up_sync(0xffffffffu, st, o);
-      if (lane >= o) { si += a; st += b; }
-    }
-    if (idx < R.n) {
-      fo_eo[r] = (short)(carry_i + si - ex);
-      fo_xt[r] = (short)(carry_t + st - nt);
-      for (int t = 0; t < nt; ++t) task_rx[carry_t + st - nt + t] = (unsigned char)r;
-    }
-    carry_i += __shfl_sync(0xffffffffu, si, 31);
-    carry_t += __shfl_sync(0xffffffffu, st, 31);
-  }
-  n_items = carry_i - base_items;
-  n_tasks = carry_t;
+  const int nw4 = (int)(sizeof(Op) / 16);
+  const int4* src = reinterpret_cast<const int4*>(P.ops + oi);
+  int4* dst = reinterpret_cast<int4*>(O);
+  for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
+  __syncwarp();
+  if (!W) return;
+  const CtaWork* gw = O->work + cta;
+  if (lane < 2) reinterpret_cast<int4*>(W)[lane] = __ldg(reinterpret_cast<const int4*>(gw) + lane);
+  __syncwarp();
+  const int n = W->n_tasks, t0 = W->task0;
+  for (int k = lane; k < n; k += 32) tasks[k] = __ldg(P.tasks + t0 + k);
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
@@ -570,23 +488,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 }
 
 // ---------------------------------------------------------------------------
-// Epochs, the stage counter and the step control
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned stage_epoch(const Prog& P, int step_no, int si) {
-  return (unsigned)step_no * (unsigned)P.n_stages + (unsigned)si + 1u;
-}
-// every CTA arrives once per stage after its last read of that stage's inputs
-__device__ __forceinline__ void stage_arrive(const Prog& P) {
-  CSYNC();
-  if (threadIdx.x == 0) red_rel_addu64(P.bar, 1ull);
-}
-// before writing the double-buffered state of stage E: all CTAs are done with E - 2
-__device__ __forceinline__ bool stage_done(const Prog& P, unsigned E) {
-  if (E <= 2) return true;
-  return ld_acq64(P.bar) >= (u64)(E - 2) * gridDim.x;
-}
-
-// ---------------------------------------------------------------------------
 // Estimator accumulators (fixed point, per step slot) and statistics
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ long long* acc_slot(const Prog& P, int slot) { return P.acc + (size_t)slot * P.acc_stride; }
@@ -599,8 +500,8 @@ __device__ __forceinline__ long long* stat_words(const Prog& P, int cur, int ins
 // rows j, j + m, ...; its i-th row goes to warp kFeedW0 + i % kFeedWarps.
 // Row r of feed F: partial G_F[w][r] . x[w] in fp32 lanes + double warp sum,
 // fixed point at 2^fb, added to the set's accumulator, then a release count.
-constexpr int kFeedW0 = 8, kFeedWarps = 6;      // warps 8..13 (warps 0..7 build the LUT)
-constexpr int kStatW = 14;                       // statistics warp
+constexpr int kFeedW0 = 0, kFeedWarps = NCW - 1; // warps 0..NCW-2 (then the LUT build, all warps)
+constexpr int kStatW = NCW - 1;                  // statistics warp
 
 struct FeedSel {      // the feed a row belongs to and where it accumulates
   const Feed* F;
@@ -619,17 +520,35 @@ __device__ __forceinline__ long long* feed_acc(const Prog& P, const ECtl& C, con
   return acc_slot(P, slot) + F.acc;
 }
 
-// Window partial of G row r (lanes: 16 columns each) against xw.
-__device__ __forceinline__ double feed_row_dot(const Feed& F, int w, int r, const float* xw) {
+// G row r of feed F in window w, lanes 16 columns each: raw data (f16: 2
+// words, f32: 4, e4m3: 1 + the row scale), loaded ahead of the input window.
+struct GRow {
+  uint4 g[2];
+  float scale;
+};
+__device__ __forceinline__ void feed_row_load(const Feed& F, int w, int r, GRow& R) {
+  const int lane = threadIdx.x & 31;
+  const size_t base = ((size_t)w * F.k + r) * kWinCols + 16 * lane;
+  R.scale = 1.f;
+  if (F.dtype == G_F16) {
+    const uint4* g = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(F.G) + base);
+    R.g[0] = ld_nc16(g);
+    R.g[1] = ld_nc16(g + 1);
+  } else if (F.dtype == G_F32) {
+    // 16 floats per lane: loaded in feed_row_dot (not held across the input wait)
+  } else {   // e4m3 with a per-row scale
+    R.g[0] = ld_nc16(reinterpret_cast<const unsigned char*>(F.G) + base);
+    R.scale = __ldg(F.gscale + r);
+  }
+}
+// Window partial G[w][r] . x[w] from the loaded row (fp32 lanes + double warp sum).
+__device__ __forceinline__ double feed_row_dot(const Feed& F, int w, int r, const GRow& R, const float* xw) {
   const int lane = threadIdx.x & 31;
   const float* xl = xw + 16 * lane;
   float s = 0.f;
-  const size_t base = ((size_t)w * F.k + r) * kWinCols + 16 * lane;
   if (F.dtype == G_F16) {
-    const uint4* g = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(F.G) + base);
-    const uint4 a = ld_nc16(g), b = ld_nc16(g + 1);
-    const __half2* ha = reinterpret_cast<const __half2*>(&a);
-    const __half2* hb = reinterpret_cast<const __half2*>(&b);
+    const __half2* ha = reinterpret_cast<const __half2*>(&R.g[0]);
+    const __half2* hb = reinterpret_cast<const __half2*>(&R.g[1]);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const float2 u = __half22float2(ha[i]), v = __half22float2(hb[i]);
@@ -639,7 +558,8 @@ __device__ __forceinline__ double feed_row_dot(const Feed& F, int w, int r, cons
       s = fmaf(v.y, xl[8 + 2 * i + 1], s);
     }
   } else if (F.dtype == G_F32) {
-    const uint4* g = reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(F.G) + base);
+    const uint4* g = reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(F.G) +
+                                                    ((size_t)w * F.k + r) * kWinCols + 16 * lane);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint4 a = ld_nc16(g + q);
@@ -648,9 +568,8 @@ __device__ __forceinline__ double feed_row_dot(const Feed& F, int w, int r, cons
       s = fmaf(__uint_as_float(a.z), xl[4 * q + 2], s);
       s = fmaf(__uint_as_float(a.w), xl[4 * q + 3], s);
     }
-  } else {   // e4m3 with a per-row scale
-    const uint4 a = ld_nc16(reinterpret_cast<const unsigned char*>(F.G) + base);
-    const unsigned wd[4] = {a.x, a.y, a.z, a.w};
+  } else {
+    const unsigned wd[4] = {R.g[0].x, R.g[0].y, R.g[0].z, R.g[0].w};
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -659,7 +578,7 @@ __device__ __forceinline__ double feed_row_dot(const Feed& F, int w, int r, cons
         e.__x = (unsigned char)(wd[q] >> (8 * j));
         s = fmaf((float)e, xl[4 * q + j], s);
       }
-    s *= __ldg(F.gscale + r);
+    s *= R.scale;
   }
   return wsum((double)s);
 }
@@ -675,27 +594,62 @@ __device__ __forceinline__ const Feed* feed_of_row(const Prog& P, int inst, int 
   return F;
 }
 
-// Statistics + feeds of the op's input window (warps kFeedW0.. / kStatW), after
-// the LUT build started (xw complete).
-__device__ __forceinline__ void window_feeds(const Prog& P, const ECtl& C, const Op& O, const Work& W,
-                                             const float* xw) {
+// Feed rows of this CTA (rows j, j + m, ... of the instance's row list; its
+// i-th row -> warp kFeedW0 + i % kFeedWarps). The first kFeedPre rows of a
+// warp are loaded before the input window arrives (feed_prefetch) and
+// finished once it is staged (feed_finish); further rows are loaded then.
+constexpr int kFeedPre = 2;
+struct FeedPre {
+  bool pre;                // the warp's first kFeedPre rows were prefetched
+  const Feed* F[kFeedPre];
+  int r[kFeedPre];
+  GRow R[kFeedPre];
+};
+
+__device__ __forceinline__ void feed_prefetch(const Prog& P, const ECtl& C, const Op& O, const CtaWork& W,
+                                              FeedPre& fp) {
+  const int warp = threadIdx.x >> 5;
+  fp.pre = true;
+#pragma unroll
+  for (int i = 0; i < kFeedPre; ++i) {
+    fp.F[i] = nullptr;
+    const int q = W.j + (warp - kFeedW0 + i * kFeedWarps) * W.m;
+    if (warp < kFeedW0 || warp >= kFeedW0 + kFeedWarps || q >= O.feed_rows) continue;
+    const Feed* F = feed_of_row(P, O.inst, q);
+    if (!feed_active(*F, C)) continue;
+    fp.F[i] = F;
+    fp.r[i] = q - F->row0;
+    feed_row_load(*F, W.w, fp.r[i], fp.R[i]);
+  }
+}
+
+// Row partial -> fixed point at 2^fb into the set's accumulator, then a release count.
+__device__ __forceinline__ void feed_add(const Prog& P, const ECtl& C, const Feed& F, int r, double v) {
+  if ((threadIdx.x & 31) == 0) {
+    long long* a = feed_acc(P, C, F);
+    red_add64(a + r, fx(v, F.fxscale, P.err));
+    red_rel_add64(a + F.k + 1, 1);          // count (release: the value above is visible first)
+  }
+}
+
+// Feeds + statistics of the op's input window, once it is staged in xw.
+__device__ __forceinline__ void feed_finish(const Prog& P, const ECtl& C, const Op& O, const CtaWork& W,
+                                            const FeedPre& fp, const float* xw) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int cta = blockIdx.x;
-  const int j = cta - W.cb, m = W.m;
+  const int j = W.j, m = W.m;
   if (warp >= kFeedW0 && warp < kFeedW0 + kFeedWarps) {
-    // projection rows: this CTA's i-th row -> warp kFeedW0 + i % kFeedWarps
-    for (int i = warp - kFeedW0;; i += kFeedWarps) {
+    if (fp.pre)
+#pragma unroll
+      for (int i = 0; i < kFeedPre; ++i)
+        if (fp.F[i]) feed_add(P, C, *fp.F[i], fp.r[i], feed_row_dot(*fp.F[i], W.w, fp.r[i], fp.R[i], xw));
+    for (int i = warp - kFeedW0 + (fp.pre ? kFeedPre * kFeedWarps : 0);; i += kFeedWarps) {
       const int q = j + i * m;
       if (q >= O.feed_rows) break;
       const Feed* F = feed_of_row(P, O.inst, q);
       if (!feed_active(*F, C)) continue;
-      const int r = q - F->row0;
-      const double v = feed_row_dot(*F, W.w, r, xw);
-      if (lane == 0) {
-        long long* a = feed_acc(P, C, *F);
-        red_add64(a + r, fx(v, F->fxscale, P.err));
-        red_rel_add64(a + F->k + 1, 1);          // count (release: the value above is visible first)
-      }
+      GRow R;
+      feed_row_load(*F, W.w, q - F->row0, R);
+      feed_add(P, C, *F, q - F->row0, feed_row_dot(*F, W.w, q - F->row0, R, xw));
     }
   } else if (warp == kStatW && j == 0) {
     // sum x, sum x^2 of the window: op statistics + the feeds' sum x^2 words
@@ -786,141 +740,295 @@ __device__ __forceinline__ float4 rope4(const u64* v, int i0, int hd, float4 c, 
 }
 __device__ __forceinline__ float dot4(float4 a, float4 b) { return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w; }
 
-__device__ __noinline__ void attn_window(const Prog& P, const ECtl& C, const Op& O, const Work& W, float* scratch,
-                                         float* xw, unsigned e_qkv) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int hd = P.hd, qh = P.H / P.KV, b = O.block;
-  const int t = C.pos;
-  const int h0 = W.w * kWinCols / hd;
-  const int nh = min(kWinCols / hd, P.H - h0);
-  const int nsub = max(1, NW / nh);
-  const int units = nh * nsub;
-  const float scale = 1.0f / sqrtf((float)hd);
+// Attention unit (head h, 64-position chunk ch), run in the o
+// op's prologue (runtime.py:351-362), on kAttnWarps warps (kw) of this CTA;
+// O is the o op (O.in = the q|k|v op's tagged output).
+//  * The cached K / V rows of the chunk (positions < t; they do not depend on
+//    this step) are copied into shared memory (kv: [64][hd] K | [64][hd] V)
+//    with cp.async before the q / k / v tags are awaited.
+//  * q, k_t, v_t: all tag loads of a poll are issued together (one L2 round
+//    trip once published); RoPE (runtime.py:288-298). Position t (last chunk)
+//    is this step's k / v; the first head of a KV group appends them to the
+//    cache (runtime.py:355-356).
+//  * Scores (runtime.py:358): warp kw takes rows 16 kw .. 16 kw + 15, two
+//    lanes per row (half the dims each, columns rotated by lane so a quarter
+//    warp hits distinct banks); per-warp softmax state (m, l) and o = sum_s
+//    p_s V_s with lanes over dims; the warps' states are merged in fixed order
+//    and published unnormalised as tagged words (epoch e). o's input load
+//    merges the chunks of a head (attn_merge).
+constexpr int kAttnChunk = 64;
+constexpr int kAttnWarps = 4;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void attn_unit(const Prog& P, const ECtl& C, const Op& O, Smem& sm, int h, int ch, int kw,
+                                          float* kv, unsigned e, u64* dbg) {
+  const int lane = threadIdx.x & 31, tix = kw * 32 + lane;
+  const bool stamp = dbg && tix == 0;
+  const long long ck0 = clock64();
+  if (stamp) dbg[8] = gclock();
+  const int hd = P.hd, qh = P.H / P.KV, g = h / qh, t = C.pos;
+  const int s0 = kAttnChunk * ch, s1 = min(s0 + kAttnChunk, t + 1);
+  const int nc = min(s1, t) - s0;                                       // cached rows of the chunk
+  float* Ks = kv;
+  float* Vs = kv + kAttnChunk * hd;
+  float* kc = P.kc[O.block];
+  float* vc = P.vc[O.block];
+  const size_t goff = (size_t)g * hd;
+  {
+    const int q4 = hd / 4;
+    for (int i = tix; i < nc * q4; i += 32 * kAttnWarps) {
+      const int r = i / q4, c = 4 * (i - r * q4);
+      cp_async16(Ks + r * hd + c, kc + (size_t)(s0 + r) * P.dkv + goff + c);
+      cp_async16(Vs + r * hd + c, vc + (size_t)(s0 + r) * P.dkv + goff + c);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  if (stamp) dbg[12] = clock64() - ck0;
+  const int half = hd / 2;
   const int i0 = 4 * lane;
   const bool act = i0 < hd;
-  const int jj = i0 < hd / 2 ? i0 : i0 - hd / 2;
-  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float4 c4 = act ? __ldg(reinterpret_cast<const float4*>(P.cosv + (size_t)t * (hd / 2) + jj)) : z4;
-  const float4 s4 = act ? __ldg(reinterpret_cast<const float4*>(P.sinv + (size_t)t * (hd / 2) + jj)) : z4;
-  float* kc = P.kc[b];
-  float* vc = P.vc[b];
-  const unsigned long long kvpol = l2_evict_last_policy();   // the KV cache is re-read every step
-  const int ps = hd + 4;
-  bool wrote = false;
-  for (int u = warp; u < units; u += NW) {
-    const int hh = u % nh, sub = u / nh;
-    const int h = h0 + hh, g = h / qh;
-    const float4 q4 = act ? rope4(O.in + (size_t)h * hd, i0, hd, c4, s4, e_qkv) : z4;
-    float4 kt = z4, vt = z4;
-    const bool own_t = (t % nsub) == sub;
-    if (own_t && act) {
-      kt = rope4(O.in + P.d + (size_t)g * hd, i0, hd, c4, s4, e_qkv);      // RoPE'd k of this step
-      vt = tag4(O.in + P.d + P.dkv + (size_t)g * hd + i0, e_qkv);
-      if (W.cb == (int)blockIdx.x && h % qh == 0) {                        // KV append (runtime.py:355-356)
-        *reinterpret_cast<float4*>(kc + (size_t)t * P.dkv + g * hd + i0) = kt;
-        *reinterpret_cast<float4*>(vc + (size_t)t * P.dkv + g * hd + i0) = vt;
-        wrote = true;
+  if (kw == 0) {
+    const bool lo = i0 < half;
+    const int ip = lo ? i0 + half : i0 - half;
+    const int jj = lo ? i0 : i0 - half;
+    const bool cur = t < s1;                                             // position t is in this chunk
+    const u64* qv = O.in + (size_t)h * hd;
+    const u64* kv_ = O.in + P.d + goff;
+    const u64* vv_ = O.in + P.d + P.dkv + goff;
+    float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f), s4 = c4;
+    if (act) {
+      c4 = __ldg(reinterpret_cast<const float4*>(P.cosv + (size_t)t * half + jj));
+      s4 = __ldg(reinterpret_cast<const float4*>(P.sinv + (size_t)t * half + jj));
+    }
+    uint4 w[10];
+    bool ok;
+    auto poll = [&]() {
+      if (!act) return true;
+      w[0] = ld_tag2(qv + i0); w[1] = ld_tag2(qv + i0 + 2);
+      w[2] = ld_tag2(qv + ip); w[3] = ld_tag2(qv + ip + 2);
+      bool r = true;
+      if (cur) {
+        w[4] = ld_tag2(kv_ + i0); w[5] = ld_tag2(kv_ + i0 + 2);
+        w[6] = ld_tag2(kv_ + ip); w[7] = ld_tag2(kv_ + ip + 2);
+        w[8] = ld_tag2(vv_ + i0); w[9] = ld_tag2(vv_ + i0 + 2);
+#pragma unroll
+        for (int j = 4; j < 10; ++j) r &= w[j].y == e && w[j].w == e;
       }
-    }
-    float m = -CUDART_INF_F, l = 0.f;
-    float4 o = z4;
-    // cached positions s < t, 2-deep register pipeline
-    float4 k0 = z4, v0 = z4, k1 = z4, v1 = z4;
-    int s = sub;
-    const size_t goff = (size_t)g * hd + i0;
-    if (act && s < t) { k0 = ld_keep(kc + (size_t)s * P.dkv + goff, kvpol); v0 = ld_keep(vc + (size_t)s * P.dkv + goff, kvpol); }
-    if (act && s + nsub < t) {
-      k1 = ld_keep(kc + (size_t)(s + nsub) * P.dkv + goff, kvpol);
-      v1 = ld_keep(vc + (size_t)(s + nsub) * P.dkv + goff, kvpol);
-    }
-#define ATTN_UPDATE(K_, V_)                                                          \
-    {                                                                                \
-      const float a = wsum(dot4(q4, K_)) * scale;              /* runtime.py:358 */  \
-      const float mn = fmaxf(m, a);                                                  \
-      const float corr = expf(m - mn), p = expf(a - mn);       /* runtime.py:359-361 */ \
-      l = l * corr + p;                                                              \
-      o.x = o.x * corr + p * V_.x; o.y = o.y * corr + p * V_.y;                      \
-      o.z = o.z * corr + p * V_.z; o.w = o.w * corr + p * V_.w;                      \
-      m = mn;                                                                        \
-    }
-    for (; s < t; s += 2 * nsub) {
-      ATTN_UPDATE(k0, v0)
-      if (act && s + 2 * nsub < t) {
-        k0 = ld_keep(kc + (size_t)(s + 2 * nsub) * P.dkv + goff, kvpol);
-        v0 = ld_keep(vc + (size_t)(s + 2 * nsub) * P.dkv + goff, kvpol);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r &= w[j].y == e && w[j].w == e;
+      return r;
+    };
+    SPIN_UNTIL((ok = poll()), "q|k|v", h, e);
+    auto val4 = [&](int j) {
+      return make_float4(__uint_as_float(w[j].x), __uint_as_float(w[j].z), __uint_as_float(w[j + 1].x),
+                         __uint_as_float(w[j + 1].z));
+    };
+    auto rope = [&](float4 a, float4 b) {                              // runtime.py:288-298 (half split)
+      float4 r;
+      if (lo) {
+        r.x = a.x * c4.x - b.x * s4.x; r.y = a.y * c4.y - b.y * s4.y;
+        r.z = a.z * c4.z - b.z * s4.z; r.w = a.w * c4.w - b.w * s4.w;
+      } else {
+        r.x = b.x * s4.x + a.x * c4.x; r.y = b.y * s4.y + a.y * c4.y;
+        r.z = b.z * s4.z + a.z * c4.z; r.w = b.w * s4.w + a.w * c4.w;
       }
-      if (s + nsub < t) {
-        ATTN_UPDATE(k1, v1)
-        if (act && s + 3 * nsub < t) {
-          k1 = ld_keep(kc + (size_t)(s + 3 * nsub) * P.dkv + goff, kvpol);
-          v1 = ld_keep(vc + (size_t)(s + 3 * nsub) * P.dkv + goff, kvpol);
+      return r;
+    };
+    if (act) {
+      *reinterpret_cast<float4*>(sm.attn_q + i0) = rope(val4(0), val4(2));
+      if (cur) {
+        const float4 k4 = rope(val4(4), val4(6)), v4 = val4(8);
+        *reinterpret_cast<float4*>(Ks + (t - s0) * hd + i0) = k4;
+        *reinterpret_cast<float4*>(Vs + (t - s0) * hd + i0) = v4;
+        if (h % qh == 0) {                                               // KV append (runtime.py:355-356)
+          *reinterpret_cast<float4*>(kc + (size_t)t * P.dkv + goff + i0) = k4;
+          *reinterpret_cast<float4*>(vc + (size_t)t * P.dkv + goff + i0) = v4;
         }
       }
     }
-    if (own_t) ATTN_UPDATE(kt, vt)
-#undef ATTN_UPDATE
-    float* pr = scratch + u * ps;
-    if (act) *reinterpret_cast<float4*>(pr + i0) = o;
-    if (lane == 0) { pr[hd] = m; pr[hd + 1] = l; }
   }
-  if (wrote) __threadfence();        // the appended rows are read by other CTAs in later steps
-  CSYNC();
-  // merge the nsub units of each head in fixed order -> xw
-  for (int q = tid; q < kWinCols; q += NT) {
-    const int hh = q / hd, i = q - hh * hd;
-    float r = 0.f;
-    if (hh < nh) {
-      float M = -CUDART_INF_F;
-      for (int sb = 0; sb < nsub; ++sb) M = fmaxf(M, scratch[(sb * nh + hh) * ps + hd]);
-      float L = 0.f, acc = 0.f;
-      for (int sb = 0; sb < nsub; ++sb) {
-        const float* pr = scratch + (sb * nh + hh) * ps;
-        const float mw = pr[hd];
-        const float e = mw == -CUDART_INF_F ? 0.f : expf(mw - M);
-        L += e * pr[hd + 1];
-        acc += e * pr[i];
-      }
-      r = acc / L;                                             // runtime.py:362
+  if (stamp) { dbg[9] = gclock(); dbg[13] = clock64() - ck0; }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  asm volatile("bar.sync 2, %0;" :: "n"(32 * kAttnWarps) : "memory");
+  if (stamp) { dbg[10] = gclock(); dbg[14] = clock64() - ck0; }
+  // scores: row r of the chunk, half hf of the dims
+  const float scale = 1.0f / sqrtf((float)hd);
+  const int r = 16 * kw + (lane >> 1), hf = lane & 1;
+  const bool valid = s0 + r < s1;
+  float a0 = 0.f, a1 = 0.f;
+  {
+    const float* kr = Ks + r * hd + hf * half;
+    const float* qr = sm.attn_q + hf * half;
+    const int rot = 4 * ((lane >> 1) & 7);
+    for (int j = 0; j < half; j += 8) {
+      const int c0 = (j + rot) & (half - 1), c1 = (j + 4 + rot) & (half - 1);
+      a0 += dot4(*reinterpret_cast<const float4*>(qr + c0), *reinterpret_cast<const float4*>(kr + c0));
+      if (half >= 8) a1 += dot4(*reinterpret_cast<const float4*>(qr + c1), *reinterpret_cast<const float4*>(kr + c1));
     }
-    xw[q] = r;
   }
+  float a = a0 + a1;
+  a += __shfl_xor_sync(0xffffffffu, a, 1);
+  const float sc = valid ? a * scale : -CUDART_INF_F;
+  float m = sc;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  const float p = valid ? expf(sc - m) : 0.f;                            // runtime.py:359-361
+  const float l = wsum(hf == 0 ? p : 0.f);
+  if (stamp) dbg[15] = clock64() - ck0;
+  float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int n = max(0, min(16, s1 - s0 - 16 * kw));
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (j < n) {
+      const float pj = __shfl_sync(0xffffffffu, p, 2 * j);
+      if (act) {
+        const float4 vv = *reinterpret_cast<const float4*>(Vs + (16 * kw + j) * hd + i0);
+        o.x += pj * vv.x; o.y += pj * vv.y; o.z += pj * vv.z; o.w += pj * vv.w;
+      }
+    }
+  }
+  float* mw = sm.attn_m[kw];
+  if (act) *reinterpret_cast<float4*>(mw + i0) = o;
+  if (lane == 0) { mw[hd] = n > 0 ? m : -CUDART_INF_F; mw[hd + 1] = l; }
+  asm volatile("bar.sync 2, %0;" :: "n"(32 * kAttnWarps) : "memory");
+  if (kw == 0) {
+    float M = -CUDART_INF_F;
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm.attn_m[w][hd]);
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) {
+      const float mw_ = sm.attn_m[w][hd];
+      const float ew = mw_ == -CUDART_INF_F ? 0.f : expf(mw_ - M);
+      L += ew * sm.attn_m[w][hd + 1];
+      if (act) {
+        const float4 ow = *reinterpret_cast<const float4*>(sm.attn_m[w] + i0);
+        acc.x += ew * ow.x; acc.y += ew * ow.y; acc.z += ew * ow.z; acc.w += ew * ow.w;
+      }
+    }
+    u64* dst = P.attn_part + ((size_t)h * P.attn_maxch + ch) * (hd + 2);
+    if (act) {
+      st_tag(dst + i0, acc.x, e);
+      st_tag(dst + i0 + 1, acc.y, e);
+      st_tag(dst + i0 + 2, acc.z, e);
+      st_tag(dst + i0 + 3, acc.w, e);
+    }
+    if (lane == 0) {
+      st_tag(dst + hd, M, e);
+      st_tag(dst + hd + 1, L, e);
+    }
+  }
+  asm volatile("bar.sync 2, %0;" :: "n"(32 * kAttnWarps) : "memory");   // kv / attn_m reusable
+  if (stamp) { dbg[11] = gclock(); dbg[6] = clock64() - ck0; }
+}
+
+// o's input window: the attention output of the window's heads, merged over
+// the heads' chunk partials in fixed chunk order (runtime.py:359-362).
+__device__ __forceinline__ void attn_merge(const Prog& P, const ECtl& C, int w, unsigned e, float* xw) {
+  const int t = threadIdx.x;
+  if (t >= 128) return;
+  const int hd = P.hd;
+  const int c0 = w * kWinCols + 4 * t;
+  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c0 < P.d) {
+    const int h = c0 / hd, i = c0 - h * hd;
+    const int nch = (C.pos + kAttnChunk) / kAttnChunk;
+    const u64* base = P.attn_part + (size_t)h * P.attn_maxch * (hd + 2);
+    float M = -CUDART_INF_F, L = 0.f;
+    for (int ch = 0; ch < nch; ++ch) {                                   // online merge, fixed chunk order
+      const u64* q = base + (size_t)ch * (hd + 2);
+      uint4 a, b, s;
+      bool ok;
+      SPIN_UNTIL((a = ld_tag2(q + i), b = ld_tag2(q + i + 2), s = ld_tag2(q + hd),
+                  ok = a.y == e && a.w == e && b.y == e && b.w == e && s.y == e && s.w == e), "attention partial", h, ch);
+      const float mc = __uint_as_float(s.x);
+      const float Mn = fmaxf(M, mc);
+      const float ea = expf(M - Mn), eb = expf(mc - Mn);
+      L = L * ea + __uint_as_float(s.z) * eb;
+      r.x = r.x * ea + __uint_as_float(a.x) * eb;
+      r.y = r.y * ea + __uint_as_float(a.z) * eb;
+      r.z = r.z * ea + __uint_as_float(b.x) * eb;
+      r.w = r.w * ea + __uint_as_float(b.z) * eb;
+      M = Mn;
+    }
+    const float inv = 1.0f / L;                                          // runtime.py:362
+    r.x *= inv; r.y *= inv; r.z *= inv; r.w *= inv;
+  }
+  *reinterpret_cast<float4*>(xw + 4 * t) = r;
 }
 
 // ---------------------------------------------------------------------------
-// Tile reduction + epilogue (one warp, lane = row of the tile)
+// The stage counter. Global stage number gs = step * n_stages + si (steps
+// since reset); epoch(gs) = gs + 1 tags everything stage gs publishes. Every
+// CTA's reducer warp arrives once per stage, in order, after its consumers
+// and itself are done with the stage; a stage writes its double-buffered
+// state only after stage gs - 2 is done everywhere.
 // ---------------------------------------------------------------------------
-// S of op tile t: sum of the window partials in fixed window order, each
-// awaited until it carries this stage's epoch.
-__device__ __forceinline__ float tile_S(const u64* slot, const Op& O, int t, unsigned epoch) {
+__device__ __forceinline__ bool stage_done(const Prog& P, unsigned gs) {
+  if (gs < 2) return true;
+  return ld_acq64(P.bar) >= (u64)(gs - 1) * gridDim.x;
+}
+
+// ---------------------------------------------------------------------------
+// Reduction + epilogue (reducer warp, lane = row of the tile)
+// ---------------------------------------------------------------------------
+// Window partials of up to two op tiles (t0, t1 = -1 for none): base sums
+// from slot, extra-plane sums from slotx when ex0 / ex1 > 0. All words of a
+// poll are loaded together, each awaited until it carries the stage's epoch,
+// then summed in fixed window order: S = 2^ex S_base + S_extra.
+__device__ __forceinline__ float2 tiles_S(const Prog& P, const Op& O, int t0, int ex0, int t1, int ex1,
+                                         unsigned epoch) {
   const int lane = threadIdx.x & 31;
   const int rows = O.n_tiles * 32;
-  const u64* base = slot + (size_t)t * 32 + lane;
-  float acc = 0.f;
-  for (int w0 = 0; w0 < O.n_win; w0 += 8) {
-    const int nw = min(8, O.n_win - w0);
-    u64 v[8];
-    bool ok;
-    unsigned n_ = 0;
-    u64 t0 = 0;
-    do {
+  const size_t par = (size_t)((epoch - 1u) & 1u) * P.slot_half;   // parity of the stage (epoch = gs + 1)
+  const u64* b0 = P.slot + par + (size_t)t0 * 32 + lane;
+  const u64* x0 = P.slotx + par + (size_t)t0 * 32 + lane;
+  const u64* b1 = P.slot + par + (size_t)max(t1, 0) * 32 + lane;
+  const u64* x1 = P.slotx + par + (size_t)max(t1, 0) * 32 + lane;
+  const bool two = t1 >= 0;
+  float s0, e0, s1, e1;
+  bool ok;
+  unsigned n_ = 0;
+  u64 tt0 = 0;
+  do {
+    // one pass: every window's words (loads of a chunk are independent of the
+    // previous chunk's sums, so they stream), checked and summed in order
+    s0 = e0 = s1 = e1 = 0.f;
+    ok = true;
+    for (int w0 = 0; w0 < O.n_win; w0 += 8) {
+      const int nw = min(8, O.n_win - w0);
+      u64 v[4][8];
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (j < nw) v[j] = ld_relaxed64(base + (size_t)(w0 + j) * rows);
-      ok = true;
+        if (j < nw) {
+          const size_t o = (size_t)(w0 + j) * rows;
+          v[0][j] = ld_relaxed64(b0 + o);
+          v[1][j] = ex0 > 0 ? ld_relaxed64(x0 + o) : ((u64)epoch << 32);
+          v[2][j] = two ? ld_relaxed64(b1 + o) : ((u64)epoch << 32);
+          v[3][j] = two && ex1 > 0 ? ld_relaxed64(x1 + o) : ((u64)epoch << 32);
+        }
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (j < nw) ok &= (unsigned)(v[j] >> 32) == epoch;
-      if ((++n_ & 1023u) == 0) {
-        const u64 t_ = gclock();
-        if (t0 == 0) t0 = t_;
-        else if (t_ - t0 > 4000000000ull) hang("window partials", t, epoch);
-      }
-    } while (!__all_sync(0xffffffffu, ok));
+        if (j < nw) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < nw) acc += __uint_as_float((unsigned)v[j]);
-  }
-  return acc;
+          for (int q = 0; q < 4; ++q) ok &= (unsigned)(v[q][j] >> 32) == epoch;
+          s0 += __uint_as_float((unsigned)v[0][j]);
+          e0 += __uint_as_float((unsigned)v[1][j]);
+          s1 += __uint_as_float((unsigned)v[2][j]);
+          e1 += __uint_as_float((unsigned)v[3][j]);
+        }
+    }
+    if ((++n_ & 1023u) == 0) {
+      const u64 t_ = gclock();
+      if (tt0 == 0) tt0 = t_;
+      else if (t_ - tt0 > 4000000000ull) hang("window partials", t0, epoch);
+    }
+  } while (!__all_sync(0xffffffffu, ok));
+  return make_float2(ex0 > 0 ? ldexpf(s0, ex0) + e0 : s0, ex1 > 0 ? ldexpf(s1, ex1) + e1 : s1);
 }
 
 struct Epi { float scale, sx; };
@@ -937,303 +1045,375 @@ __device__ __forceinline__ Epi op_epi(const Prog& P, const ECtl& C, const Op& O)
   return e;
 }
 
-__device__ __forceinline__ float tile_y(const u64* slot, const Op& O, const int* fin, const Epi& E, int t,
-                                        unsigned epoch, int& li, int& r, bool& valid) {
-  const int lane = threadIdx.x & 31;
-  li = layer_of(O, t);
-  const Layer& L = O.L[li];
-  const float S = tile_S(slot, O, t, epoch);
-  r = (t - L.tile_off) * 32 + lane;
-  valid = r < L.rows;
-  if (!valid) return 0.f;
-  const float lo = __ldg(L.lo + r), span = __ldg(L.span + r);
-  return E.scale * (lo * E.sx + ldexpf(span, -fin[li]) * (S + 0.5f * E.sx));
-}
-
 // ---------------------------------------------------------------------------
-// The TMA producer warp: streams every op's planes into the ring, running
-// ahead of the consumers (bounded by ring space), and takes each op's
-// decisions (runtime.py:184-193) once the base planes are queued.
+// Precision decisions of an op (producer warp), runtime.py:184-193: from the
+// estimator accumulators (identical integers on every CTA, so every CTA takes
+// the same decisions without another exchange).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op& O, const Work& W, int* fin,
+__device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op& O, const I3& nb, I3& fin,
                                           int cta) {
   const int lane = threadIdx.x & 31;
   const bool dyn = C.mode == MODE_DYNAMIC;
-  for (int li = 0; li < O.n_layers; ++li) {
+  // every estimating layer's accumulator set: count complete, then all its
+  // words loaded together (one round trip for the op)
+  const long long* acc[kMaxOpLayers] = {nullptr, nullptr, nullptr};
+  bool any = false;
+#pragma unroll
+  for (int li = 0; li < kMaxOpLayers; ++li) {
+    if (li >= O.n_layers) break;
     const Layer& L = O.L[li];
-    int bit = W.nb[li];
-    double est = CUDART_NAN;
-    const bool estimating = dyn && L.sentinel == 0 && L.est != EST_NONE;
-    if (estimating) {
+    if (dyn && L.sentinel == 0 && L.est != EST_NONE) {
       const int slot = (L.src == SRC_PREV_STEP && C.has_prev) ? kCurSlots + ((C.rot - 1) & (kPrevSlots - 1))
                                                               : (C.n_steps_done & (kCurSlots - 1));
-      const long long* a = acc_slot(P, slot) + L.acc;
-      if (lane == 0) SPIN_UNTIL(ld_acq_s64(a + L.k + 1) >= L.cnt_expect, "estimator feeds", L.trace, L.cnt_expect);
-      __syncwarp();
+      acc[li] = acc_slot(P, slot) + L.acc;
+      any = true;
+    }
+  }
+  if (any) {
+    const long long* am = lane == 0 ? acc[0] : lane == 1 ? acc[1] : acc[2];
+    const bool mine = lane < O.n_layers && am != nullptr;
+    const Layer& Lm = O.L[min(lane, O.n_layers - 1)];
+    bool ok;
+    SPIN_UNTIL((ok = __all_sync(0xffffffffu, !mine || ld_acq_s64(am + Lm.k + 1) >= Lm.cnt_expect)), "estimator feeds",
+               O.L[0].trace, O.n_layers);
+  }
+  long long v[kMaxOpLayers][kMaxK / 32 + 1];
+#pragma unroll
+  for (int li = 0; li < kMaxOpLayers; ++li)
+#pragma unroll
+    for (int q = 0; q <= kMaxK / 32; ++q) {
+      const int i = q * 32 + lane;
+      v[li][q] = 0;
+      if (acc[li] && i <= O.L[li].k) v[li][q] = __ldcg(acc[li] + i);   // G.x values, then sum x^2 at i = k
+    }
+#pragma unroll
+  for (int li = 0; li < kMaxOpLayers; ++li) {
+    if (li >= O.n_layers) break;
+    const Layer& L = O.L[li];
+    int bit = nb[li];
+    double est = CUDART_NAN;
+    if (acc[li]) {
       double q = 0.0;
-      for (int i = lane; i < L.k; i += 32) {
-        const double g = (double)__ldcg(a + i) * L.fbscale;
-        q += g * g;
+      long long sqw = 0;
+#pragma unroll
+      for (int qq = 0; qq <= kMaxK / 32; ++qq) {
+        const int i = qq * 32 + lane;
+        if (i < L.k) {
+          const double g = (double)v[li][qq] * L.fbscale;
+          q += g * g;
+        } else if (i == L.k) {
+          sqw = v[li][qq];
+        }
       }
       q = wsum(q);
-      const double sq = (double)__ldcg(a + L.k) * (1.0 / kFxSq);
+      sqw = __shfl_sync(0xffffffffu, sqw, L.k & 31);
+      const double sq = (double)sqw * (1.0 / kFxSq);
       const double sc = O.rms ? rsqrt_d(sq / (double)O.cols + (double)P.eps) : 1.0;
       if (L.est == EST_PROJECTION) est = q > 0.0 ? sc * q * rsqrt_d(q) : 0.0;                 // estimator.py:56-57
       else est = L.slope * (sq > 0.0 ? sc * sq * rsqrt_d(sq) : 0.0) + L.intercept;           // estimator.py:41-42
       if (!C.force) bit = est > L.T ? L.h : L.l;                                              // strict > (runtime.py:192)
     }
-    fin[li] = bit;
+    fin.set(li, bit);
     if (lane == 0 && dyn && cta == 0 && L.trace >= 0 && P.n_trace > 0 && C.trace_step < P.max_steps) {
       const size_t o = (size_t)C.trace_step * P.n_trace + L.trace;
       P.tr_bits[o] = (signed char)bit;
-      P.tr_est[o] = estimating ? (float)est : CUDART_NAN_F;
+      P.tr_est[o] = acc[li] ? (float)est : CUDART_NAN_F;
     }
   }
   __syncwarp();
 }
 
-__device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G, int n_steps) {
+// ---------------------------------------------------------------------------
+// The TMA producer warp: streams every op's items into the ring (FIFO order:
+// base items of the CTA's tasks, then the extra items of the layers that
+// decided high), running ahead of the consumers as far as the ring allows.
+// ---------------------------------------------------------------------------
+// Items are issued by kIssueLanes lanes at once, one task per lane (its planes
+// in lockstep): a batch spans <= kIssueLanes * 8 <= kMaxSlots consecutive FIFO
+// items, so the slot each lane waits for holds an item issued before the batch
+// (no lane can wait on an item another lane of the batch has yet to issue).
+constexpr int kIssueLanes = 8;
+static_assert(kIssueLanes * 8 <= kMaxSlots, "an issue batch must fit the ring");
+
+__device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G, int n_steps, int s0) {
   const int lane = threadIdx.x & 31;
-  int j = 0, op_no = 0;
+  int fifo = 0, oi = 0;
   const unsigned char* dyn0 = reinterpret_cast<const unsigned char*>(&sm);
   const unsigned long long l2pol = l2_evict_first_policy();
-  auto issue = [&](const Op& O, const Run& r, int p) {
-    const int slot = j & (kMaxSlots - 1);
-    if (j >= kMaxSlots) {
-      const uint32_t a = smem_u32(&sm.empty[slot]);
-      const unsigned par = (unsigned)(((j / kMaxSlots) - 1) & 1);
-      SPIN_UNTIL_NS(mbar_test(a, par), "producer slot", j, op_no, 12000000000ull);
-      // the consumers' generic reads of the slot precede this async-proxy write
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  // items [jb, jb + n) of task k: planes p0 .. p0 + n - 1 of its tile
+  auto issue_task = [&](int k, int jb, int p0, int n, long long pstride) {
+    const unsigned char* src0 = reinterpret_cast<const unsigned char*>(sm.psrc[k]) + (long long)p0 * pstride;
+    for (int p = 0; p < n; ++p) {
+      const int j = jb + p;
+      const int slot = j % kMaxSlots;
+      if (j >= kMaxSlots) {
+        // the consumer's release (mbarrier arrive after its reads) orders its
+        // reads of the slot before this TMA write
+        const unsigned par = (unsigned)(((j / kMaxSlots) - 1) & 1);
+        SPIN_UNTIL_NS(mbar_test(smem_u32(&sm.empty[slot]), par), "producer slot", j, oi, 12000000000ull);
+      }
+      sm.seq[slot] = j;
+      mbar_expect_tx(&sm.full[slot], (unsigned)kItemBytes);
+      tma_load_1d(const_cast<unsigned char*>(dyn0) + sm.slot_off[slot], src0 + (long long)p * pstride,
+                  (unsigned)kItemBytes, &sm.full[slot], l2pol);
     }
-    sm.seq[slot] = j;
-    const Layer& L = O.L[r.li];
-    const uint4* src = L.planes + p * L.pstride + ((long long)r.w * L.n_tiles + (r.t0 - L.tile_off)) * (kTileBytes / 16);
-    mbar_expect_tx(&sm.full[slot], (unsigned)r.nt * kTileBytes);
-    tma_load_1d(const_cast<unsigned char*>(dyn0) + sm.slot_off[slot], src, (unsigned)r.nt * kTileBytes, &sm.full[slot],
-                l2pol);
-    ++j;
   };
   for (int step = 0; step < n_steps; ++step) {
     if (lane == 0) SPIN_UNTIL_NS(sm.step_ready >= step + 1, "producer step", step, 0, 12000000000ull);
     __syncwarp();
     __threadfence_block();
-    const ECtl& C = sm.ctl;
+    const ECtl& C = sm.ctl[step & 1];
     for (int si = 0; si < P.n_stages; ++si) {
       const int2 st = P.stages[si];
       if (st.x != ST_OP) continue;
-      {
-        const int nw4 = (int)(sizeof(Op) / 16);
-        const int4* src = reinterpret_cast<const int4*>(P.ops + st.y);
-        int4* dst = reinterpret_cast<int4*>(&sm.pop);
-        for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
-      }
-      __syncwarp();
+      load_op(P, st.y, cta, &sm.pop, &sm.pw, sm.ptask);
       const Op& O = sm.pop;
-      build_work_warp(O, C, cta, G, sm.pw);
-      const int nbi = build_runs_warp(O, sm.pw, sm.pruns, sm.pfo, sm.ptask);   // same runs as the consumers'
-      const RunList& R = sm.pruns;
-      if (lane == 0)
-        for (int r = 0; r < R.n; ++r)
-          for (int p = 0; p < sm.pw.nb[R.r[r].li]; ++p) issue(O, R.r[r], p);
-      __syncwarp();
-      const int par = op_no & 1;
-      int fin[kMaxOpLayers];
-      decide_op(P, C, O, sm.pw, fin, cta);
-      // the decision tables are double-buffered by op parity: the consumers
-      // must be done with op op_no - 2 before they are overwritten
-      if (lane == 0) SPIN_UNTIL_NS(sm.cons_done >= op_no - 1, "consumer progress", op_no, sm.cons_done, 12000000000ull);
-      __syncwarp();
-      if (lane < O.n_layers) sm.dec_fin[par][lane] = lane == 0 ? fin[0] : lane == 1 ? fin[1] : fin[2];
-      int ni, nt;
-      extra_fifo_warp(sm.pw, fin, R, nbi, sm.fo_eo[par], sm.fo_xt[par], sm.task_rx[par], ni, nt);
-      if (lane == 0) {
-        sm.n_ext_items[par] = ni;
-        sm.t_ext[par] = nt;
-        __threadfence_block();
-        sm.dec_op = op_no + 1;          // the consumers may now run the extra planes
-        for (int r = R.n - 1; r >= 0; --r) {
-          const int li = R.r[r].li;
-          for (int p = sm.pw.nb[li]; p < fin[li]; ++p) issue(O, R.r[r], p);
-        }
+      const CtaWork& W = sm.pw;
+      const I3 nb = base_bits(O, C);
+      I3 fin = nb;
+      const long long ps0 = O.L[0].pstride * 16, ps1 = O.L[1].pstride * 16, ps2 = O.L[2].pstride * 16;
+      // plane-0 address of every task's tile
+      for (int k = lane; k < W.n_tasks; k += 32) {
+        const uint2 tk = sm.ptask[k];
+        const Layer& L = O.L[task_layer(tk)];
+        sm.psrc[k] = L.planes + ((long long)W.w * L.n_tiles + (task_tile(tk) - L.tile_off)) * (kItemBytes / 16);
       }
       __syncwarp();
-      ++op_no;
+      u64* pdbg = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr;
+      for (int k0 = 0; k0 < W.n_tasks; k0 += kIssueLanes) {
+        const int k = k0 + lane;
+        if (lane < kIssueLanes && k < W.n_tasks) {
+          const uint2 tk = sm.ptask[k];
+          const int li = task_layer(tk);
+          issue_task(k, fifo + task_before(tk, nb), 0, nb[li], li == 0 ? ps0 : li == 1 ? ps1 : ps2);
+        }
+        __syncwarp();
+      }
+      const int n_base = W.cnt[0] * nb.v0 + W.cnt[1] * nb.v1 + W.cnt[2] * nb.v2;
+      if (pdbg && lane == 0) pdbg[5] = gclock();
+      // the op's decisions (taken by the reducer warp)
+      if (lane == 0) SPIN_UNTIL_NS(sm.dec_op >= oi + 1, "producer decision", oi, 0, 12000000000ull);
+      __syncwarp();
+      __threadfence_block();
+      fin = I3{sm.dec_fin[oi % kDecRing][0], sm.dec_fin[oi % kDecRing][1], sm.dec_fin[oi % kDecRing][2]};
+      if (pdbg && lane == 0) pdbg[6] = gclock();
+      const I3 ex{fin.v0 - nb.v0, fin.v1 - nb.v1, fin.v2 - nb.v2};
+      const int n_ext = W.cnt[0] * ex.v0 + W.cnt[1] * ex.v1 + W.cnt[2] * ex.v2;
+      if (n_ext > 0)
+        for (int k0 = 0; k0 < W.n_tasks; k0 += kIssueLanes) {
+          const int k = k0 + lane;
+          if (lane < kIssueLanes && k < W.n_tasks) {
+            const uint2 tk = sm.ptask[k];
+            const int li = task_layer(tk);
+            if (ex[li] > 0)
+              issue_task(k, fifo + n_base + task_before(tk, ex), nb[li], ex[li], li == 0 ? ps0 : li == 1 ? ps1 : ps2);
+          }
+          __syncwarp();
+        }
+      fifo += n_base + n_ext;
+      ++oi;
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// The op stage (consumer warps 0..NW-1)
+// Consumer warps: one op stage
 // ---------------------------------------------------------------------------
-// Reduction of the op's units: unit u belongs to CTA u mod G, its i-th unit to
-// warp i mod NW. Warp NW - 1 first prepares the next op's work and runs.
-__device__ __forceinline__ void reduce_duty(const Prog& P, const ECtl& C, const Op& O, Smem& sm, int cta, int G,
-                                            unsigned epoch, const int* fin, const u64* slot, Op* On, Work* Wn,
-                                            int op_no, unsigned e_res) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n_units = O.pair ? O.L[0].n_tiles : O.n_tiles;
-  const int mine = n_units > cta ? (n_units - cta + G - 1) / G : 0;
-  if (warp == NW - 1 && On && !Wn->valid) {
-    build_work_warp(*On, C, cta, G, *Wn);
-    const int nbi = build_runs_warp(*On, *Wn, sm.runs, sm.fo_bo, sm.task_rb);
-    if (lane == 0) {
-      Wn->valid = 1;
-      sm.last = nbi;
-      sm.runs_op = op_no + 1;
-    }
+// Horner over items [j0, j0 + n) of the FIFO (one 2 KB item per plane) for
+// the tile at slot offset: S = 2 S + P_p.
+__device__ __forceinline__ float stream_task(Smem& sm, int j0, int n, uint32_t lanereg) {
+  const int lane = threadIdx.x & 31;
+  const unsigned char* dyn0 = reinterpret_cast<const unsigned char*>(&sm);
+  float S = 0.f;
+  for (int q = 0; q < n; ++q) {
+    const int j = j0 + q;
+    const int sl = j % kMaxSlots;
+    if (lane == 0) SPIN_UNTIL_NS(sm.seq[sl] == j, "ring sequence", j, sm.seq[sl], 4000000000ull);
+    __syncwarp();
+    const uint32_t fa = smem_u32(&sm.full[sl]);
+    const unsigned fpar = (unsigned)((j / kMaxSlots) & 1);
+    SPIN_UNTIL_NS(mbar_test(fa, fpar), "ring slot", j, fpar, 4000000000ull);
+    const uint4* d = reinterpret_cast<const uint4*>(dyn0 + sm.slot_off[sl]) + lane;
+    const uint4 d0 = d[0], d1 = d[32], d2 = d[64], d3 = d[96];
+    __syncwarp();
+    if (lane == 0) mbar_arrive_n(&sm.empty[sl], 1u);
+    S = 2.f * S + plane_sum(d0, d1, d2, d3, lanereg);
   }
-  if (mine == 0) return;
-  const Epi E = op_epi(P, C, O);
-  for (int i = warp; i < mine; i += NW) {
-    const int u = cta + i * G;
-    if (O.pair) {
-      const int half = O.L[0].n_tiles;
-      int li, r, li2, r2;
-      bool ok, ok2;
-      const float up = tile_y(slot, O, fin, E, u, epoch, li, r, ok);
-      const float gt = tile_y(slot, O, fin, E, u + half, epoch, li2, r2, ok2);
-      if (ok) st_tag(O.out + r, up * (gt / (1.0f + expf(-gt))), epoch);        // runtime.py:368
-    } else {
-      int li, r;
-      bool ok;
-      const float y = tile_y(slot, O, fin, E, u, epoch, li, r, ok);
-      if (ok) {
-        const int o = O.L[li].out_off + r;
-        float v = y;
-        if (O.add) {                                                            // runtime.py:364, 370
-          u64 x;
-          SPIN_UNTIL((x = ld_relaxed64(O.res_in + o), (unsigned)(x >> 32) == e_res), "residual", o, e_res);
-          v = __uint_as_float((unsigned)x) + y;
-        }
-        st_tag(O.out + o, v, epoch);
-      }
-    }
-  }
+  return S;
 }
 
-__device__ __forceinline__ int op_stage(const Prog& P, const ECtl& C, const Op& O, Work& W, Op* On, Work* Wn,
-                                        const Op* On_global, Smem& sm, int cta, int G, unsigned epoch,
-                                        unsigned step_base, u64* dbg, int op_no, int j_op) {
+__device__ __forceinline__ void cons_op(const Prog& P, Smem& sm, int oi, int op_idx, int n_ops, int si, unsigned gs,
+                                        unsigned step_base, int cta, int G, int& fifo, const ECtl& C, u64* dbg) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int par = op_no & 1;
-  // ---- work and base runs (decision independent)
-  const bool built = W.valid != 0;
-  CSYNC();
-  if (!built) {
-    if (warp == 0) build_work_warp(O, C, cta, G, W);
-    CSYNC();
-  }
-  if (warp == 0 && sm.runs_op != op_no) {
-    const int nbi = build_runs_warp(O, W, sm.runs, sm.fo_bo, sm.task_rb);
-    if (lane == 0) sm.last = nbi;
-  }
-  if (dbg && tid == 0) dbg[0] = gclock();
-  // the next op's descriptor -> shared memory (its work is built in the reduce phase)
-  if (warp == NW - 1 && On && !Wn->valid) {
-    const int nw4 = (int)(sizeof(Op) / 16);
-    const int4* src = reinterpret_cast<const int4*>(On_global);
-    int4* dst = reinterpret_cast<int4*>(On);
-    for (int q = lane; q < nw4; q += 32) dst[q] = __ldg(src + q);
-  }
-  // ---- input window -> xw (skew bound checked on the way: stage E - 2 done)
+  const int b = oi & 1;
   float* lut = reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLut - smem_u32(&sm)));
-  if (tid == 32) SPIN_UNTIL(stage_done(P, epoch), "stage counter", epoch, 0);
-  if (O.in_kind == IN_ATTN) {
-    attn_window(P, C, O, W, lut, sm.xw, step_base + (unsigned)O.in_stage + 1u);
+  if (dbg && tid == 0) dbg[0] = gclock();
+  // skew bound: this stage writes partials / attention states of parity gs
+  if (tid == 0) SPIN_UNTIL(stage_done(P, gs), "stage counter", gs, 0);
+  CSYNC();
+  const Op& O = sm.cop[b];
+  const CtaWork& W = sm.cw[b];
+  const unsigned e_in = step_base + (unsigned)O.in_stage + 1u;
+  FeedPre fp;
+  fp.pre = false;
+  // attention units (the o op): unit u = (head u mod H, chunk u / H) on CTA G - 1 - (u mod G)
+  if (O.attn_in && warp < kAttnWarps) {
+    const int n_att = P.H * ((C.pos + kAttnChunk) / kAttnChunk);
+    for (int u = G - 1 - cta; u < n_att; u += G) attn_unit(P, C, O, sm, u % P.H, u / P.H, warp, lut, e_in, dbg);
+  }
+  // the next op's descriptor, work and tasks (consumed at its start; warp NW - 1
+  // is idle while the input window is awaited)
+  if (warp == NW - 1) load_op(P, (op_idx + 1) % n_ops, cta, &sm.cop[b ^ 1], &sm.cw[b ^ 1], sm.ctask[b ^ 1]);
+  // input window (other ops: the estimator G rows are loaded while it is awaited)
+  if (O.attn_in) {
+    attn_merge(P, C, W.w, e_in, sm.xw);
   } else {
-    load_window(O.in, O.cols, W.w, step_base + (unsigned)O.in_stage + 1u, sm.xw);
+    feed_prefetch(P, C, O, W, fp);
+    load_window(O.in, O.cols, W.w, e_in, sm.xw);
   }
   CSYNC();
   if (dbg && tid == 0) dbg[1] = gclock();
-  // ---- LUT (warps 0..7) | estimator feeds and statistics (warps 8..14)
+  // estimator feeds + statistics of the window, then its LUT (all warps)
+  feed_finish(P, C, O, W, fp, sm.xw);
   lut_build(lut, sm.xw);
-  window_feeds(P, C, O, W, sm.xw);
   CSYNC();
   if (dbg && tid == 0) dbg[2] = gclock();
-  // ---- stream: tasks (run, tile) in FIFO order
-  const RunList& R = sm.runs;
-  const unsigned char* dyn0 = reinterpret_cast<const unsigned char*>(&sm);
+  const I3 nb = base_bits(O, C);
   const uint32_t lanereg = kLut | ((uint32_t)lane * 4u);
-  const int n_base = sm.last;
-  u64* slot = P.slot + (size_t)(epoch & 1u) * P.slot_half + (size_t)W.w * O.n_tiles * 32;
-  for (int kind = 0; kind < 2; ++kind) {
-    if (kind) {
-      if (lane == 0) SPIN_UNTIL_NS(sm.dec_op >= op_no + 1, "decision", op_no, 0, 8000000000ull);
-      __syncwarp();
-      __threadfence_block();
-    }
-    const int n_tasks = kind ? sm.t_ext[par] : W.gb - W.ga;
-    for (int kt = warp; kt < n_tasks; kt += NW) {
-      const int r = kind ? sm.task_rx[par][kt] : sm.task_rb[kt];
-      const Run& q = R.r[r];
-      const int i = kt - (kind ? sm.fo_xt[par][r] : q.k0);
-      const int nb = W.nb[q.li];
-      const int fin = kind ? sm.dec_fin[par][q.li] : nb;
-      const int p0 = kind ? nb : 0, p1 = kind ? fin : nb;
-      const int jr = j_op + (kind ? sm.fo_eo[par][r] : sm.fo_bo[r]);
-      const int pk = q.k0 + i;                                   // group index in [ga, gb)
-      float S = 0.f;
-      if (kind) S = pk < kMaxTiles ? sm.sbuf[pk][lane]
-                                   : __ldcg(P.park + ((size_t)cta * (kMaxTasks - kMaxTiles) + pk - kMaxTiles) * 32 + lane);
-      for (int p = p0; p < p1; ++p) {
-        const int j = jr + (p - p0);
-        const int sl = j & (kMaxSlots - 1);
-        if (lane == 0) SPIN_UNTIL_NS(sm.seq[sl] == j, "ring sequence", j, sm.seq[sl], 2000000000ull);
-        __syncwarp();
-        const uint32_t fa = smem_u32(&sm.full[sl]);
-        const unsigned fpar = (unsigned)((j / kMaxSlots) & 1);
-        SPIN_UNTIL_NS(mbar_test(fa, fpar), "ring slot", j, fpar, 2000000000ull);
-        const uint4* d = reinterpret_cast<const uint4*>(dyn0 + sm.slot_off[sl] + i * kTileBytes) + lane;
-        const uint4 d0 = d[0], d1 = d[32], d2 = d[64], d3 = d[96];
-        __syncwarp();
-        if (lane == 0) mbar_arrive_n(&sm.empty[sl], i == q.nt - 1 ? (unsigned)(kSlotTiles + 1 - q.nt) : 1u);
-        S = 2.f * S + plane_sum(d0, d1, d2, d3, lanereg);       // Horner over planes
-      }
-      const int t = q.t0 + i;
-      // base pass of a layer that may still add planes: park; else publish
-      const bool may_extra = !kind && C.mode == MODE_DYNAMIC && !C.force && O.L[q.li].sentinel == 0 &&
-                             O.L[q.li].est != EST_NONE && O.L[q.li].h > nb;
-      if (may_extra) {
-        if (pk < kMaxTiles) sm.sbuf[pk][lane] = S;
-        else __stcg(P.park + ((size_t)cta * (kMaxTasks - kMaxTiles) + pk - kMaxTiles) * 32 + lane, S);
-      }
-      if (!may_extra || kind) st_tag(slot + (size_t)t * 32 + lane, S, epoch);
-    }
-    if (!kind) {
-      CSYNC();          // parked base sums visible
-      // groups that parked but whose layer decided low: publish the base sum
-      if (lane == 0) SPIN_UNTIL_NS(sm.dec_op >= op_no + 1, "decision", op_no, 0, 8000000000ull);
-      __syncwarp();
-      __threadfence_block();
-      for (int kt = warp; kt < W.gb - W.ga; kt += NW) {
-        const int r = sm.task_rb[kt];
-        const Run& q = R.r[r];
-        const int nb = W.nb[q.li];
-        const bool may_extra = C.mode == MODE_DYNAMIC && !C.force && O.L[q.li].sentinel == 0 &&
-                               O.L[q.li].est != EST_NONE && O.L[q.li].h > nb;
-        if (!may_extra || sm.dec_fin[par][q.li] > nb) continue;
-        const int i = kt - q.k0, pk = kt;
-        const float S = pk < kMaxTiles ? sm.sbuf[pk][lane]
-                                       : __ldcg(P.park + ((size_t)cta * (kMaxTasks - kMaxTiles) + pk - kMaxTiles) * 32 + lane);
-        st_tag(slot + (size_t)(q.t0 + i) * 32 + lane, S, epoch);
-      }
+  const size_t par = (size_t)(gs & 1u) * P.slot_half + (size_t)W.w * O.n_tiles * 32 + lane;
+  const unsigned epoch = gs + 1u;
+  const uint2* tasks = sm.ctask[b];
+  for (int k = warp; k < W.n_tasks; k += NW) {
+    const uint2 tk = tasks[k];
+    const int li = task_layer(tk);
+    const float S = stream_task(sm, fifo + task_before(tk, nb), nb[li], lanereg);
+    st_tag(P.slot + par + (size_t)task_tile(tk) * 32, S, epoch);
+  }
+  if (dbg && tid == 0) dbg[3] = gclock();
+  const int n_base = W.cnt[0] * nb.v0 + W.cnt[1] * nb.v1 + W.cnt[2] * nb.v2;
+  // extra planes of the layers that decided high
+  if (lane == 0) SPIN_UNTIL_NS(sm.dec_op >= oi + 1, "decision", oi, 0, 8000000000ull);
+  __syncwarp();
+  __threadfence_block();
+  const int* df = sm.dec_fin[oi % kDecRing];
+  const I3 ex{df[0] - nb.v0, O.n_layers > 1 ? df[1] - nb.v1 : 0, O.n_layers > 2 ? df[2] - nb.v2 : 0};
+  const int n_ext = W.cnt[0] * ex.v0 + W.cnt[1] * ex.v1 + W.cnt[2] * ex.v2;
+  if (n_ext > 0) {
+    for (int k = warp; k < W.n_tasks; k += NW) {
+      const uint2 tk = tasks[k];
+      const int li = task_layer(tk);
+      if (ex[li] <= 0) continue;
+      const float S = stream_task(sm, fifo + n_base + task_before(tk, ex), ex[li], lanereg);
+      st_tag(P.slotx + par + (size_t)task_tile(tk) * 32, S, epoch);
     }
   }
-  CSYNC();              // every warp is done with the run tables (the reduce phase rebuilds them)
-  if (dbg && tid == 0) dbg[3] = gclock();
-  // ---- reduce this CTA's units of the op, then the stage is done
-  const int fin3[kMaxOpLayers] = {sm.dec_fin[par][0], sm.dec_fin[par][1], sm.dec_fin[par][2]};
-  const int n_ext = sm.n_ext_items[par];
-  const unsigned e_res = O.add ? step_base + (unsigned)O.res_stage + 1u : 0u;
-  reduce_duty(P, C, O, sm, cta, G, epoch, fin3, P.slot + (size_t)(epoch & 1u) * P.slot_half, On, Wn, op_no, e_res);
-  if (dbg && tid == 0) dbg[4] = gclock();
+  fifo += n_base + n_ext;
   CSYNC();
   if (tid == 0) {
-    W.valid = 0;
-    sm.cons_done = op_no + 1;
+    sm.cons_ops = oi + 1;
+    sm.cons_gs = gs + 1;
   }
-  return n_base + n_ext;
+  if (dbg && tid == 0) dbg[4] = gclock();
+}
+
+// ---------------------------------------------------------------------------
+// The reducer warp: every stage in order; the units of op stages as their
+// partials arrive, then one arrival on the stage counter once the consumers
+// are done with the stage too.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G, int n_steps, int s0) {
+  const int lane = threadIdx.x & 31;
+  int oi = 0;
+  load_op_async(P, 0, &sm.rop[0]);
+  for (int step = 0; step < n_steps; ++step) {
+    if (lane == 0) SPIN_UNTIL_NS(sm.step_ready >= step + 1, "reducer step", step, 0, 12000000000ull);
+    __syncwarp();
+    __threadfence_block();
+    const ECtl& C = sm.ctl[step & 1];
+    const unsigned step_base = (unsigned)(s0 + step) * (unsigned)P.n_stages;
+    for (int si = 0; si < P.n_stages; ++si) {
+      const int2 st = P.stages[si];
+      const unsigned gs = step_base + (unsigned)si;
+      if (st.x == ST_OP) {
+        asm volatile("cp.async.wait_all;" ::: "memory");   // this op's descriptor (prefetched)
+        __syncwarp();
+        const Op& O = sm.rop[oi & 1];
+        load_op_async(P, (st.y + 1) % (P.n_stages - 2), &sm.rop[(oi + 1) & 1]);
+        // the op's precision decisions, published to the producer (extra
+        // planes) and the consumers; entry oi - kDecRing is free: this warp
+        // only gets here once the consumers have finished op oi - 1
+        const I3 nb = base_bits(O, C);
+        I3 fin = nb;
+        decide_op(P, C, O, nb, fin, cta);
+        if (lane == 0) {
+          sm.dec_fin[oi % kDecRing][0] = fin.v0;
+          sm.dec_fin[oi % kDecRing][1] = fin.v1;
+          sm.dec_fin[oi % kDecRing][2] = fin.v2;
+          __threadfence_block();
+          sm.dec_op = oi + 1;
+        }
+        __syncwarp();
+        if (cta < O.n_units) {
+          const Epi E = op_epi(P, C, O);
+          if (lane == 0) SPIN_UNTIL(stage_done(P, gs), "stage counter (reducer)", gs, 0);
+          __syncwarp();
+          const unsigned epoch = gs + 1u;
+          const unsigned e_res = O.add ? step_base + (unsigned)O.res_stage + 1u : 0u;
+          // the affine epilogue (quant.py:74-78): y = s_in (lo sum x + span 2^-b (S + sum x / 2))
+          for (int u = cta; u < O.n_units; u += G) {
+            if (O.pair) {
+              // unit u: up tile u and gate tile u (runtime.py:366-368)
+              const int half = O.L[0].n_tiles;
+              const int r = u * 32 + lane;
+              float lo0 = 0.f, sp0 = 0.f, lo1 = 0.f, sp1 = 0.f;
+              if (r < O.L[0].rows) {
+                lo0 = __ldg(O.L[0].lo + r); sp0 = __ldg(O.L[0].span + r);
+                lo1 = __ldg(O.L[1].lo + r); sp1 = __ldg(O.L[1].span + r);
+              }
+              const float2 S = tiles_S(P, O, u, fin.v0 - nb.v0, u + half, fin.v1 - nb.v1, epoch);
+              if (r < O.L[0].rows) {
+                const float up = E.scale * (lo0 * E.sx + ldexpf(sp0, -fin.v0) * (S.x + 0.5f * E.sx));
+                const float gt = E.scale * (lo1 * E.sx + ldexpf(sp1, -fin.v1) * (S.y + 0.5f * E.sx));
+                st_tag(O.out + r, up * (gt / (1.0f + expf(-gt))), epoch);        // runtime.py:368
+              }
+            } else {
+              const int li = layer_of(O, u);
+              const Layer& L = O.L[li];
+              const int r = (u - L.tile_off) * 32 + lane;
+              const bool ok = r < L.rows;
+              const int o = L.out_off + r;
+              float lo = 0.f, sp = 0.f, res = 0.f;
+              if (ok) {
+                lo = __ldg(L.lo + r);
+                sp = __ldg(L.span + r);
+              }
+              u64 xr = 0;
+              if (O.add && ok) xr = ld_relaxed64(O.res_in + o);
+              const float S = tiles_S(P, O, u, fin[li] - nb[li], -1, 0, epoch).x;
+              if (ok) {
+                float v = E.scale * (lo * E.sx + ldexpf(sp, -fin[li]) * (S + 0.5f * E.sx));
+                if (O.add) {                                                            // runtime.py:364, 370
+                  if ((unsigned)(xr >> 32) != e_res)
+                    SPIN_UNTIL((xr = ld_relaxed64(O.res_in + o), (unsigned)(xr >> 32) == e_res), "residual", o, e_res);
+                  res = __uint_as_float((unsigned)xr);
+                  v = res + v;
+                }
+                st_tag(O.out + o, v, epoch);
+              }
+            }
+          }
+        }
+        ++oi;
+        u64* dbg = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr;
+        if (dbg && lane == 0) dbg[7] = gclock();
+      }
+      if (lane == 0) {
+        SPIN_UNTIL_NS(sm.cons_gs >= gs + 1, "consumer stage", gs, sm.cons_gs, 12000000000ull);
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" :: "l"(P.bar) : "memory");
+      }
+      __syncwarp();
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1313,24 +1493,29 @@ __device__ __noinline__ void head_stage(const Prog& P, const ECtl& C, Smem& sm, 
   }
 }
 
-// BEGIN: the step's control block, zeroing of the accumulator slots used two
-// steps ahead, x = embed[token] (runtime.py:345) as a tagged vector.
+// BEGIN: the step's control block (-> ctl[step & 1]), zeroing of the
+// accumulator slots used two steps ahead, x = embed[token] (runtime.py:345)
+// as a tagged vector.
 __device__ __forceinline__ void begin_stage(const Prog& P, Smem& sm, int cta, int G, int step, int expect_done,
-                                            unsigned epoch) {
+                                            unsigned gs) {
   const int tid = threadIdx.x;
-  if (tid == 0) SPIN_UNTIL(ld_acq_s32(&P.ctl->n_steps_done) >= expect_done, "step control", expect_done, 0);
+  if (tid == 0) {
+    SPIN_UNTIL(ld_acq_s32(&P.ctl->n_steps_done) >= expect_done, "step control", expect_done, 0);
+    SPIN_UNTIL(stage_done(P, gs), "stage counter", gs, 0);
+  }
   CSYNC();
+  ECtl& Cw = sm.ctl[step & 1];
   {
     const int* src = reinterpret_cast<const int*>(P.ctl);
-    int* dst = reinterpret_cast<int*>(&sm.ctl);
+    int* dst = reinterpret_cast<int*>(&Cw);
     if (tid < (int)(sizeof(ECtl) / 4)) dst[tid] = __ldcg(src + tid);
   }
   CSYNC();
   if (tid == 0) {
     __threadfence_block();
-    sm.step_ready = step + 1;                   // the producer may stream this step
+    sm.step_ready = step + 1;                   // the producer and reducer may run this step
   }
-  const ECtl& C = sm.ctl;
+  const ECtl& C = Cw;
   {
     long long* a = acc_slot(P, (C.n_steps_done + 2) & (kCurSlots - 1));
     long long* z = acc_slot(P, kCurSlots + ((C.rot + 1) & (kPrevSlots - 1)));
@@ -1338,84 +1523,73 @@ __device__ __forceinline__ void begin_stage(const Prog& P, Smem& sm, int cta, in
     for (int i = cta * NT + tid; i < P.acc_stride; i += G * NT) { a[i] = 0; z[i] = 0; }
     for (int i = cta * NT + tid; i < P.n_inst * 3; i += G * NT) vs[(size_t)i * kStatSpread] = 0;
   }
-  for (int i = cta * NT + tid; i < P.d; i += G * NT) st_tag(P.xe + i, __ldg(P.embed + (size_t)C.token * P.d + i), epoch);
+  for (int i = cta * NT + tid; i < P.d; i += G * NT) st_tag(P.xe + i, __ldg(P.embed + (size_t)C.token * P.d + i), gs + 1u);
 }
 
 // ---------------------------------------------------------------------------
 // The kernel: n_steps decode steps (greedy token feedback on the device when
 // n_steps > 1; the host writes the token / mode of a single step).
 // ---------------------------------------------------------------------------
-extern "C" __global__ void __launch_bounds__(NTB, 1) engine_kernel(const Prog Pk, int n_steps) {
+extern "C" __global__ void __maxnreg__(168) engine_kernel(const Prog Pk, int n_steps) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-  const int cta = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
+  const int cta = blockIdx.x, G = gridDim.x, tid = threadIdx.x, warp = tid >> 5;
   if (tid == 0) {
     sm.prog = Pk;
-    sm.work[0].valid = 0;
-    sm.work[1].valid = 0;
     sm.dec_op = 0;
-    sm.cons_done = 0;
-    sm.runs_op = -1;
+    sm.cons_ops = 0;
+    sm.cons_gs = 0;
     sm.step_ready = 0;
     // ring slots: below the LUT (after Smem) and above its zero row
     const uint32_t base = smem_u32(smem_raw);
-    uint32_t lo = (base + (uint32_t)sizeof(Smem) + 1023u) & ~1023u;
+    uint32_t lo = (base + (uint32_t)sizeof(Smem) + 127u) & ~127u;
     int n = 0;
-    while (lo + kSlotBytes <= kLut && n < kMaxSlots) { sm.slot_off[n++] = lo - base; lo += kSlotBytes; }
+    while (lo + kItemBytes <= kLut && n < kMaxSlots) { sm.slot_off[n++] = lo - base; lo += kItemBytes; }
     uint32_t hi = kLut + kLutBytes;
-    while (hi + kSlotBytes <= base + (uint32_t)Pk.smem_dyn && n < kMaxSlots) {
+    while (hi + kItemBytes <= base + (uint32_t)Pk.smem_dyn && n < kMaxSlots) {
       sm.slot_off[n++] = hi - base;
-      hi += kSlotBytes;
+      hi += kItemBytes;
     }
     if (n < kMaxSlots) __trap();        // host sizing guarantees kMaxSlots ring slots
     for (int q = 0; q < kMaxSlots; ++q) {
       mbar_init(&sm.full[q], 1);
-      mbar_init(&sm.empty[q], kSlotTiles);
+      mbar_init(&sm.empty[q], 1);
       sm.seq[q] = -1;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const Prog& P = sm.prog;
-  if (tid >= NT) {                        // TMA producer warp
-    producer(P, sm, cta, G, n_steps);
+  const int s0 = __ldcg(&P.ctl->n_steps_done);   // steps completed before this launch
+  if (warp == kProdWarp) {
+    producer(P, sm, cta, G, n_steps, s0);
+    return;
+  }
+  if (warp == kRedWarp) {
+    reducer(P, sm, cta, G, n_steps, s0);
     return;
   }
   float* lut = reinterpret_cast<float*>(smem_raw + (kLut - smem_u32(smem_raw)));
-  const int s0 = __ldcg(&P.ctl->n_steps_done);   // steps completed before this launch
-  int wi = 0, op_no = 0, j_op = 0;
+  const int n_ops = P.n_stages - 2;
+  if (warp == 0) load_op(P, 0, cta, &sm.cop[0], &sm.cw[0], sm.ctask[0]);
+  int oi = 0, fifo = 0;
   for (int step = 0; step < n_steps; ++step) {
     const unsigned step_base = (unsigned)(s0 + step) * (unsigned)P.n_stages;
     for (int si = 0; si < P.n_stages; ++si) {
       const int2 st = P.stages[si];
-      const unsigned epoch = step_base + (unsigned)si + 1u;
+      const unsigned gs = step_base + (unsigned)si;
       u64* dbg = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr;
       if (st.x == ST_OP) {
-        int nsi = si + 1;
-        while (nsi < P.n_stages && P.stages[nsi].x != ST_OP) ++nsi;
-        const bool has_next = nsi < P.n_stages;
-        if (sm.work[wi].valid == 0) {
-          CSYNC();
-          const int nw4 = (int)(sizeof(Op) / 16);
-          const int4* src = reinterpret_cast<const int4*>(P.ops + st.y);
-          int4* dst = reinterpret_cast<int4*>(&sm.op[wi]);
-          for (int q = tid; q < nw4; q += NT) dst[q] = __ldg(src + q);
-          CSYNC();
-        }
-        j_op += op_stage(P, sm.ctl, sm.op[wi], sm.work[wi], has_next ? &sm.op[wi ^ 1] : nullptr, &sm.work[wi ^ 1],
-                         has_next ? P.ops + P.stages[nsi].y : nullptr, sm, cta, G, epoch, step_base, dbg, op_no,
-                         j_op);
-        ++op_no;
-        wi ^= 1;
-      } else if (st.x == ST_BEGIN) {
-        if (dbg && tid == 0) dbg[0] = gclock();
-        begin_stage(P, sm, cta, G, step, s0 + step, epoch);
+        cons_op(P, sm, oi, st.y, n_ops, si, gs, step_base, cta, G, fifo, sm.ctl[step & 1], dbg);
+        ++oi;
       } else {
         if (dbg && tid == 0) dbg[0] = gclock();
-        head_stage(P, sm.ctl, sm, lut, cta, G, step_base + (unsigned)P.final_stage + 1u);
+        if (st.x == ST_BEGIN) begin_stage(P, sm, cta, G, step, s0 + step, gs);
+        else head_stage(P, sm.ctl[step & 1], sm, lut, cta, G, step_base + (unsigned)P.final_stage + 1u);
+        CSYNC();
+        if (tid == 0) sm.cons_gs = gs + 1;
+        if (dbg && tid == 0) dbg[4] = gclock();
       }
-      if (dbg && tid == 0) dbg[7] = gclock();
-      stage_arrive(P);
     }
   }
 }

@@ -44,8 +44,14 @@ def trace_arrays(records, ids):
     return bits, est
 
 
-def decision_mismatches(bits_dev, bits_ref, est_ref, T, eps):
-    """Indices of decisions that differ although |est_ref - T| > eps*|T|."""
+def decision_mismatches(bits_dev, bits_ref, est_ref, T, eps, until_first=True):
+    """Decisions that differ although |est_ref - T| > eps*|T|.
+
+    Scanned in execution order (step-major, layers in block/kind order). With
+    until_first (the free-run rule of SURVEY 8c) the scan stops at the first
+    differing decision: later layers see a different input from there on, so
+    only that first one is held to the eps rule.
+    """
     bad = []
     for s in range(bits_ref.shape[0]):
         for i in range(bits_ref.shape[1]):
@@ -53,4 +59,6 @@ def decision_mismatches(bits_dev, bits_ref, est_ref, T, eps):
                 e, t = est_ref[s, i], T[i]
                 if not (np.isfinite(e) and np.isfinite(t) and abs(e - t) <= eps * abs(t)):
                     bad.append((s, i, bits_dev[s, i], bits_ref[s, i], e, t))
+                if until_first:
+                    return bad
     return bad

@@ -65,7 +65,7 @@ def test_report_numbers_on_device(report_setup, golden_summary, name):
         np.testing.assert_allclose(est_d, est_o, rtol=1e-4, equal_nan=True)
         implied = np.where(np.isnan(est_d), bits_o, np.where(est_d > T, [plan.layers[l].pair[1] for l in ids],
                                                                [plan.layers[l].pair[0] for l in ids]))
-        assert not decision_mismatches(implied, bits_o, est_o, T, EPS_DECISION["f32"])
+        assert not decision_mismatches(implied, bits_o, est_o, T, EPS_DECISION["f32"], until_first=False)
     exp = golden_summary["plans"][name]
     assert float(np.exp(np.mean(losses))) == pytest.approx(exp["perplexity"], rel=1e-6)
     assert float(np.mean(effs)) == pytest.approx(exp["effective_bits"], abs=1e-12)

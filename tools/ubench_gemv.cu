@@ -483,8 +483,15 @@ int main() {
   // large shapes: steady-state streaming rate (startup amortised)
   run_core<512, 4, 0>("big", 229376, 4096, 3, 4, 1, nsm, reps);
   run_core<512, 4, 1>("big", 229376, 4096, 3, 4, 1, nsm, reps);
+  run_tma<384, 9, 1>("big", 229376, 4096, 3, 4, 1, reps);
+  run_tma<448, 9, 1>("big", 229376, 4096, 3, 4, 1, reps);
   run_tma<544, 9, 1>("big", 229376, 4096, 3, 4, 1, reps);
   run_tma<672, 9, 1>("big", 229376, 4096, 3, 4, 1, reps);
   run_tma<800, 9, 1>("big", 229376, 4096, 3, 4, 1, reps);
+  // one up|gate-sized op (2 x 14336 rows, 3 planes) and a down-sized one, 8 copies (cold in L2)
+  run_tma<384, 9, 1>("upgate", 28672, 4096, 3, 4, 8, reps);
+  run_tma<544, 9, 1>("upgate", 28672, 4096, 3, 4, 8, reps);
+  run_tma<384, 9, 1>("down", 4096, 14336, 3, 4, 8, reps);
+  run_tma<544, 9, 1>("down", 4096, 14336, 3, 4, 8, reps);
   return 0;
 }
