@@ -249,6 +249,7 @@ struct dpq_session {
   unsigned long long* eng_dbg = nullptr;
   std::vector<unsigned long long*> eng_vec;   // tagged vectors (reset to "no epoch")
   std::vector<size_t> eng_vec_len;
+  size_t eng_fpart_len = 0;         // tagged estimator-set words (engine)
 };
 
 // ---------------------------------------------------------------------------
@@ -630,17 +631,18 @@ extern "C" int dpq_plan_create(dpq_store* s, int n_layers, const dpq_sel_desc* s
     }
     p->gt_fb.push_back(0);
     if (S.sentinel == 0 && d.est_kind == EST_PROJECTION) {
-      // fixed-point fraction bits of the engine's G.x accumulators:
-      // |G_k . x| <= maxl1 * 2^16 must fit in int64 after scaling by 2^fb
-      // (larger inputs raise the engine's range flag, DPQ_ERR_RANGE)
+      // fixed-point fraction bits of the engine's packed G.x words: a window
+      // partial |G_k[w] . x[w]| <= maxl1 * 2^16 must stay below 2^46 (< the
+      // 2^47 bias) after scaling by 2^fb (larger inputs raise the engine's
+      // range flag, DPQ_ERR_RANGE)
       double maxl1 = 0.0;
       for (int r = 0; r < d.k; ++r) {
         double a = 0.0;
         for (int c = 0; c < L.cols; ++c) a += std::fabs(d.G[(size_t)r * L.cols + c]);
         maxl1 = std::max(maxl1, a);
       }
-      int fb = 62 - (int)std::ceil(std::log2(std::max(maxl1, 1e-30) * 65536.0));
-      p->gt_fb.back() = std::min(52, std::max(8, fb));
+      int fb = 46 - (int)std::ceil(std::log2(std::max(maxl1, 1e-30) * 65536.0));
+      p->gt_fb.back() = std::min(52, std::max(-16, fb));
     }
     if (S.sentinel == 0 && d.prev_residual) p->any_prev = 1;
     p->sel.push_back(S);

@@ -55,13 +55,16 @@ constexpr int NTB = NT + 64;
 constexpr int kItemBytes = 2048;   // one (tile, plane) item = kTileBytes
 constexpr int kMaxSlots = 64;      // ring slots (2 KB); the host checks they fit
 constexpr int kDecRing = 4;        // op decision entries in flight
-constexpr int kCurSlots = 4;       // accumulator slots of the current step (step % 4)
-constexpr int kPrevSlots = 4;      // previous-step slots (rotation % 4)
-constexpr int kAccSlots = kCurSlots + kPrevSlots;
-constexpr int kStatSpread = 16;    // statistics words: one 128-byte line each
 constexpr int kDbgRec = 16;        // debug stamps per (stage, CTA)
-constexpr double kFxSum = 4294967296.0;   // 2^32: sum x
-constexpr double kFxSq = 16777216.0;      // 2^24: sum x^2
+constexpr unsigned kPrevTag = 0x80000000u;   // previous-step sum x^2 words: tag = kPrevTag | rotation
+constexpr int kCurSlots = 4;       // estimator-set slots of the current step (step % 4)
+constexpr int kPrevSlots = 4;      // previous-step slots (rotation % 4)
+constexpr int kSetSlots = kCurSlots + kPrevSlots;
+// Packed G.x words: each window adds (1 << 56) + (v + 2^47), v = G_r[w] . x[w]
+// at 2^fb with |v| < 2^47, so one relaxed red.add carries value and count
+// (no release fence, no second atomic): count = word >> 56 (<= 255 windows).
+constexpr int kCntShift = 56;
+constexpr long long kFxBias = 1ll << 47;
 constexpr uint32_t kLut = 0x20000;        // the window LUT (absolute shared address)
 
 enum { ST_BEGIN = 0, ST_OP = 1, ST_HEAD = 3 };
@@ -82,11 +85,11 @@ struct Layer {
   int est;                 // EST_NONE / EST_LINEAR / EST_PROJECTION
   int src;                 // SRC_*
   int k;                   // projection rank (0: linear)
-  int acc;                 // accumulator set offset in a slot: [k values][sum x^2][count]
-  int cnt_expect;          // count of a complete set: n_win(cols) * (k + 1)
+  double fbscale;          // 2^-fb of the packed G.x words
+  int set;                 // estimator set in each Prog.fpart slot: [k packed G.x words][n_win sum x^2 words]
+  int feed_stage;          // stage (index in the step) whose consumers write the set
   int trace;               // trace column
   double T, slope, intercept;
-  double fbscale;          // 2^-fb of the set's G.x values
 };
 
 // Static work of one CTA in one op (host-built): window w (CTA j of the m
@@ -128,10 +131,10 @@ struct Feed {
   const void* G;
   const float* gscale;
   int dtype, k, row0;      // row0: first row of this feed in the instance's row list
-  int acc;
+  int set;                 // the layer's set in Prog.fpart
   int kind;                // FEED_*
   int pad;
-  double fxscale;          // 2^fb
+  double fxscale;          // 2^fb of the packed G.x words
 };
 
 struct ECtl {
@@ -171,9 +174,12 @@ struct Prog {
   u64* slot;               // [2][slot_half] tagged (tile, window) base partial sums
   u64* slotx;              // [2][slot_half] tagged extra-plane partial sums
   long long slot_half;
-  long long* acc;          // [kAccSlots][acc_stride]
-  int acc_stride;
-  long long* vstat;        // [kCurSlots][n_inst][3 (sum, sumsq, count)][kStatSpread]
+  u64* fpart;              // estimator sets [kSetSlots][set_stride]: per estimating layer k packed
+                           // G.x words (kCntShift) + n_win tagged sum x[w]^2 words; slots
+                           // step % 4 (current step), kCurSlots + rot % 4 (previous-step feeds)
+  long long set_stride;
+  u64* istat;              // [n_inst][istat_win][2] tagged window sums (sum x, sum x^2)
+  int istat_win;
   u64* bar;                // stage arrivals (one per CTA and stage)
   unsigned* head_cnt;
   unsigned* err;           // sticky error flags (ERR_RANGE: fixed-point range exceeded)
@@ -268,12 +274,6 @@ __device__ __forceinline__ T wsum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
-}
-// fixed point with a range check (sticky error flag instead of a silent wrap)
-__device__ __forceinline__ long long fx(double v, double scale, unsigned* err) {
-  const double s = v * scale;
-  if (!(fabs(s) < 4.0e18)) { atomicOr(err, (unsigned)ERR_RANGE); return 0; }
-  return llrint(s);
 }
 // 1/sqrt(x) in double without library slow paths (MUFU seed + two Newton steps).
 __device__ __forceinline__ double rsqrt_d(double x) {
@@ -488,26 +488,21 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 }
 
 // ---------------------------------------------------------------------------
-// Estimator accumulators (fixed point, per step slot) and statistics
+// Estimator sets and input statistics: tagged per-window partials (plain
+// 64-bit stores, no atomics, no fences); readers sum the windows in fixed
+// order, so every CTA gets the same value.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ long long* acc_slot(const Prog& P, int slot) { return P.acc + (size_t)slot * P.acc_stride; }
-__device__ __forceinline__ long long* stat_words(const Prog& P, int cur, int inst) {
-  return P.vstat + ((size_t)cur * P.n_inst + inst) * 3 * kStatSpread;
+__device__ __forceinline__ u64* istat_words(const Prog& P, int inst, int w) {
+  return P.istat + ((size_t)inst * P.istat_win + w) * 2;
 }
 
 // Feed rows of the op's input window (consumer prologue). Rows of all feeds
 // of the instance are numbered 0..feed_rows-1; CTA j of the window's m takes
 // rows j, j + m, ...; its i-th row goes to warp kFeedW0 + i % kFeedWarps.
 // Row r of feed F: partial G_F[w][r] . x[w] in fp32 lanes + double warp sum,
-// fixed point at 2^fb, added to the set's accumulator, then a release count.
+// stored as the tagged float word (w, r) of the layer's set.
 constexpr int kFeedW0 = 0, kFeedWarps = NCW - 1; // warps 0..NCW-2 (then the LUT build, all warps)
 constexpr int kStatW = NCW - 1;                  // statistics warp
-
-struct FeedSel {      // the feed a row belongs to and where it accumulates
-  const Feed* F;
-  long long* acc;
-  int r;
-};
 
 __device__ __forceinline__ bool feed_active(const Feed& F, const ECtl& C) {
   const bool dyn = C.mode == MODE_DYNAMIC;
@@ -515,9 +510,15 @@ __device__ __forceinline__ bool feed_active(const Feed& F, const ECtl& C) {
   if (F.kind == FEED_CURFB) return dyn && !C.has_prev;
   return dyn;
 }
-__device__ __forceinline__ long long* feed_acc(const Prog& P, const ECtl& C, const Feed& F) {
+// Slot of a feed's words: previous-step feeds kCurSlots + rot % 4, current-step
+// feeds step % 4 (zeroed two steps ahead in BEGIN); tag of its sum x^2 words:
+// the rotation (previous step) or the stage epoch.
+__device__ __forceinline__ u64* feed_words(const Prog& P, const ECtl& C, const Feed& F) {
   const int slot = F.kind == FEED_PREV ? kCurSlots + (C.rot & (kPrevSlots - 1)) : (C.n_steps_done & (kCurSlots - 1));
-  return acc_slot(P, slot) + F.acc;
+  return P.fpart + (size_t)slot * P.set_stride + F.set;
+}
+__device__ __forceinline__ unsigned feed_tag(const ECtl& C, const Feed& F, unsigned epoch) {
+  return F.kind == FEED_PREV ? (kPrevTag | ((unsigned)C.rot & 0x7fffffffu)) : epoch;
 }
 
 // G row r of feed F in window w, lanes 16 columns each: raw data (f16: 2
@@ -623,18 +624,22 @@ __device__ __forceinline__ void feed_prefetch(const Prog& P, const ECtl& C, cons
   }
 }
 
-// Row partial -> fixed point at 2^fb into the set's accumulator, then a release count.
+// Row partial -> packed fixed point (value + count) into word r of the set:
+// one relaxed red.add; |v| 2^fb >= 2^47 raises the sticky range flag.
 __device__ __forceinline__ void feed_add(const Prog& P, const ECtl& C, const Feed& F, int r, double v) {
   if ((threadIdx.x & 31) == 0) {
-    long long* a = feed_acc(P, C, F);
-    red_add64(a + r, fx(v, F.fxscale, P.err));
-    red_rel_add64(a + F.k + 1, 1);          // count (release: the value above is visible first)
+    const double s = v * F.fxscale;
+    long long f = 0;
+    if (fabs(s) < (double)kFxBias) f = llrint(s);
+    else atomicOr(P.err, (unsigned)ERR_RANGE);
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(feed_words(P, C, F) + r),
+                 "l"((1ull << kCntShift) + (u64)(f + kFxBias)) : "memory");
   }
 }
 
 // Feeds + statistics of the op's input window, once it is staged in xw.
 __device__ __forceinline__ void feed_finish(const Prog& P, const ECtl& C, const Op& O, const CtaWork& W,
-                                            const FeedPre& fp, const float* xw) {
+                                            const FeedPre& fp, const float* xw, unsigned epoch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = W.j, m = W.m;
   if (warp >= kFeedW0 && warp < kFeedW0 + kFeedWarps) {
@@ -663,18 +668,14 @@ __device__ __forceinline__ void feed_finish(const Prog& P, const ECtl& C, const 
     s = wsum(s);
     q = wsum(q);
     if (lane == 0) {
-      long long* st = stat_words(P, C.n_steps_done & (kCurSlots - 1), O.inst);
-      red_add64(st, fx(s, kFxSum, P.err));
-      red_add64(st + kStatSpread, fx(q, kFxSq, P.err));
-      red_rel_add64(st + 2 * kStatSpread, 1);
+      u64* st = istat_words(P, O.inst, W.w);
+      st_tag(st, (float)s, epoch);
+      st_tag(st + 1, (float)q, epoch);
     }
-    const long long qf = fx(q, kFxSq, P.err);
     for (int f = P.feed_begin[O.inst] + lane; f < P.feed_begin[O.inst + 1]; f += 32) {
       const Feed& F = P.feeds[f];
       if (!feed_active(F, C)) continue;
-      long long* a = feed_acc(P, C, F);
-      red_add64(a + F.k, qf);
-      red_rel_add64(a + F.k + 1, 1);
+      st_tag(feed_words(P, C, F) + F.k + W.w, (float)q, feed_tag(C, F, epoch));
     }
   }
 }
@@ -1033,12 +1034,22 @@ __device__ __forceinline__ float2 tiles_S(const Prog& P, const Op& O, int t0, in
 
 struct Epi { float scale, sx; };
 
-// op input statistics (sum x, sum x^2) once every window has added them
-__device__ __forceinline__ Epi op_epi(const Prog& P, const ECtl& C, const Op& O) {
-  const long long* st = stat_words(P, C.n_steps_done & (kCurSlots - 1), O.inst);
-  SPIN_UNTIL(ld_acq_s64(st + 2 * kStatSpread) >= O.n_win, "statistics", O.inst, 0);
-  const double s = (double)__ldcg(st) * (1.0 / kFxSum);
-  const double q = (double)__ldcg(st + kStatSpread) * (1.0 / kFxSq);
+// op input statistics (sum x, sum x^2): the windows' tagged sums (lane =
+// window), summed in a fixed shuffle tree (identical on every CTA).
+__device__ __forceinline__ Epi op_epi(const Prog& P, const Op& O, unsigned epoch) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0, q = 0.0;
+  for (int w0 = 0; w0 < O.n_win; w0 += 32) {
+    const int w = w0 + lane;
+    if (w < O.n_win) {
+      uint4 v;
+      SPIN_UNTIL((v = ld_tag2(istat_words(P, O.inst, w)), v.y == epoch && v.w == epoch), "statistics", O.inst, w);
+      s += (double)__uint_as_float(v.x);
+      q += (double)__uint_as_float(v.z);
+    }
+  }
+  s = wsum(s);
+  q = wsum(q);
   Epi e;
   e.sx = (float)s;
   e.scale = O.rms ? (float)rsqrt_d(q / (double)O.cols + (double)P.eps) : 1.f;
@@ -1051,63 +1062,84 @@ __device__ __forceinline__ Epi op_epi(const Prog& P, const ECtl& C, const Op& O)
 // the same decisions without another exchange).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op& O, const I3& nb, I3& fin,
-                                          int cta) {
+                                          int cta, unsigned step_base) {
   const int lane = threadIdx.x & 31;
   const bool dyn = C.mode == MODE_DYNAMIC;
-  // every estimating layer's accumulator set: count complete, then all its
-  // words loaded together (one round trip for the op)
-  const long long* acc[kMaxOpLayers] = {nullptr, nullptr, nullptr};
-  bool any = false;
+  // every estimating layer's words in one poll: lane holds packed G.x words
+  // r = lane + 32 q and the sum x^2 word of window lane (+ 32); complete when
+  // every packed count is n_win and every sum x^2 word carries its tag
+  constexpr int NQ = kMaxK / 32;
+  const u64* base[kMaxOpLayers] = {nullptr, nullptr, nullptr};
+  unsigned tag[kMaxOpLayers] = {0u, 0u, 0u};
 #pragma unroll
   for (int li = 0; li < kMaxOpLayers; ++li) {
     if (li >= O.n_layers) break;
     const Layer& L = O.L[li];
-    if (dyn && L.sentinel == 0 && L.est != EST_NONE) {
-      const int slot = (L.src == SRC_PREV_STEP && C.has_prev) ? kCurSlots + ((C.rot - 1) & (kPrevSlots - 1))
-                                                              : (C.n_steps_done & (kCurSlots - 1));
-      acc[li] = acc_slot(P, slot) + L.acc;
-      any = true;
-    }
+    if (!(dyn && L.sentinel == 0 && L.est != EST_NONE)) continue;
+    const bool prev = L.src == SRC_PREV_STEP && C.has_prev;
+    const int slot = prev ? kCurSlots + ((C.rot - 1) & (kPrevSlots - 1)) : (C.n_steps_done & (kCurSlots - 1));
+    base[li] = P.fpart + (size_t)slot * P.set_stride + L.set;
+    tag[li] = prev ? (kPrevTag | ((unsigned)(C.rot - 1) & 0x7fffffffu)) : step_base + (unsigned)L.feed_stage + 1u;
   }
-  if (any) {
-    const long long* am = lane == 0 ? acc[0] : lane == 1 ? acc[1] : acc[2];
-    const bool mine = lane < O.n_layers && am != nullptr;
-    const Layer& Lm = O.L[min(lane, O.n_layers - 1)];
+  u64 g[kMaxOpLayers][NQ], sw[kMaxOpLayers][2];
+  {
     bool ok;
-    SPIN_UNTIL((ok = __all_sync(0xffffffffu, !mine || ld_acq_s64(am + Lm.k + 1) >= Lm.cnt_expect)), "estimator feeds",
-               O.L[0].trace, O.n_layers);
+    unsigned n_ = 0;
+    u64 t0_ = 0;
+    do {
+      ok = true;
+#pragma unroll
+      for (int li = 0; li < kMaxOpLayers; ++li) {
+        const int k = O.L[li].k;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int r = q * 32 + lane;
+          g[li][q] = (base[li] && r < k) ? ld_relaxed64(base[li] + r) : ((u64)O.n_win << kCntShift);
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int w = q * 32 + lane;
+          sw[li][q] = (base[li] && w < O.n_win) ? ld_relaxed64(base[li] + k + w) : ((u64)tag[li] << 32);
+        }
+      }
+#pragma unroll
+      for (int li = 0; li < kMaxOpLayers; ++li) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) ok &= (int)(g[li][q] >> kCntShift) == O.n_win;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) ok &= (unsigned)(sw[li][q] >> 32) == tag[li];
+      }
+      if ((++n_ & 1023u) == 0) {
+        const u64 t_ = gclock();
+        if (t0_ == 0) t0_ = t_;
+        else if (t_ - t0_ > 4000000000ull) hang("estimator feeds", O.L[0].trace, O.n_layers);
+      }
+    } while (!__all_sync(0xffffffffu, ok));
   }
-  long long v[kMaxOpLayers][kMaxK / 32 + 1];
-#pragma unroll
-  for (int li = 0; li < kMaxOpLayers; ++li)
-#pragma unroll
-    for (int q = 0; q <= kMaxK / 32; ++q) {
-      const int i = q * 32 + lane;
-      v[li][q] = 0;
-      if (acc[li] && i <= O.L[li].k) v[li][q] = __ldcg(acc[li] + i);   // G.x values, then sum x^2 at i = k
-    }
 #pragma unroll
   for (int li = 0; li < kMaxOpLayers; ++li) {
     if (li >= O.n_layers) break;
     const Layer& L = O.L[li];
     int bit = nb[li];
     double est = CUDART_NAN;
-    if (acc[li]) {
-      double q = 0.0;
-      long long sqw = 0;
+    const bool has = base[li] != nullptr;
+    if (has) {
+      double q = 0.0, sq = 0.0;
 #pragma unroll
-      for (int qq = 0; qq <= kMaxK / 32; ++qq) {
-        const int i = qq * 32 + lane;
-        if (i < L.k) {
-          const double g = (double)v[li][qq] * L.fbscale;
-          q += g * g;
-        } else if (i == L.k) {
-          sqw = v[li][qq];
+      for (int qq = 0; qq < NQ; ++qq) {
+        const int r = qq * 32 + lane;
+        if (r < L.k) {
+          const long long c = (long long)(g[li][qq] >> kCntShift);
+          const long long v = (long long)(g[li][qq] & ((1ull << kCntShift) - 1)) - c * kFxBias;
+          const double gv = (double)v * L.fbscale;
+          q += gv * gv;
         }
       }
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq)
+        if (qq * 32 + lane < O.n_win) sq += (double)__uint_as_float((unsigned)sw[li][qq]);
       q = wsum(q);
-      sqw = __shfl_sync(0xffffffffu, sqw, L.k & 31);
-      const double sq = (double)sqw * (1.0 / kFxSq);
+      sq = wsum(sq);
       const double sc = O.rms ? rsqrt_d(sq / (double)O.cols + (double)P.eps) : 1.0;
       if (L.est == EST_PROJECTION) est = q > 0.0 ? sc * q * rsqrt_d(q) : 0.0;                 // estimator.py:56-57
       else est = L.slope * (sq > 0.0 ? sc * sq * rsqrt_d(sq) : 0.0) + L.intercept;           // estimator.py:41-42
@@ -1117,7 +1149,7 @@ __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op
     if (lane == 0 && dyn && cta == 0 && L.trace >= 0 && P.n_trace > 0 && C.trace_step < P.max_steps) {
       const size_t o = (size_t)C.trace_step * P.n_trace + L.trace;
       P.tr_bits[o] = (signed char)bit;
-      P.tr_est[o] = acc[li] ? (float)est : CUDART_NAN_F;
+      P.tr_est[o] = has ? (float)est : CUDART_NAN_F;
     }
   }
   __syncwarp();
@@ -1273,11 +1305,12 @@ __device__ __forceinline__ void cons_op(const Prog& P, Smem& sm, int oi, int op_
   }
   CSYNC();
   if (dbg && tid == 0) dbg[1] = gclock();
-  // estimator feeds + statistics of the window, then its LUT (all warps)
-  feed_finish(P, C, O, W, fp, sm.xw);
+  // the window's LUT (all warps), then its estimator feeds + statistics
+  // (tagged stores, off the CTA's critical path: no CSYNC after them)
   lut_build(lut, sm.xw);
   CSYNC();
   if (dbg && tid == 0) dbg[2] = gclock();
+  feed_finish(P, C, O, W, fp, sm.xw, gs + 1u);
   const I3 nb = base_bits(O, C);
   const uint32_t lanereg = kLut | ((uint32_t)lane * 4u);
   const size_t par = (size_t)(gs & 1u) * P.slot_half + (size_t)W.w * O.n_tiles * 32 + lane;
@@ -1344,7 +1377,7 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
         // only gets here once the consumers have finished op oi - 1
         const I3 nb = base_bits(O, C);
         I3 fin = nb;
-        decide_op(P, C, O, nb, fin, cta);
+        decide_op(P, C, O, nb, fin, cta, step_base);
         if (lane == 0) {
           sm.dec_fin[oi % kDecRing][0] = fin.v0;
           sm.dec_fin[oi % kDecRing][1] = fin.v1;
@@ -1354,7 +1387,7 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
         }
         __syncwarp();
         if (cta < O.n_units) {
-          const Epi E = op_epi(P, C, O);
+          const Epi E = op_epi(P, O, gs + 1u);
           if (lane == 0) SPIN_UNTIL(stage_done(P, gs), "stage counter (reducer)", gs, 0);
           __syncwarp();
           const unsigned epoch = gs + 1u;
@@ -1516,12 +1549,10 @@ __device__ __forceinline__ void begin_stage(const Prog& P, Smem& sm, int cta, in
     sm.step_ready = step + 1;                   // the producer and reducer may run this step
   }
   const ECtl& C = Cw;
-  {
-    long long* a = acc_slot(P, (C.n_steps_done + 2) & (kCurSlots - 1));
-    long long* z = acc_slot(P, kCurSlots + ((C.rot + 1) & (kPrevSlots - 1)));
-    long long* vs = stat_words(P, (C.n_steps_done + 2) & (kCurSlots - 1), 0);
-    for (int i = cta * NT + tid; i < P.acc_stride; i += G * NT) { a[i] = 0; z[i] = 0; }
-    for (int i = cta * NT + tid; i < P.n_inst * 3; i += G * NT) vs[(size_t)i * kStatSpread] = 0;
+  {  // estimator-set slots used two steps / rotations ahead
+    u64* a = P.fpart + (size_t)((C.n_steps_done + 2) & (kCurSlots - 1)) * P.set_stride;
+    u64* z = P.fpart + (size_t)(kCurSlots + ((C.rot + 1) & (kPrevSlots - 1))) * P.set_stride;
+    for (long long i = cta * NT + tid; i < P.set_stride; i += G * NT) { a[i] = 0; z[i] = 0; }
   }
   for (int i = cta * NT + tid; i < P.d; i += G * NT) st_tag(P.xe + i, __ldg(P.embed + (size_t)C.token * P.d + i), gs + 1u);
 }

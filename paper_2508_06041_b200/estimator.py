@@ -8,9 +8,11 @@ Types mirror the reference: ``LinearEstimator`` (estimator.py:35-46),
 decode step the same estimators are evaluated by the fused op kernel
 (libdpq_b200: op_kernel P1 + decider), never here.
 
-The offline half (threshold translation, calibration, projection build) is
-out of scope for the hot path; ``build_projection`` and ``translate_threshold``
-are provided for synthetic plan construction (tools, bench).
+The offline half (calibration, the fitter) is out of scope for the hot path.
+``translate_threshold`` (estimator.py:106-121, returns a ``ThresholdEntry``)
+and ``build_projection`` (estimator.py:190-200, returns a
+``ProjectionEstimator``) keep the reference signatures; the product
+``A @ dW`` is formed on the GPU from device-dequantized planes.
 """
 
 from __future__ import annotations
@@ -154,11 +156,20 @@ def empirical_quantile(sorted_vals, r: float) -> float:
     return float(sorted_vals[idx])
 
 
-def translate_threshold(err_list, p: float, l: int):
+@dataclass
+class ThresholdEntry:
+    """estimator.py:86-91."""
+    layer: object
+    T: float                    # may be +/- inf
+    r_quantile: float
+    pair: tuple
+
+
+def translate_threshold(err_list, p: float, l: int) -> ThresholdEntry:
     """Threshold of a (l, l+1) layer from an error list (estimator.py:106-121):
     r = 1 - (p - l); r >= 1 -> +inf (always low), r <= 0 -> -inf (always
-    high), else the empirical r-quantile. Returns (T, r). The list is used in
-    the order given, like the reference (callers pass it sorted)."""
+    high), else the empirical r-quantile. The list is used in the order
+    given, like the reference (callers pass it sorted)."""
     err_list = np.asarray(err_list, dtype=np.float64)
     if len(err_list) == 0:
         raise ValueError("empty error list")
@@ -166,14 +177,16 @@ def translate_threshold(err_list, p: float, l: int):
         raise ValueError(f"p={p} outside [{l}, {l + 1}]")
     r = 1.0 - (p - l)
     if r >= 1.0:
-        return math.inf, r
-    if r <= 0.0:
-        return -math.inf, r
-    return empirical_quantile(err_list, r), r
+        T = math.inf
+    elif r <= 0.0:
+        T = -math.inf
+    else:
+        T = empirical_quantile(err_list, r)
+    return ThresholdEntry(None, T, r, (l, l + 1))
 
 
-def build_projection(delta_rows_fn, rows: int, k: int, seed: int, A=None) -> np.ndarray:
-    """G = A @ dW with A ~ N(0,1)/sqrt(k) (estimator.py:190-200). ``delta_rows_fn``
+def projection_matrix(delta_rows_fn, rows: int, k: int, seed: int, A=None) -> np.ndarray:
+    """G = A @ dW with A ~ N(0,1)/sqrt(k) (estimator.py:196-200). ``delta_rows_fn``
     returns dW as a float64 (rows, cols) array or a CUDA tensor; the product
     is formed on the GPU for large layers."""
     if k < 1:
@@ -186,3 +199,19 @@ def build_projection(delta_rows_fn, rows: int, k: int, seed: int, A=None) -> np.
         At = torch.as_tensor(A, device=dW.device, dtype=dW.dtype)
         return (At @ dW).double().cpu().numpy()
     return A @ dW
+
+
+def build_projection(layer: Q.QuantizedLayer, l: int, h: int, k: int, seed: int,
+                     A=None) -> ProjectionEstimator:
+    """estimator.py:190-200: G = A @ (W_h - W_l), A seeded N(0,1)/sqrt(k);
+    dW is dequantized on the device in fp64 (quant.py:83-92)."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    ds, i = layer.device_handle()
+
+    def dW():
+        d = ds.dequantize(i, h)
+        d -= ds.dequantize(i, l)
+        return d
+
+    return ProjectionEstimator(projection_matrix(dW, layer.shape[0], k, seed, A), k, seed)

@@ -117,7 +117,6 @@ def calibrate_thresholds(weights, store, plan, tokens, high_rate: dict | float =
     dyn = [lid for lid, pl in plan.layers.items() if pl.estimator is not None]
     for lid in dyn:
         plan.layers[lid].T = 1e300
-    plan.__dict__.pop("_device_plans", None)
     eng = R.DecodeEngine(weights, store, plan, **engine_kw)
     eng.step(int(tokens[0]), dynamic=False, want_logits=False)
     for t in tokens[1:]:
@@ -128,5 +127,4 @@ def calibrate_thresholds(weights, store, plan, tokens, high_rate: dict | float =
         plan.layers[lid].T = E.empirical_quantile(vals, r)
         plan.layers[lid].r = r
     eng.close()
-    plan.__dict__.pop("_device_plans", None)
     return plan

@@ -1,0 +1,99 @@
+"""Drop-in API behaviour of the device runtime (advisor findings, round 1):
+plans stay plain data after an engine is built, plan edits reach the device
+selector, forced bits and projection shapes are validated before any device
+work, and the public API's G defaults to f32 (the reference's G is float64)."""
+
+import copy
+import pickle
+
+import numpy as np
+import pytest
+
+from paper_2508_06041_b200 import estimator as E
+from paper_2508_06041_b200 import model as M
+from paper_2508_06041_b200 import quant as Q
+from paper_2508_06041_b200 import runtime as R
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def small():
+    cfg = M.ModelConfig(n_blocks=2, d_model=64, n_heads=4, d_ff=128, seq_cap=32)
+    w = M.init_model(0, cfg)
+    store = Q.quantize_model(w, 6, 3)
+    rng = np.random.default_rng(0)
+    layers = {}
+    for lid in store.ordered_ids():
+        cols = store.layers[lid].shape[1]
+        G = rng.standard_normal((8, cols)) * 0.1
+        est = E.ErrorEstimator(E.ProjectionEstimator(G, 8, 0), E.IMMEDIATE, (3, 4))
+        layers[lid] = R.PlanLayer(lid, 5, 3.5, (3, 4), 0.05, 0.5, est)
+    plan = R.PrecisionPlan("dp", 3.5, 5.0, layers, store.param_counts())
+    return w, store, plan
+
+
+def _bits(eng, toks):
+    eng.step(int(toks[0]), dynamic=False)
+    for t in toks[1:]:
+        eng.step(int(t))
+    return np.array([[s.bits[l] for l in eng._ids] for s in eng.trace.steps])
+
+
+def test_plan_stays_plain_data(small):
+    w, store, plan = small
+    eng = R.DecodeEngine(w, store, plan)
+    eng.step(1, dynamic=False)
+    assert "_device_plans" not in plan.__dict__
+    copy.deepcopy(plan)
+    pickle.dumps(plan)
+    eng.close()
+
+
+def test_plan_edits_reach_the_device(small):
+    w, store, plan = small
+    plan = copy.deepcopy(plan)
+    toks = [3, 7, 11, 5]
+    e1 = R.DecodeEngine(w, store, plan)
+    assert np.all(_bits(e1, toks) == 4)          # T = 0.05: every estimate above -> high
+    for pl in plan.layers.values():
+        pl.T = 1e30                               # now every decision is low
+    e2 = R.DecodeEngine(w, store, plan)
+    assert e2.dplan is not e1.dplan
+    assert np.all(_bits(e2, toks) == 3)
+    e3 = R.DecodeEngine(w, store, plan)          # unchanged plan: cached selector state
+    assert e3.dplan is e2.dplan
+    for e in (e1, e2, e3):
+        e.close()
+
+
+def test_forced_bits_validated(small):
+    w, store, plan = small
+    eng = R.DecodeEngine(w, store, plan)
+    ids = store.ordered_ids()
+    eng.step(1, dynamic=False)
+    with pytest.raises(ValueError):
+        eng.step(2, forced_bits={ids[0]: 3})                         # layers missing
+    with pytest.raises(ValueError):
+        eng.step(2, forced_bits=np.full(len(ids), 7, np.int8))       # above n_bits = 6
+    with pytest.raises(ValueError):
+        eng.step(2, forced_bits=np.full(len(ids), -1, np.int8))
+    with pytest.raises(ValueError):
+        eng.step(2, forced_bits=np.full(len(ids) - 1, 4, np.int8))   # wrong length
+    eng.step(2, forced_bits={l: 5 for l in ids})                    # in range: fine
+    assert all(b == 5 for b in eng.trace.steps[-1].bits.values())
+    eng.close()
+
+
+def test_projection_shape_checked(small):
+    w, store, plan = small
+    bad = copy.deepcopy(plan)
+    lid = store.ordered_ids()[0]
+    bad.layers[lid].estimator.kind.G = np.zeros((8, 3))
+    with pytest.raises(ValueError, match="projection G"):
+        R.DecodeEngine(w, store, bad)
+
+
+def test_public_api_defaults_to_f32_G(small):
+    import inspect
+    assert inspect.signature(R.DecodeEngine).parameters["g_dtype"].default == "f32"

@@ -204,14 +204,9 @@ def test_build_projection_on_device_matches_oracle(shape, pair):
     rng = np.random.default_rng(shape[0])
     q = Q.quantize_layer(rng.normal(0, 1 / np.sqrt(shape[1]), shape), 6, 3)
     l, h = pair
-    ds, i = q.device_handle()
-
-    def dW():
-        d = ds.dequantize(i, h)
-        d -= ds.dequantize(i, l)
-        return d
-
-    G = E.build_projection(dW, shape[0], 64, seed=9)
+    est = E.build_projection(q, l, h, 64, seed=9)
+    assert isinstance(est, E.ProjectionEstimator) and (est.k, est.seed) == (64, 9)
+    G = est.G
     G_ref = O.build_projection_G(O.as_layer(q), l, h, 64, 9)
     assert G.shape == (64, shape[1])
     np.testing.assert_allclose(G, G_ref, rtol=1e-10, atol=1e-12 * np.abs(G_ref).max())

@@ -236,9 +236,11 @@ def test_translate_threshold_matches_oracle():
         for l in (3, 4):
             for frac in (0.0, 0.1, 0.3, 0.5, 1 / 3, 0.7, 0.99, 1.0):
                 p = l + frac
-                assert E.translate_threshold(errs, p, l) == O.translate_threshold(errs, p, l)
-    assert E.translate_threshold([0.5], 3.0, 3)[0] == np.inf
-    assert E.translate_threshold([0.5], 4.0, 3)[0] == -np.inf
+                e = E.translate_threshold(errs, p, l)
+                assert (e.T, e.r_quantile) == O.translate_threshold(errs, p, l)
+                assert e.pair == (l, l + 1) and e.layer is None
+    assert E.translate_threshold([0.5], 3.0, 3).T == np.inf
+    assert E.translate_threshold([0.5], 4.0, 3).T == -np.inf
     with pytest.raises(ValueError):
         E.translate_threshold([], 3.5, 3)
     with pytest.raises(ValueError):

@@ -19,7 +19,7 @@ w, store, _ = synth.random_device_model(cfg, n_bits, b_min, seed=1234)
 pairs, prefill, high = B.pairs_for_target(store, 3.5)
 plan = synth.projection_plan(store, pairs, prefill, k=64, seed=0, target=3.5)
 synth.calibrate_thresholds(w, store, plan, np.random.default_rng(7).integers(0, cfg.vocab, 8), high_rate=high)
-eng = R.DecodeEngine(w, store, plan)
+eng = R.DecodeEngine(w, store, plan, g_dtype="f16")
 eng.prefill(np.random.default_rng(11).integers(0, cfg.vocab, 4))
 torch.cuda.synchronize()
 torch.cuda.profiler.start()          # ncu --profile-from-start off: only this launch

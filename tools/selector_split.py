@@ -52,7 +52,7 @@ def main():
     ids = store.ordered_ids()
     prompt = np.random.default_rng(11).integers(0, cfg.vocab, 16)
     toks = np.random.default_rng(12).integers(0, cfg.vocab, args.steps)
-    eng = R.DecodeEngine(w, store, plan)
+    eng = R.DecodeEngine(w, store, plan, g_dtype="f16")
     eng.prefill(prompt)
     t_dyn = timed_steps(eng, toks)
     recs = eng.trace.steps[-args.steps:]

@@ -48,7 +48,7 @@ def main():
         plan = synth.projection_plan(store, pairs, prefill, k=64, seed=0, target=args.target)
         calib = np.random.default_rng(7).integers(0, cfg.vocab, 24)
         synth.calibrate_thresholds(weights, store, plan, calib, high_rate=high)
-    eng = R.DecodeEngine(weights, store, plan)
+    eng = R.DecodeEngine(weights, store, plan, g_dtype="f16")
     eng.prefill(np.random.default_rng(11).integers(0, cfg.vocab, 16))
     eng.decode_greedy(4)
     torch.cuda.synchronize()
