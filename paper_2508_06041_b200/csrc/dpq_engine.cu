@@ -41,6 +41,12 @@
 #include "dpq_common.cuh"
 
 // Consumer-only CTA barrier (the producer and reducer warps never join).
+#ifndef DPQ_RING_SLOTS
+#define DPQ_RING_SLOTS 64          // ring slots (2 KB): bytes in flight per SM = the queueing depth
+#endif
+#ifndef DPQ_PF_ITEMS
+#define DPQ_PF_ITEMS 0             // (measured slower at 64-256) next op's first base items prefetched into L2 per CTA
+#endif
 #define CSYNC() asm volatile("bar.sync 1, %0;" :: "n"(dpq::eng::NT) : "memory")
 
 namespace dpq {
@@ -53,9 +59,9 @@ constexpr int kRedWarp = NCW;      // reducer warp
 constexpr int kProdWarp = NCW + 1; // TMA producer warp
 constexpr int NTB = NT + 64;
 constexpr int kItemBytes = 2048;   // one (tile, plane) item = kTileBytes
-constexpr int kMaxSlots = 64;      // ring slots (2 KB); the host checks they fit
+constexpr int kMaxSlots = DPQ_RING_SLOTS;      // ring slots (2 KB); the host checks they fit
 constexpr int kDecRing = 4;        // op decision entries in flight
-constexpr int kDbgRec = 16;        // debug stamps per (stage, CTA)
+constexpr int kDbgRec = 24;        // debug stamps per (stage, CTA)
 constexpr unsigned kPrevTag = 0x80000000u;   // previous-step sum x^2 words: tag = kPrevTag | rotation
 constexpr int kCurSlots = 4;       // estimator-set slots of the current step (step % 4)
 constexpr int kPrevSlots = 4;      // previous-step slots (rotation % 4)
@@ -171,8 +177,9 @@ struct Prog {
   float* logits;
   float* const* kc;        // [n_blocks] -> [seq_cap][dkv]
   float* const* vc;
-  u64* slot;               // [2][slot_half] tagged (tile, window) base partial sums
-  u64* slotx;              // [2][slot_half] tagged extra-plane partial sums
+  u64* slot;               // [2 (stage parity)][slot_half]: per op row (hi, lo) packed fixed-point
+                           // sums of the windows' base partials (see add_partial)
+  u64* slotx;              // [2][slot_half] the same for the extra-plane partials
   long long slot_half;
   u64* fpart;              // estimator sets [kSetSlots][set_stride]: per estimating layer k packed
                            // G.x words (kCntShift) + n_win tagged sum x[w]^2 words; slots
@@ -291,6 +298,9 @@ __device__ __forceinline__ double rsqrt_d(double x) {
 
 __device__ __forceinline__ float plane_sum(const uint4 d0, const uint4 d1, const uint4 d2, const uint4 d3,
                                            uint32_t lanereg) {
+#ifdef DPQ_NO_LOOKUP   // timing experiment only: the data path without the LUT lookups
+  return __uint_as_float((d0.x ^ d1.y ^ d2.z ^ d3.w) & 0x007fffffu);
+#endif
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #define ENG_WORD(W, S0)                                                 \
   {                                                                     \
@@ -977,59 +987,78 @@ __device__ __forceinline__ bool stage_done(const Prog& P, unsigned gs) {
 // ---------------------------------------------------------------------------
 // Reduction + epilogue (reducer warp, lane = row of the tile)
 // ---------------------------------------------------------------------------
-// Window partials of up to two op tiles (t0, t1 = -1 for none): base sums
-// from slot, extra-plane sums from slotx when ex0 / ex1 > 0. All words of a
-// poll are loaded together, each awaited until it carries the stage's epoch,
-// then summed in fixed window order: S = 2^ex S_base + S_extra.
+// ---------------------------------------------------------------------------
+// Cross-window partial sums (quant.py:74 @ x, one 512-column window per
+// task): every window adds its row partial S_w to the row's two packed words
+// (hi, lo) in one relaxed red.add each, no fence. v = round(S_w 2^30) (exact
+// for fp32 S_w >= 2^-6) is split into hi = v >> 24 and lo = v mod 2^24; a
+// word holds (count << 56) + sum of (part + 2^47), so the reader knows from
+// the word itself when all n_win windows are in. Integer sums: the total is
+// independent of the arrival order (deterministic). Range |S_w| < 2^33.
+// ---------------------------------------------------------------------------
+constexpr double kFxPart = 1073741824.0;   // 2^30
+__device__ __forceinline__ void add_partial(u64* w, float S, unsigned* err) {
+  long long v = 0;
+  if (fabsf(S) < 8.0e9f) v = llrint((double)S * kFxPart);
+  else atomicOr(err, (unsigned)ERR_RANGE);
+  const long long hi = v >> 24, lo = v & 0xffffff;
+  const u64 one = 1ull << kCntShift;
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(w), "l"(one + (u64)(hi + kFxBias)) : "memory");
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(w + 1), "l"(one + (u64)(lo + kFxBias)) : "memory");
+}
+__device__ __forceinline__ int packed_count(u64 w) { return (int)(w >> kCntShift); }
+__device__ __forceinline__ long long packed_value(u64 w) {
+  const long long c = (long long)(w >> kCntShift);
+  return (long long)(w & ((1ull << kCntShift) - 1)) - c * kFxBias;
+}
+// the row's total from its (hi, lo) words
+__device__ __forceinline__ double partial_total(uint4 q) {
+  const u64 h = ((u64)q.y << 32) | q.x, l = ((u64)q.w << 32) | q.z;
+  return (double)packed_value(h) * (1.0 / 64.0) + (double)packed_value(l) * (1.0 / kFxPart);
+}
+
+// Row totals of up to two op tiles (t1 = -1: none): base sums from slot,
+// extra-plane sums from slotx when ex0 / ex1 > 0; every word of the poll is
+// loaded at once (16 bytes per stream and lane), complete when each word
+// counts n_win windows; S = 2^ex S_base + S_extra. The words are zeroed once
+// read (this warp is their only reader; the stage parity reuses them two
+// stages later).
 __device__ __forceinline__ float2 tiles_S(const Prog& P, const Op& O, int t0, int ex0, int t1, int ex1,
                                          unsigned epoch) {
   const int lane = threadIdx.x & 31;
-  const int rows = O.n_tiles * 32;
   const size_t par = (size_t)((epoch - 1u) & 1u) * P.slot_half;   // parity of the stage (epoch = gs + 1)
-  const u64* b0 = P.slot + par + (size_t)t0 * 32 + lane;
-  const u64* x0 = P.slotx + par + (size_t)t0 * 32 + lane;
-  const u64* b1 = P.slot + par + (size_t)max(t1, 0) * 32 + lane;
-  const u64* x1 = P.slotx + par + (size_t)max(t1, 0) * 32 + lane;
-  const bool two = t1 >= 0;
-  float s0, e0, s1, e1;
+  u64* b0 = P.slot + par + ((size_t)t0 * 32 + lane) * 2;
+  u64* x0 = P.slotx + par + ((size_t)t0 * 32 + lane) * 2;
+  u64* b1 = P.slot + par + ((size_t)max(t1, 0) * 32 + lane) * 2;
+  u64* x1 = P.slotx + par + ((size_t)max(t1, 0) * 32 + lane) * 2;
+  const bool two = t1 >= 0, e0 = ex0 > 0, e1 = two && ex1 > 0;
+  const unsigned nw = (unsigned)O.n_win;
+  uint4 q0, q1, q2, q3;
+  const uint4 full = make_uint4(0u, nw << 24, 0u, nw << 24);   // count n_win, value 0 (unused streams)
   bool ok;
   unsigned n_ = 0;
   u64 tt0 = 0;
   do {
-    // one pass: every window's words (loads of a chunk are independent of the
-    // previous chunk's sums, so they stream), checked and summed in order
-    s0 = e0 = s1 = e1 = 0.f;
-    ok = true;
-    for (int w0 = 0; w0 < O.n_win; w0 += 8) {
-      const int nw = min(8, O.n_win - w0);
-      u64 v[4][8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < nw) {
-          const size_t o = (size_t)(w0 + j) * rows;
-          v[0][j] = ld_relaxed64(b0 + o);
-          v[1][j] = ex0 > 0 ? ld_relaxed64(x0 + o) : ((u64)epoch << 32);
-          v[2][j] = two ? ld_relaxed64(b1 + o) : ((u64)epoch << 32);
-          v[3][j] = two && ex1 > 0 ? ld_relaxed64(x1 + o) : ((u64)epoch << 32);
-        }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < nw) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) ok &= (unsigned)(v[q][j] >> 32) == epoch;
-          s0 += __uint_as_float((unsigned)v[0][j]);
-          e0 += __uint_as_float((unsigned)v[1][j]);
-          s1 += __uint_as_float((unsigned)v[2][j]);
-          e1 += __uint_as_float((unsigned)v[3][j]);
-        }
-    }
+    q0 = ld_tag2(b0);
+    q1 = e0 ? ld_tag2(x0) : full;
+    q2 = two ? ld_tag2(b1) : full;
+    q3 = e1 ? ld_tag2(x1) : full;
+    ok = (q0.y >> 24) == nw && (q0.w >> 24) == nw && (q1.y >> 24) == nw && (q1.w >> 24) == nw &&
+         (q2.y >> 24) == nw && (q2.w >> 24) == nw && (q3.y >> 24) == nw && (q3.w >> 24) == nw;
     if ((++n_ & 1023u) == 0) {
       const u64 t_ = gclock();
       if (tt0 == 0) tt0 = t_;
       else if (t_ - tt0 > 4000000000ull) hang("window partials", t0, epoch);
     }
   } while (!__all_sync(0xffffffffu, ok));
-  return make_float2(ex0 > 0 ? ldexpf(s0, ex0) + e0 : s0, ex1 > 0 ? ldexpf(s1, ex1) + e1 : s1);
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  *reinterpret_cast<uint4*>(b0) = z;
+  if (e0) *reinterpret_cast<uint4*>(x0) = z;
+  if (two) *reinterpret_cast<uint4*>(b1) = z;
+  if (e1) *reinterpret_cast<uint4*>(x1) = z;
+  const double s0 = e0 ? ldexp(partial_total(q0), ex0) + partial_total(q1) : partial_total(q0);
+  const double s1 = e1 ? ldexp(partial_total(q2), ex1) + partial_total(q3) : partial_total(q2);
+  return make_float2((float)s0, (float)s1);
 }
 
 struct Epi { float scale, sx; };
@@ -1164,7 +1193,7 @@ __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op
 // in lockstep): a batch spans <= kIssueLanes * 8 <= kMaxSlots consecutive FIFO
 // items, so the slot each lane waits for holds an item issued before the batch
 // (no lane can wait on an item another lane of the batch has yet to issue).
-constexpr int kIssueLanes = 8;
+constexpr int kIssueLanes = kMaxSlots / 8;
 static_assert(kIssueLanes * 8 <= kMaxSlots, "an issue batch must fit the ring");
 
 __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G, int n_steps, int s0) {
@@ -1244,6 +1273,29 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
         }
       fifo += n_base + n_ext;
       ++oi;
+      // L2 prefetch of the next op's first DPQ_PF_ITEMS base items (FIFO
+      // order): HBM keeps streaming through this op's tail (last items,
+      // reduction, the next input's latency); the ring's TMA loads then hit L2
+      if (DPQ_PF_ITEMS > 0) {
+        const int on = (st.y + 1) % (P.n_stages - 2);
+        const Op* On = P.ops + on;
+        const CtaWork* Wn = On->work + cta;
+        const int nt = Wn->n_tasks, t0 = Wn->task0, wn = Wn->w;
+        const I3 nbn = base_bits(*On, C);
+        for (int k = lane; k < nt; k += 32) {
+          const uint2 tk = __ldg(P.tasks + t0 + k);
+          const int li = task_layer(tk);
+          const int j0 = task_before(tk, nbn);
+          if (j0 >= DPQ_PF_ITEMS) continue;
+          const Layer& L = On->L[li];
+          const unsigned char* src = reinterpret_cast<const unsigned char*>(
+              L.planes + ((long long)wn * L.n_tiles + (task_tile(tk) - L.tile_off)) * (kItemBytes / 16));
+          const int np = min(nbn[li], DPQ_PF_ITEMS - j0);
+          for (int q = 0; q < np; ++q)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src + (long long)q * L.pstride * 16),
+                         "r"((unsigned)kItemBytes) : "memory");
+        }
+      }
     }
   }
 }
@@ -1313,14 +1365,14 @@ __device__ __forceinline__ void cons_op(const Prog& P, Smem& sm, int oi, int op_
   feed_finish(P, C, O, W, fp, sm.xw, gs + 1u);
   const I3 nb = base_bits(O, C);
   const uint32_t lanereg = kLut | ((uint32_t)lane * 4u);
-  const size_t par = (size_t)(gs & 1u) * P.slot_half + (size_t)W.w * O.n_tiles * 32 + lane;
+  const size_t par = (size_t)(gs & 1u) * P.slot_half + (size_t)lane * 2;
   const unsigned epoch = gs + 1u;
   const uint2* tasks = sm.ctask[b];
   for (int k = warp; k < W.n_tasks; k += NW) {
     const uint2 tk = tasks[k];
     const int li = task_layer(tk);
     const float S = stream_task(sm, fifo + task_before(tk, nb), nb[li], lanereg);
-    st_tag(P.slot + par + (size_t)task_tile(tk) * 32, S, epoch);
+    add_partial(P.slot + par + (size_t)task_tile(tk) * 64, S, P.err);
   }
   if (dbg && tid == 0) dbg[3] = gclock();
   const int n_base = W.cnt[0] * nb.v0 + W.cnt[1] * nb.v1 + W.cnt[2] * nb.v2;
@@ -1337,7 +1389,7 @@ __device__ __forceinline__ void cons_op(const Prog& P, Smem& sm, int oi, int op_
       const int li = task_layer(tk);
       if (ex[li] <= 0) continue;
       const float S = stream_task(sm, fifo + n_base + task_before(tk, ex), ex[li], lanereg);
-      st_tag(P.slotx + par + (size_t)task_tile(tk) * 32, S, epoch);
+      add_partial(P.slotx + par + (size_t)task_tile(tk) * 64, S, P.err);
     }
   }
   fifo += n_base + n_ext;
@@ -1377,7 +1429,10 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
         // only gets here once the consumers have finished op oi - 1
         const I3 nb = base_bits(O, C);
         I3 fin = nb;
+        u64* rdbg = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr;
+        if (rdbg && lane == 0) rdbg[16] = gclock();
         decide_op(P, C, O, nb, fin, cta, step_base);
+        if (rdbg && lane == 0) rdbg[17] = gclock();
         if (lane == 0) {
           sm.dec_fin[oi % kDecRing][0] = fin.v0;
           sm.dec_fin[oi % kDecRing][1] = fin.v1;
@@ -1388,6 +1443,7 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
         __syncwarp();
         if (cta < O.n_units) {
           const Epi E = op_epi(P, O, gs + 1u);
+          if (rdbg && lane == 0) rdbg[18] = gclock();
           if (lane == 0) SPIN_UNTIL(stage_done(P, gs), "stage counter (reducer)", gs, 0);
           __syncwarp();
           const unsigned epoch = gs + 1u;
@@ -1434,14 +1490,17 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
                 st_tag(O.out + o, v, epoch);
               }
             }
+            if (rdbg && lane == 0 && u == cta) rdbg[19] = gclock();
           }
         }
         ++oi;
         u64* dbg = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr;
         if (dbg && lane == 0) dbg[7] = gclock();
       }
+      __syncwarp();
       if (lane == 0) {
         SPIN_UNTIL_NS(sm.cons_gs >= gs + 1, "consumer stage", gs, sm.cons_gs, 12000000000ull);
+        __threadfence();   // the zeroed partial words (tiles_S) before the arrival: reused two stages on
         asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" :: "l"(P.bar) : "memory");
       }
       __syncwarp();

@@ -102,6 +102,27 @@ def main():
     for nm, (c, t, ab, mn) in agg.items():
         print(f"{nm:>7} {c:3d} crit {t / c:7.2f} | max " + " ".join(f"{v:6.2f}" for v in ab / c)
               + " | mean " + " ".join(f"{v:6.2f}" for v in mn / c))
+    if rec >= 20:
+        # reducer warp phases: [16] decide start, [17] decided, [18] statistics, [19] first unit out, [7] done
+        print("reducer (max | mean over CTAs, us rel. prev stage end): decide-start decided stats first-unit done")
+        oi = 0
+        ragg = {}
+        for k in range(n.value):
+            if kinds[k] != 1:
+                continue
+            nm = opn[oi % 4]
+            oi += 1
+            s = st[k]
+            ref = last_end[k - 1]
+            cols_r = (16, 17, 18, 19, 7)
+            mx = np.array([(s[:, j][s[:, j] > 0].max() - ref) / 1e3 if np.any(s[:, j] > 0) else 0 for j in cols_r])
+            mn = np.array([(s[:, j][s[:, j] > 0].mean() - ref) / 1e3 if np.any(s[:, j] > 0) else 0 for j in cols_r])
+            a_ = ragg.setdefault(nm, [0, np.zeros(5), np.zeros(5)])
+            a_[0] += 1
+            a_[1] += mx
+            a_[2] += mn
+        for nm, (c, mx, mn) in ragg.items():
+            print(f"{nm:>7} max " + " ".join(f"{v:6.2f}" for v in mx / c) + " | mean " + " ".join(f"{v:6.2f}" for v in mn / c))
     if rec >= 12:
         # attention units (qkv stages): stamps [8] enter, [9] q ready, [10] rows ready, [11] published
         oi, acc, nq = 0, np.zeros(6), 0
