@@ -1091,7 +1091,7 @@ __device__ __forceinline__ Epi op_epi(const Prog& P, const Op& O, unsigned epoch
 // the same decisions without another exchange).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op& O, const I3& nb, I3& fin,
-                                          int cta, unsigned step_base) {
+                                          int cta, unsigned step_base, u64* rdbg) {
   const int lane = threadIdx.x & 31;
   const bool dyn = C.mode == MODE_DYNAMIC;
   // every estimating layer's words in one poll: lane holds packed G.x words
@@ -1138,12 +1138,14 @@ __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op
 #pragma unroll
         for (int q = 0; q < 2; ++q) ok &= (unsigned)(sw[li][q] >> 32) == tag[li];
       }
+      if (rdbg && n_ == 0 && (threadIdx.x & 31) == 0) rdbg[22] = gclock();
       if ((++n_ & 1023u) == 0) {
         const u64 t_ = gclock();
         if (t0_ == 0) t0_ = t_;
         else if (t_ - t0_ > 4000000000ull) hang("estimator feeds", O.L[0].trace, O.n_layers);
       }
     } while (!__all_sync(0xffffffffu, ok));
+    if (rdbg && (threadIdx.x & 31) == 0) rdbg[23] = n_;
   }
 #pragma unroll
   for (int li = 0; li < kMaxOpLayers; ++li) {
@@ -1363,6 +1365,8 @@ __device__ __forceinline__ void cons_op(const Prog& P, Smem& sm, int oi, int op_
   CSYNC();
   if (dbg && tid == 0) dbg[2] = gclock();
   feed_finish(P, C, O, W, fp, sm.xw, gs + 1u);
+  if (dbg && lane == 0 && O.feed_rows > 0 && C.mode == MODE_DYNAMIC)
+    atomicMax(reinterpret_cast<unsigned long long*>(dbg + 20), gclock());
   const I3 nb = base_bits(O, C);
   const uint32_t lanereg = kLut | ((uint32_t)lane * 4u);
   const size_t par = (size_t)(gs & 1u) * P.slot_half + (size_t)lane * 2;
@@ -1431,7 +1435,7 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
         I3 fin = nb;
         u64* rdbg = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr;
         if (rdbg && lane == 0) rdbg[16] = gclock();
-        decide_op(P, C, O, nb, fin, cta, step_base);
+        decide_op(P, C, O, nb, fin, cta, step_base, rdbg);
         if (rdbg && lane == 0) rdbg[17] = gclock();
         if (lane == 0) {
           sm.dec_fin[oi % kDecRing][0] = fin.v0;

@@ -104,7 +104,7 @@ def main():
               + " | mean " + " ".join(f"{v:6.2f}" for v in mn / c))
     if rec >= 20:
         # reducer warp phases: [16] decide start, [17] decided, [18] statistics, [19] first unit out, [7] done
-        print("reducer (max | mean over CTAs, us rel. prev stage end): decide-start decided stats first-unit done")
+        print("reducer (max | mean over CTAs, us rel. prev stage end): decide-start first-poll feeds-done(CTA) decided stats first-unit done")
         oi = 0
         ragg = {}
         for k in range(n.value):
@@ -114,15 +114,17 @@ def main():
             oi += 1
             s = st[k]
             ref = last_end[k - 1]
-            cols_r = (16, 17, 18, 19, 7)
+            cols_r = (16, 22, 20, 17, 18, 19, 7)
             mx = np.array([(s[:, j][s[:, j] > 0].max() - ref) / 1e3 if np.any(s[:, j] > 0) else 0 for j in cols_r])
             mn = np.array([(s[:, j][s[:, j] > 0].mean() - ref) / 1e3 if np.any(s[:, j] > 0) else 0 for j in cols_r])
-            a_ = ragg.setdefault(nm, [0, np.zeros(5), np.zeros(5)])
+            a_ = ragg.setdefault(nm, [0, np.zeros(7), np.zeros(7), 0.0])
+            a_[3] += float(np.mean(buf.reshape(n.value, G, rec)[k][:, 23].astype(np.float64)))
             a_[0] += 1
             a_[1] += mx
             a_[2] += mn
-        for nm, (c, mx, mn) in ragg.items():
-            print(f"{nm:>7} max " + " ".join(f"{v:6.2f}" for v in mx / c) + " | mean " + " ".join(f"{v:6.2f}" for v in mn / c))
+        for nm, (c, mx, mn, npoll) in ragg.items():
+            print(f"{nm:>7} max " + " ".join(f"{v:6.2f}" for v in mx / c) + " | mean " + " ".join(f"{v:6.2f}" for v in mn / c)
+                  + f" | polls {npoll / c:.1f}")
     if rec >= 12:
         # attention units (qkv stages): stamps [8] enter, [9] q ready, [10] rows ready, [11] published
         oi, acc, nq = 0, np.zeros(6), 0
