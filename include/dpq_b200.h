@@ -56,7 +56,9 @@ typedef struct {
   int32_t prev_residual;  /* input_source == "previous_residual"              */
   int32_t k;              /* projection rank (rows of G)                      */
   int32_t g_dtype;        /* device copy of G: 0 f32, 1 f16, 2 e4m3+row scale */
-  int32_t pad_;
+  int32_t fx_bits_plus128; /* 0: fixed-point fraction bits of the engine's G.x
+                             words derived from G; else 128 + those bits (tensor
+                             parallel shards of G: the full layer's value)     */
   double T;               /* threshold; +/-INFINITY are the sentinels         */
   double slope, intercept;
   const double* G;        /* host, [k][cols] row-major (projection)           */
@@ -158,6 +160,38 @@ int dpq_session_logits_dev(dpq_session* ss, float** logits_dev);
 /* Diagnostics (env DPQ_DEBUG_TIMES=1 at session creation): per-CTA phase
  * timestamps (globaltimer ns) of every op of the last step, [op][per_op]. */
 int dpq_session_debug_times(dpq_session* ss, uint64_t* out, int64_t n, int* per_op);
+/* Wait for the session's enqueued work (dpq_session_step with logits_host =
+ * NULL, dpq_session_launch_steps) and check the engine's error flags;
+ * dpq_session_logits copies the last step's float32 [vocab] logits. */
+int dpq_session_sync(dpq_session* ss);
+int dpq_session_logits(dpq_session* ss, float* logits_host);
+
+/* ---- tensor parallelism (north star (4); runtime.py:348-369 sharded by
+ * output rows, replaces the reference's single-process matvec loop) ------
+ * One session per rank, each on its row shard of every linear layer: store
+ * layer i holds rows [rank R_i / N, (rank + 1) R_i / N) (q/k/v: the rank's
+ * heads, o/down: d/N rows, up/gate: d_ff/N rows); plan layer i holds the
+ * rank's rows [rank k / N, ...) of the full layer's projection G and the
+ * full layer's threshold. The persistent engine of each rank publishes its
+ * output rows, attention states, estimator partials and stage arrivals into
+ * every rank's exchange arena (peer stores over NVLink / same-device
+ * memory), so ranks take identical decisions and identical tokens. */
+typedef struct {
+  int32_t tp_rank, tp_size;   /* 1..8 ranks                                   */
+  int32_t grid;               /* CTAs of this rank's engine (0: every SM)     */
+  int32_t pad_;
+} dpq_tp_desc;
+int dpq_session_create_tp(dpq_store* s, dpq_plan* p, const dpq_model_desc* m, const dpq_tp_desc* tp,
+                          dpq_session** out);
+/* The rank's exchange arena (device pointer, bytes) and its CUDA IPC handle
+ * (64 bytes, cudaIpcMemHandle_t) for ranks in other processes. */
+int dpq_session_tp_arena(dpq_session* ss, void** base, int64_t* bytes);
+int dpq_session_tp_ipc_handle(dpq_session* ss, void* handle_out);
+int dpq_tp_ipc_open(int device, const void* handle, void** base);
+int dpq_tp_ipc_close(int device, void* base);
+/* peer_bases[q]: rank q's arena as mapped in this process (own arena at
+ * tp_rank). Call on every rank before the first step. */
+int dpq_session_tp_connect(dpq_session* ss, void* const* peer_bases);
 
 /* Host-side reference of the device plane layout (test infrastructure for the
  * repack; the product path repacks on the device). */

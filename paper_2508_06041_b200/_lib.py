@@ -27,7 +27,7 @@ class LayerDesc(C.Structure):
 class SelDesc(C.Structure):
     _fields_ = [("l", C.c_int32), ("h", C.c_int32), ("prefill_bit", C.c_int32),
                 ("est_kind", C.c_int32), ("prev_residual", C.c_int32), ("k", C.c_int32),
-                ("g_dtype", C.c_int32), ("pad_", C.c_int32), ("T", C.c_double),
+                ("g_dtype", C.c_int32), ("fx_bits_plus128", C.c_int32), ("T", C.c_double),
                 ("slope", C.c_double), ("intercept", C.c_double), ("G", C.c_void_p)]
 
 
@@ -38,6 +38,10 @@ class ModelDesc(C.Structure):
                 ("lm_head", C.c_void_p), ("track_exact", C.c_int32),
                 ("async_prev_block", C.c_int32), ("prime_from_prefill", C.c_int32),
                 ("use_graph", C.c_int32), ("use_pdl", C.c_int32), ("use_persistent", C.c_int32)]
+
+
+class TpDesc(C.Structure):
+    _fields_ = [("tp_rank", C.c_int32), ("tp_size", C.c_int32), ("grid", C.c_int32), ("pad_", C.c_int32)]
 
 
 P = C.c_void_p
@@ -72,6 +76,14 @@ _SIGS = {
     "dpq_session_engine_stages": ([P, C.POINTER(C.c_int), P, P], C.c_int),
     "dpq_session_profile_ops": ([P, C.c_int, C.c_int, P, C.c_int, C.POINTER(C.c_int)], C.c_int),
     "dpq_session_debug_times": ([P, P, C.c_int64, C.POINTER(C.c_int)], C.c_int),
+    "dpq_session_sync": ([P], C.c_int),
+    "dpq_session_logits": ([P, P], C.c_int),
+    "dpq_session_create_tp": ([P, P, C.POINTER(ModelDesc), C.POINTER(TpDesc), C.POINTER(P)], C.c_int),
+    "dpq_session_tp_arena": ([P, C.POINTER(P), C.POINTER(C.c_int64)], C.c_int),
+    "dpq_session_tp_ipc_handle": ([P, P], C.c_int),
+    "dpq_tp_ipc_open": ([C.c_int, P, C.POINTER(P)], C.c_int),
+    "dpq_tp_ipc_close": ([C.c_int, P], C.c_int),
+    "dpq_session_tp_connect": ([P, P], C.c_int),
     "dpq_repack_host": ([P, C.c_int, C.c_int, C.c_int, P, C.c_int64], C.c_int),
     "dpq_planes_bytes": ([C.c_int, C.c_int, C.c_int], C.c_int64),
 }

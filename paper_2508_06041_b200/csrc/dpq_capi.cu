@@ -250,6 +250,10 @@ struct dpq_session {
   std::vector<unsigned long long*> eng_vec;   // tagged vectors (reset to "no epoch")
   std::vector<size_t> eng_vec_len;
   size_t eng_fpart_len = 0;         // tagged estimator-set words (engine)
+  // tensor parallelism (row shards over tp_size ranks; dpq_session_create_tp)
+  int tp_size = 1, tp_rank = 0;
+  void* xarena = nullptr;           // exchange arena (cudaMalloc: one IPC handle)
+  size_t xarena_bytes = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -643,6 +647,8 @@ extern "C" int dpq_plan_create(dpq_store* s, int n_layers, const dpq_sel_desc* s
       }
       int fb = 46 - (int)std::ceil(std::log2(std::max(maxl1, 1e-30) * 65536.0));
       p->gt_fb.back() = std::min(52, std::max(-16, fb));
+      // tensor parallel shards of G (rows by k) must share the full layer's scale
+      if (d.fx_bits_plus128 != 0) p->gt_fb.back() = d.fx_bits_plus128 - 128;
     }
     if (S.sentinel == 0 && d.prev_residual) p->any_prev = 1;
     p->sel.push_back(S);

@@ -117,6 +117,7 @@ struct alignas(16) Op {
   int pair;                // up|gate SiLU pair epilogue
   int add;                 // residual add: out = res_in + y
   int attn_in;             // input = attention of the q|k|v op (out of stage in_stage)
+  int push;                // output published to every tensor-parallel rank (row-shard all-gather)
   int in_stage;            // stage (index in the step) publishing `in`
   int res_stage;           // stage publishing res_in
   int inst;                // input instance: statistics + estimator feeds
@@ -138,8 +139,9 @@ struct Feed {
   const float* gscale;
   int dtype, k, row0;      // row0: first row of this feed in the instance's row list
   int set;                 // the layer's set in Prog.fpart
+  int set_r0;              // first set row of this rank's G rows (tensor parallel: G sharded by k)
+  int kset;                // G rows of the set (all ranks'); its sum x^2 words follow them
   int kind;                // FEED_*
-  int pad;
   double fxscale;          // 2^fb of the packed G.x words
 };
 
@@ -165,7 +167,14 @@ struct Prog {
   const int* feed_begin;   // [n_inst + 1]
   const Feed* feeds;
   int n_inst;
-  int d, H, KV, hd, dkv, f, vocab, seq_cap, n_blocks;
+  int d, H, KV, hd, dkv, f, vocab, seq_cap, n_blocks;   // H, KV, dkv: this rank's heads (tensor parallel)
+  int dq;                  // this rank's q width (H hd)
+  int hg0;                 // global index of this rank's first head
+  // tensor parallelism (row shards): peer_off[q] = byte offset from this
+  // rank's exchange arena to rank q's, mapped in this address space (peer
+  // memory over NVLink; q = tp_rank: 0); pushed words go to every rank
+  int tp_size, tp_rank;
+  long long peer_off[8];
   float eps;
   const float* embed;
   const float* lm;
@@ -200,6 +209,17 @@ struct Prog {
   u64* attn_part;          // [H][attn_maxch][hd + 2] tagged chunk partials (o[hd], m, l)
   int attn_maxch;
 };
+
+__device__ __forceinline__ void st_tag_all(const Prog& P, u64* p, float v, unsigned e) {
+  const u64 w = ((u64)e << 32) | __float_as_uint(v);
+  for (int q = 0; q < P.tp_size; ++q)
+    __stcg(reinterpret_cast<u64*>(reinterpret_cast<char*>(p) + P.peer_off[q]), w);
+}
+__device__ __forceinline__ void red_all(const Prog& P, u64* p, u64 v) {
+  for (int q = 0; q < P.tp_size; ++q)
+    asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" :: "l"(reinterpret_cast<char*>(p) + P.peer_off[q]), "l"(v)
+                 : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // PTX helpers
@@ -237,6 +257,9 @@ __device__ __forceinline__ void red_rel_addu64(u64* p, u64 v) {
 __device__ __forceinline__ void st_tag(u64* p, float v, unsigned e) {
   __stcg(p, ((u64)e << 32) | __float_as_uint(v));
 }
+// A tagged word published to every tensor-parallel rank (p in the exchange arena).
+__device__ __forceinline__ void st_tag_all(const struct Prog& P, u64* p, float v, unsigned e);
+__device__ __forceinline__ void red_all(const struct Prog& P, u64* p, u64 v);
 __device__ __forceinline__ uint4 ld_tag2(const u64* p) {   // two tagged words (16-byte aligned)
   uint4 r;
   asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -642,8 +665,7 @@ __device__ __forceinline__ void feed_add(const Prog& P, const ECtl& C, const Fee
     long long f = 0;
     if (fabs(s) < (double)kFxBias) f = llrint(s);
     else atomicOr(P.err, (unsigned)ERR_RANGE);
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(feed_words(P, C, F) + r),
-                 "l"((1ull << kCntShift) + (u64)(f + kFxBias)) : "memory");
+    red_all(P, feed_words(P, C, F) + F.set_r0 + r, (1ull << kCntShift) + (u64)(f + kFxBias));
   }
 }
 
@@ -685,7 +707,7 @@ __device__ __forceinline__ void feed_finish(const Prog& P, const ECtl& C, const 
     for (int f = P.feed_begin[O.inst] + lane; f < P.feed_begin[O.inst + 1]; f += 32) {
       const Feed& F = P.feeds[f];
       if (!feed_active(F, C)) continue;
-      st_tag(feed_words(P, C, F) + F.k + W.w, (float)q, feed_tag(C, F, epoch));
+      st_tag(feed_words(P, C, F) + F.kset + W.w, (float)q, feed_tag(C, F, epoch));
     }
   }
 }
@@ -807,8 +829,8 @@ __device__ __forceinline__ void attn_unit(const Prog& P, const ECtl& C, const Op
     const int jj = lo ? i0 : i0 - half;
     const bool cur = t < s1;                                             // position t is in this chunk
     const u64* qv = O.in + (size_t)h * hd;
-    const u64* kv_ = O.in + P.d + goff;
-    const u64* vv_ = O.in + P.d + P.dkv + goff;
+    const u64* kv_ = O.in + P.dq + goff;
+    const u64* vv_ = O.in + P.dq + P.dkv + goff;
     float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f), s4 = c4;
     if (act) {
       c4 = __ldg(reinterpret_cast<const float4*>(P.cosv + (size_t)t * half + jj));
@@ -921,16 +943,17 @@ __device__ __forceinline__ void attn_unit(const Prog& P, const ECtl& C, const Op
         acc.x += ew * ow.x; acc.y += ew * ow.y; acc.z += ew * ow.z; acc.w += ew * ow.w;
       }
     }
-    u64* dst = P.attn_part + ((size_t)h * P.attn_maxch + ch) * (hd + 2);
+    // published to every rank (o's input windows span all heads)
+    u64* dst = P.attn_part + ((size_t)(P.hg0 + h) * P.attn_maxch + ch) * (hd + 2);
     if (act) {
-      st_tag(dst + i0, acc.x, e);
-      st_tag(dst + i0 + 1, acc.y, e);
-      st_tag(dst + i0 + 2, acc.z, e);
-      st_tag(dst + i0 + 3, acc.w, e);
+      st_tag_all(P, dst + i0, acc.x, e);
+      st_tag_all(P, dst + i0 + 1, acc.y, e);
+      st_tag_all(P, dst + i0 + 2, acc.z, e);
+      st_tag_all(P, dst + i0 + 3, acc.w, e);
     }
     if (lane == 0) {
-      st_tag(dst + hd, M, e);
-      st_tag(dst + hd + 1, L, e);
+      st_tag_all(P, dst + hd, M, e);
+      st_tag_all(P, dst + hd + 1, L, e);
     }
   }
   asm volatile("bar.sync 2, %0;" :: "n"(32 * kAttnWarps) : "memory");   // kv / attn_m reusable
@@ -981,7 +1004,7 @@ __device__ __forceinline__ void attn_merge(const Prog& P, const ECtl& C, int w, 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ bool stage_done(const Prog& P, unsigned gs) {
   if (gs < 2) return true;
-  return ld_acq64(P.bar) >= (u64)(gs - 1) * gridDim.x;
+  return ld_acq64(P.bar) >= (u64)(gs - 1) * gridDim.x * P.tp_size;
 }
 
 // ---------------------------------------------------------------------------
@@ -1467,7 +1490,9 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
               if (r < O.L[0].rows) {
                 const float up = E.scale * (lo0 * E.sx + ldexpf(sp0, -fin.v0) * (S.x + 0.5f * E.sx));
                 const float gt = E.scale * (lo1 * E.sx + ldexpf(sp1, -fin.v1) * (S.y + 0.5f * E.sx));
-                st_tag(O.out + r, up * (gt / (1.0f + expf(-gt))), epoch);        // runtime.py:368
+                const float hv = up * (gt / (1.0f + expf(-gt)));                 // runtime.py:368
+                if (O.push) st_tag_all(P, O.out + O.L[0].out_off + r, hv, epoch);
+                else st_tag(O.out + O.L[0].out_off + r, hv, epoch);
               }
             } else {
               const int li = layer_of(O, u);
@@ -1491,7 +1516,8 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
                   res = __uint_as_float((unsigned)xr);
                   v = res + v;
                 }
-                st_tag(O.out + o, v, epoch);
+                if (O.push) st_tag_all(P, O.out + o, v, epoch);
+                else st_tag(O.out + o, v, epoch);
               }
             }
             if (rdbg && lane == 0 && u == cta) rdbg[19] = gclock();
@@ -1505,7 +1531,8 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
       if (lane == 0) {
         SPIN_UNTIL_NS(sm.cons_gs >= gs + 1, "consumer stage", gs, sm.cons_gs, 12000000000ull);
         __threadfence();   // the zeroed partial words (tiles_S) before the arrival: reused two stages on
-        asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" :: "l"(P.bar) : "memory");
+        if (P.tp_size > 1) __threadfence_system();   // this stage's peer stores before the arrival
+        red_all(P, P.bar, 1ull);
       }
       __syncwarp();
     }

@@ -1,29 +1,26 @@
-"""Tensor-parallel decode: one process per GPU, rows of every
-linear layer split into N contiguous shards, one all-gather per op group.
+"""Tensor-parallel decode on the persistent engine (north star (4); SURVEY
+§8e): the reference's per-layer matvecs (runtime.py:348-369) sharded by
+output rows over N ranks, one rank per GPU (or N ranks on one device).
 
-Layout. Rank r holds rows [r*R', (r+1)*R') of each layer, where R' =
-ceil(rows / N). The last shard is zero-padded to R' rows (zero codes, lo = hi
-= 0, so the padded outputs are exactly 0), which lets every all-gather use
-equal, contiguous chunks. The input vector x is replicated on all ranks.
+Layout. Rank r holds rows [r R/N, (r+1) R/N) of every linear layer: its
+H/N query heads and KV/N kv heads of q/k/v (attention is head-local, the KV
+cache too), d/N rows of o and down, d_ff/N rows of up and gate. The input of
+every op is the full vector, replicated.
 
-Selector. G is replicated: option (a) of §8e. Every rank evaluates ||G x||
-(or slope*||x|| + b) on the same replicated input, using the same kernel and
-arithmetic, so all ranks take the same decision without an extra collective.
-Exact estimators (||(W_h - W_l) x|| over all rows) would need an all-reduce
-of per-shard partial norms; they and track_exact are rejected.
+Exchange (no NCCL on the data path). Each rank's engine (dpq_engine.cu)
+publishes what other ranks read into every rank's exchange arena, tile by
+tile, from the epilogue that produces it: the o / up|gate / down output rows
+(the row-shard all-gather, fused), the attention chunk states of its heads
+(o's input windows span all heads), its estimator partials and its stage
+arrivals. Arenas of other processes are mapped with CUDA IPC
+(``dpq_session_tp_ipc_handle`` / ``dpq_tp_ipc_open``, peer access over
+NVLink); ranks in one process on one device share pointers directly.
 
-Data path per layer. One dpq_select_gemv launch (selector + bitplane GEMV
-reading planes 0..b-1 of the local shard, runtime.py:184-193 + quant.py:95)
-writes the local y shard. Then an all-gather (NCCL through torch.distributed
-on GPUs; gloo with host staging in the CPU-side tests) assembles y. q/k/v
-share one all-gather, and so do up/gate. The per-step glue (RMSNorm, RoPE,
-attention with KV append, SiLU*up, residual adds, lm_head) restates
-runtime.py:345-372 in float32 on the device. Attention runs replicated: heads
-are not split, so the KV cache is per rank.
-
-This is the straightforward NCCL baseline of §8e. The fused path (GEMV
-epilogue pushing shards into peers over NVLink, with flag waits in the next
-prologue) is not built yet.
+Selector: option (b) of §8e. G is sharded by k: rank r holds rows
+[r k/N, (r+1) k/N) of each layer's projection and adds its G.x partials into
+every rank's estimator set, so every rank sees the full ||G x|| and takes the
+same decision (estimator.py:49-60, runtime.py:184-193) without a collective.
+Linear estimators need only sum x^2, which every rank has.
 """
 
 from __future__ import annotations
@@ -37,7 +34,9 @@ from . import _lib
 from . import estimator as E
 from . import model as M
 from . import quant as Q
-from .runtime import DecodeTrace, PrecisionPlan, ProvenanceError, StepRecord, DevicePlan
+from .runtime import DecodeEngine, DecodeTrace, DevicePlan, PlanLayer, PrecisionPlan, ProvenanceError
+
+IPC_HANDLE_BYTES = 64
 
 
 # ---------------------------------------------------------------------------
@@ -65,14 +64,10 @@ def shard_layer(q: Q.QuantizedLayer, world: int, rank: int) -> Q.QuantizedLayer:
     return Q.QuantizedLayer(codes, q.n_bits, q.b_min, lo, hi)
 
 
-def gather_rows(chunks, rows: int):
-    """Inverse of the sharding: concatenated padded shards -> the first `rows`."""
-    return chunks.reshape(-1)[:rows] if hasattr(chunks, "reshape") else chunks[:rows]
-
-
 def all_gather_flat(shard, group=None):
-    """All-gather equal-size 1-D shards into (world * n,), rank order.
-    NCCL gathers device tensors in place; gloo needs host tensors."""
+    """All-gather equal-size 1-D shards into (world * n,), rank order (host
+    staging for gloo). Test and tooling helper; the engine's data path
+    exchanges through peer memory."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
@@ -88,218 +83,285 @@ def all_gather_flat(shard, group=None):
     return torch.cat(parts).to(shard.device)
 
 
+def check_shardable(cfg: M.ModelConfig, world: int):
+    """Row shards must be whole heads and whole 32-row tiles."""
+    kv = cfg.kv_heads
+    hd = cfg.d_model // cfg.n_heads
+    if world < 1 or world > 8:
+        raise ValueError("tensor parallelism over 1..8 ranks")
+    if cfg.n_heads % world or kv % world or cfg.d_ff % world:
+        raise ValueError(f"heads {cfg.n_heads}, kv heads {kv} and d_ff {cfg.d_ff} must divide by {world}")
+    for rows in (cfg.d_model // world, kv * hd // world, cfg.d_ff // world):
+        if rows % 32:
+            raise ValueError(f"a {world}-way shard of {rows} rows is not a whole number of 32-row tiles")
+
+
+def fx_bits_of(G: np.ndarray) -> int:
+    """The engine's fixed-point fraction bits for a projection G (the rule of
+    dpq_plan_create), from the FULL layer's G, so every rank's shard uses the
+    same scale."""
+    maxl1 = float(np.max(np.sum(np.abs(G), axis=1))) if G.size else 0.0
+    fb = 46 - int(math.ceil(math.log2(max(maxl1, 1e-30) * 65536.0)))
+    return min(52, max(-16, fb))
+
+
+def shard_plan_layers(plan: PrecisionPlan, ids, world: int, rank: int):
+    """Per layer: the PlanLayer with this rank's rows [r k/N, (r+1) k/N) of the
+    projection (option (b)), and the full layer's fixed-point bits."""
+    out, fx = [], []
+    for lid in ids:
+        pl = plan.layers[lid]
+        est = pl.estimator
+        if est is not None and not math.isinf(pl.T) and isinstance(est.kind, E.ExactEstimator):
+            raise NotImplementedError("exact estimators need a partial-norm all-reduce; not on the TP engine")
+        if est is not None and hasattr(est.kind, "G") and not math.isinf(pl.T):
+            G = np.ascontiguousarray(est.kind.G, dtype=np.float64)
+            k = G.shape[0]
+            if k % world:
+                raise ValueError(f"{lid.name}: projection rank k={k} does not shard over {world} ranks")
+            kl = k // world
+            sub = E.ErrorEstimator(E.ProjectionEstimator(G[rank * kl:(rank + 1) * kl], kl, est.kind.seed),
+                                   est.input_source, est.pair)
+            out.append(PlanLayer(pl.layer, pl.prefill_bit, pl.p, pl.pair, pl.T, pl.r, sub))
+            fx.append(fx_bits_of(G))
+        else:
+            out.append(pl)
+            fx.append(None)
+    return out, fx
+
+
+def shard_store(store: Q.BitPlaneStore, world: int, rank: int, device=None) -> Q.DeviceStore:
+    """This rank's row shards of every layer (canonical order) on the device."""
+    return Q.DeviceStore([shard_layer(store.layers[lid], world, rank) for lid in store.ordered_ids()], device)
+
+
 # ---------------------------------------------------------------------------
-# engine
+# one rank's engine
 # ---------------------------------------------------------------------------
 
-class TPDecodeEngine:
-    """DecodeEngine (runtime.py:245-390) with tensor-parallel linears.
-
-    Same constructor arguments as runtime.DecodeEngine plus ``group`` (a
-    torch.distributed process group, default WORLD) and ``shard_store`` (a
-    DeviceStore already holding this rank's padded row shards in canonical
-    layer order, e.g. from synth.random_device_model(shard=...); otherwise the
-    host codes of ``store`` are sharded here). ``step`` returns the float64
-    logits on every rank; ``trace`` records the (identical) decisions.
-    """
+class TPDecodeEngine(DecodeEngine):
+    """DecodeEngine (runtime.py:245-390) of tensor-parallel rank ``rank`` of
+    ``world`` on the persistent engine. Same constructor arguments as
+    runtime.DecodeEngine plus ``rank`` / ``world`` (default: the
+    torch.distributed group's), ``group``, ``shard_store`` (a DeviceStore of
+    this rank's row shards in canonical order; else sharded here from the
+    host codes of ``store``) and ``grid`` (CTAs of this rank's engine, 0 =
+    every SM). ``connect`` must run on every rank before the first step;
+    ``TPDecodeEngine.create`` does it through torch.distributed (CUDA IPC
+    handles exchanged with all_gather_object). Every rank returns the same
+    logits and records the same decisions."""
 
     def __init__(self, weights: M.ModelWeights, store: Q.BitPlaneStore, plan: PrecisionPlan,
                  store_hash: str | None = None, track_exact: bool = False,
                  async_rule: str = "prev_step", prime_from_prefill: bool = True,
-                 g_dtype: str = "f16", group=None, shard_store=None):
-        import torch
-        import torch.distributed as dist
+                 g_dtype: str = "f32", rank: int = 0, world: int = 1, shard_store_=None, grid: int = 0):
         if store_hash is not None and plan.store_hash and store_hash != plan.store_hash:
             raise ProvenanceError(f"plan was built against store {plan.store_hash[:12]}, "
                                   f"got {store_hash[:12]}")
         if store.config_hash != weights.config.hash():
             raise ProvenanceError("store/model config mismatch")
+        if track_exact:
+            raise NotImplementedError("track_exact needs the per-op graph; not on the TP engine")
         if async_rule not in ("prev_step", "prev_block"):
             raise ValueError(f"unknown async rule {async_rule!r}")
-        if track_exact:
-            raise NotImplementedError("track_exact under tensor parallelism needs a partial-norm all-reduce")
-        self.group = group
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        cfg = weights.config
+        check_shardable(cfg, world)
+        self.rank, self.world = rank, world
         self.weights, self.store, self.plan = weights, store, plan
-        self.cfg = cfg = weights.config
+        self.cfg = cfg
+        self.track_exact = False
         self.async_rule = async_rule
         self.prime_from_prefill = prime_from_prefill
         self.total_params = plan.total_params()
         self._ids = store.ordered_ids()
-        self._index = {lid: i for i, lid in enumerate(self._ids)}
-        for lid in self._ids:
-            pl = plan.layers[lid]
-            if pl.estimator is not None and not math.isinf(pl.T) and E.kind_code(pl.estimator) == E.EST_EXACT:
-                raise NotImplementedError(f"{lid.name}: exact estimator under tensor parallelism")
-        self.device = _lib.torch_device()
-        # local shards: one device store + plan over the shard layers
-        self._rows = [store.layers[lid].shape[0] for lid in self._ids]
-        self._per = [shard_rows(r, self.world, self.rank)[2] for r in self._rows]
-        if shard_store is not None:
-            if [s[0] for s in shard_store.shapes] != self._per:
-                raise ValueError("shard_store does not match the row sharding")
-            self.dstore = shard_store
-        else:
-            shards = [shard_layer(store.layers[lid], self.world, self.rank) for lid in self._ids]
-            self.dstore = Q.DeviceStore(shards, self.device)
-        self.dplan = DevicePlan(self.dstore, [plan.layers[lid] for lid in self._ids], g_dtype)
         self._M = np.array([plan.M[l] for l in self._ids], dtype=np.float64)
+        pls = [plan.layers[l] for l in self._ids]
         self._ops_per_step = 0
-        for lid in self._ids:
-            pl = plan.layers[lid]
+        for lid, pl in zip(self._ids, pls):
             if not math.isinf(pl.T):
                 self._ops_per_step += pl.estimator.kind.op_cost(store.layers[lid].shape[1])
-        f32 = dict(device=self.device, dtype=torch.float32)
-        self._embed = torch.as_tensor(np.asarray(weights.embed, dtype=np.float32), **f32)
-        self._lm = torch.as_tensor(np.asarray(weights.lm_head, dtype=np.float32), **f32)
-        cos, sin = M.rope_tables(cfg.seq_cap, cfg.head_dim)
-        self._cos = None if cos is None else torch.as_tensor(cos, **f32)
-        self._sin = None if sin is None else torch.as_tensor(sin, **f32)
-        self._bit = torch.zeros(len(self._ids), dtype=torch.int32, device=self.device)
-        self._est = torch.zeros(len(self._ids), dtype=torch.float32, device=self.device)
+        self._dual = [False] * len(pls)
+        self._sentinel = [math.isinf(pl.T) for pl in pls]
+        ds = shard_store_ if shard_store_ is not None else shard_store(store, world, rank)
+        layers, fx = shard_plan_layers(plan, self._ids, world, rank)
+        self.dplan = DevicePlan(ds, layers, g_dtype, fx_bits=fx)
+        md = _lib.ModelDesc()
+        md.n_blocks, md.d_model, md.n_heads = cfg.n_blocks, cfg.d_model, cfg.n_heads
+        md.n_kv_heads, md.d_ff, md.vocab, md.seq_cap = cfg.kv_heads, cfg.d_ff, cfg.vocab, cfg.seq_cap
+        md.norm_eps = cfg.norm_eps
+        emb = np.ascontiguousarray(weights.embed, dtype=np.float32)
+        lm = np.ascontiguousarray(weights.lm_head, dtype=np.float32)
+        md.embed, md.lm_head = emb.ctypes.data, lm.ctypes.data
+        md.track_exact = 0
+        md.async_prev_block = int(async_rule == "prev_block")
+        md.prime_from_prefill = int(prime_from_prefill)
+        md.use_graph, md.use_pdl, md.use_persistent = 1, 1, 1
+        td = _lib.TpDesc(rank, world, int(grid), 0)
+        h = C.c_void_p()
+        import torch
+        from .quant import _destroy
+        import weakref
+        with torch.cuda.device(ds.device):
+            _lib.call("dpq_session_create_tp", ds.handle, self.dplan.handle, C.byref(md), C.byref(td), C.byref(h))
+        self._h = h
+        self._fin = weakref.finalize(self, _destroy, "dpq_session_destroy", h.value)
+        self._logits = np.empty(cfg.vocab, dtype=np.float32)
+        self._opened = []
         self.reset()
 
-    def reset(self):
-        import torch
-        cfg = self.cfg
-        shape = (cfg.n_blocks, cfg.seq_cap, cfg.kv_heads, cfg.head_dim)
-        self._k = torch.zeros(shape, dtype=torch.float32, device=self.device)
-        self._v = torch.zeros(shape, dtype=torch.float32, device=self.device)
-        self._pos = 0
-        self._prev_inputs = {}
-        self._cur_inputs = {}
-        self.trace = DecodeTrace()
+    # -- peers --
+    def arena(self) -> int:
+        base, n = C.c_void_p(), C.c_int64()
+        _lib.call("dpq_session_tp_arena", self._h, C.byref(base), C.byref(n))
+        return base.value
 
-    @property
-    def position(self) -> int:
-        return self._pos
+    def ipc_handle(self) -> bytes:
+        buf = (C.c_char * IPC_HANDLE_BYTES)()
+        _lib.call("dpq_session_tp_ipc_handle", self._h, buf)
+        return bytes(buf)
 
-    # -- helpers (runtime.py:288-309, 383-384) ----------------------------
-    def _norm(self, x):
-        return x / (x.square().mean() + self.cfg.norm_eps).sqrt()
+    def connect(self, peer_bases):
+        """peer_bases[q]: rank q's arena in this process (own arena at rank)."""
+        arr = (C.c_void_p * self.world)(*[C.c_void_p(b) for b in peer_bases])
+        _lib.call("dpq_session_tp_connect", self._h, arr)
 
-    def _rope(self, v, t):
-        if self._cos is None:
-            return v
-        half = self._cos.shape[1]
-        c, s = self._cos[t], self._sin[t]
-        out = v.clone()
-        v1, v2 = v[:, :half], v[:, half:2 * half]
-        out[:, :half] = v1 * c - v2 * s
-        out[:, half:2 * half] = v1 * s + v2 * c
-        return out
+    def connect_ipc(self, handles):
+        """Map the other ranks' arenas from their IPC handles (rank order)."""
+        dev = self.dplan.store.device.index
+        bases = []
+        for q, hb in enumerate(handles):
+            if q == self.rank:
+                bases.append(self.arena())
+                continue
+            base = C.c_void_p()
+            buf = C.create_string_buffer(bytes(hb), IPC_HANDLE_BYTES)
+            _lib.call("dpq_tp_ipc_open", dev, buf, C.byref(base))
+            self._opened.append(base.value)
+            bases.append(base.value)
+        self.connect(bases)
 
-    def _estimator_input(self, lid, x):
-        pl = self.plan.layers[lid]
-        est = pl.estimator
-        if est is None or est.input_source == E.IMMEDIATE:
-            return None
-        if self.async_rule == "prev_block":
-            prev = self._cur_inputs.get(M.LayerId(lid.block - 1, lid.kind))
-        else:
-            prev = self._prev_inputs.get(lid)
-        return prev
+    @classmethod
+    def create(cls, weights, store, plan, group=None, **kw):
+        """One rank per process: rank / world from torch.distributed, IPC
+        handles exchanged with all_gather_object, arenas mapped, barrier."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        eng = cls(weights, store, plan, rank=rank, world=world, **kw)
+        handles = [None] * world
+        dist.all_gather_object(handles, eng.ipc_handle(), group=group)
+        eng.connect_ipc(handles)
+        dist.barrier(group)
+        return eng
 
-    def _shard(self, lid, x, dynamic):
-        """Local y shard of layer lid (selector + GEMV on the device)."""
-        import torch
-        i = self._index[lid]
-        y = torch.empty(self._per[i], dtype=torch.float32, device=self.device)
-        pl = self.plan.layers[lid]
-        if not dynamic:
-            _lib.call("dpq_gemv", self.dstore.handle, i, int(pl.prefill_bit), C.c_void_p(x.data_ptr()),
-                      C.c_void_p(y.data_ptr()), _lib.stream_ptr())
-        else:
-            ein = self._estimator_input(lid, x)
-            _lib.call("dpq_select_gemv", self.dplan.handle, i, C.c_void_p(x.data_ptr()),
-                      C.c_void_p(ein.data_ptr()) if ein is not None else None, C.c_void_p(y.data_ptr()),
-                      C.c_void_p(self._bit.data_ptr() + 4 * i), C.c_void_p(self._est.data_ptr() + 4 * i),
-                      None, _lib.stream_ptr())
-        self._cur_inputs[lid] = x
-        return y
+    def close(self):
+        dev = self.dplan.store.device.index
+        for b in self._opened:
+            try:
+                _lib.call("dpq_tp_ipc_close", dev, C.c_void_p(b))
+            except Exception:
+                pass
+        self._opened = []
+        self._fin()
 
-    def _linears(self, lids, x, dynamic):
-        """y of each layer in lids (same input x): local shards, one all-gather."""
-        import torch
-        shards = [self._shard(lid, x, dynamic) for lid in lids]
-        full = all_gather_flat(torch.cat(shards), self.group)
-        tot = sum(self._per[self._index[l]] for l in lids)
-        full = full.view(self.world, tot)
-        out, off = [], 0
-        for lid in lids:
-            i = self._index[lid]
-            out.append(full[:, off:off + self._per[i]].reshape(-1)[: self._rows[i]])
-            off += self._per[i]
-        return out
-
-    # -- step (runtime.py:330-381) ----------------------------------------
-    def step(self, token: int, dynamic: bool = True):
-        import torch
-        cfg = self.cfg
-        t = self._pos
-        if t >= cfg.seq_cap:
+    # -- stepping: launch (no wait) / finish --
+    def launch_step(self, token: int, dynamic: bool = True, forced_bits=None):
+        if self._pos >= self.cfg.seq_cap:
             raise ValueError("sequence cap exceeded")
-        H, KV, hd = cfg.n_heads, cfg.kv_heads, cfg.head_dim
-        qh = H // KV
-        scale = 1.0 / math.sqrt(hd)
-        self._cur_inputs = {}
-        x = self._embed[int(token)].clone()
-        for b in range(cfg.n_blocks):
-            L = lambda kind: M.LayerId(b, kind)  # noqa: E731
-            n1 = self._norm(x)
-            q, k, v = self._linears([L("q"), L("k"), L("v")], n1, dynamic)
-            q = self._rope(q.view(H, hd), t)
-            k = self._rope(k.view(KV, hd), t)
-            self._k[b, t] = k
-            self._v[b, t] = v.view(KV, hd)
-            K = self._k[b, : t + 1].repeat_interleave(qh, dim=1)      # (t+1, H, hd)
-            V = self._v[b, : t + 1].repeat_interleave(qh, dim=1)
-            scores = torch.einsum("hd,shd->hs", q, K) * scale
-            probs = torch.softmax(scores, dim=1)
-            attn = torch.einsum("hs,shd->hd", probs, V).reshape(-1).contiguous()
-            (o,) = self._linears([L("o")], attn, dynamic)
-            x = x + o
-            n2 = self._norm(x)
-            up, gate = self._linears([L("up"), L("gate")], n2, dynamic)
-            h = (up * (gate / (1.0 + torch.exp(-gate)))).contiguous()
-            (down,) = self._linears([L("down")], h, dynamic)
-            x = x + down
-        logits = self._lm @ self._norm(x)
-        self._pos += 1
+        fb = self._forced(forced_bits)
+        _lib.call("dpq_session_step", self._h, int(token), int(bool(dynamic)),
+                  C.c_void_p(fb.ctypes.data) if fb is not None else None, None)
         if dynamic:
-            bits = self._bit.cpu().numpy().astype(np.int64)
-            est = self._est.cpu().numpy()
-            rec = StepRecord(t, {}, {}, {}, 0.0)
-            for i, lid in enumerate(self._ids):
-                rec.bits[lid] = int(bits[i])
-                pl = self.plan.layers[lid]
-                rec.estimates[lid] = None if (math.isinf(pl.T) or np.isnan(est[i])) else float(est[i])
-            rec.effective_bits = float((bits * self._M).sum() / self.total_params)
-            self.trace.steps.append(rec)
-            self.trace.estimator_ops += self._ops_per_step
-        if dynamic or self.prime_from_prefill:
-            self._prev_inputs = self._cur_inputs
-        return logits.double().cpu().numpy()
+            self._dyn_pos.append(self._pos)
+            self._trace.estimator_ops += self._ops_per_step
+        self._pos += 1
 
-    def prefill(self, tokens):
-        logits = None
-        for tok in tokens:
-            logits = self.step(int(tok), dynamic=False)
-        return logits
+    def finish_step(self, want_logits: bool = True):
+        if want_logits:
+            _lib.call("dpq_session_logits", self._h, C.c_void_p(self._logits.ctypes.data))
+            return self._logits.astype(np.float64)
+        _lib.call("dpq_session_sync", self._h)
+        return None
+
+    def step(self, token: int, dynamic: bool = True, forced_bits=None, want_logits: bool = True):
+        self.launch_step(token, dynamic, forced_bits)
+        return self.finish_step(want_logits)
+
+    def launch_greedy(self, n_new: int):
+        if self._pos + n_new > self.cfg.seq_cap:
+            raise ValueError("sequence cap exceeded")
+        _lib.call("dpq_session_launch_steps", self._h, int(n_new), None)
+        self.note_device_steps(n_new)
+
+    def decode_greedy(self, n_new: int) -> list:
+        if self._pos + n_new > self.cfg.seq_cap:
+            raise ValueError("sequence cap exceeded")
+        toks = np.zeros(max(n_new, 1), dtype=np.int32)
+        _lib.call("dpq_session_decode", self._h, int(n_new), C.c_void_p(toks.ctypes.data))
+        self.note_device_steps(n_new)
+        return [int(t) for t in toks[:n_new]]
 
 
 def decode(weights, store, plan, prompt, n_new, store_hash=None, group=None, **engine_kw):
-    """Greedy decode (runtime.py:393-409) under tensor parallelism."""
+    """Greedy decode (runtime.py:393-409) on this rank of the process group;
+    every rank returns the same (tokens, DecodeTrace)."""
     if len(prompt) == 0:
         raise ValueError("empty prompt")
+    eng = TPDecodeEngine.create(weights, store, plan, group=group, store_hash=store_hash, **engine_kw)
     if len(prompt) + n_new > weights.config.seq_cap:
         raise ValueError("sequence cap exceeded")
-    eng = TPDecodeEngine(weights, store, plan, store_hash, group=group, **engine_kw)
-    logits = eng.prefill(prompt)
-    out = []
-    for _ in range(n_new):
-        tok = int(np.argmax(logits))
-        out.append(tok)
-        logits = eng.step(tok, dynamic=True)
+    eng.prefill(prompt)
+    out = eng.decode_greedy(n_new) if n_new > 0 else []
     return out, eng.trace
+
+
+# ---------------------------------------------------------------------------
+# N ranks in one process on one device (tests, single-GPU demonstration)
+# ---------------------------------------------------------------------------
+
+class LocalTPGroup:
+    """``world`` TP ranks of the same model in this process on the current
+    device, each engine on n_sm / world CTAs, arenas shared by pointer; the
+    ranks' kernels run concurrently on their own streams. Rank 0's logits,
+    tokens and trace are returned; ``check_identical`` compares every rank's
+    logits (they must be equal: same decisions, same reductions)."""
+
+    def __init__(self, weights, store, plan, world: int, g_dtype: str = "f32", grid: int | None = None, **kw):
+        n_sm = C.c_int()
+        cc0, cc1 = C.c_int(), C.c_int()
+        import torch
+        _lib.call("dpq_device_info", torch.cuda.current_device(), C.byref(n_sm), C.byref(cc0), C.byref(cc1))
+        g = grid if grid is not None else n_sm.value // world
+        self.ranks = [TPDecodeEngine(weights, store, plan, g_dtype=g_dtype, rank=r, world=world, grid=g, **kw)
+                      for r in range(world)]
+        bases = [e.arena() for e in self.ranks]
+        for e in self.ranks:
+            e.connect(bases)
+        self.world = world
+
+    @property
+    def trace(self) -> DecodeTrace:
+        return self.ranks[0].trace
+
+    def step(self, token: int, dynamic: bool = True, forced_bits=None, all_logits: bool = False):
+        for e in self.ranks:
+            e.launch_step(token, dynamic, forced_bits)
+        lg = [e.finish_step(True) for e in self.ranks]
+        return lg if all_logits else lg[0]
+
+    def prefill(self, tokens):
+        out = None
+        for t in tokens:
+            out = self.step(int(t), dynamic=False)
+        return out
+
+    def decode_greedy(self, n_new: int) -> list:
+        for e in self.ranks[1:]:
+            e.launch_greedy(n_new)
+        toks = self.ranks[0].decode_greedy(n_new)
+        for e in self.ranks[1:]:
+            _lib.call("dpq_session_sync", e._h)
+        return toks
+
+    def close(self):
+        for e in self.ranks:
+            e.close()
