@@ -46,9 +46,9 @@ def parse():
     ap.add_argument("--g-dtype", default="f16", choices=["f32", "f16", "e4m3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-static", action="store_true")
-    ap.add_argument("--tp", action="store_true",
-                    help="tensor-parallel decode of ONE sequence over the N ranks (strong scaling, "
-                         "paper_2508_06041_b200.tp); default N>1 runs N replicas")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: N independent sequences, one per GPU (weak scaling); default N>1 is tensor "
+                         "parallel decode of ONE sequence over the N ranks (strong scaling)")
     return ap.parse_args()
 
 
@@ -146,7 +146,7 @@ def op_bytes(store, plan, bits_row, ids, g_bytes_per_el):
     return np.array(ops)
 
 
-def cpu_slice_oracle(cfg, host_layers, plan, weights, n_tokens=6, seed=0):
+def cpu_slice_oracle(cfg, host_layers, plan, weights, n_tokens=20, seed=0):
     """Reference CPU path (oracle port, float64 dense dequantized matvec, numpy
     BLAS on all host threads) on a 2-block slice of the same model and plan;
     tokens/s extrapolated x n_blocks/2. Returns (tokens_per_s, seconds, sample)."""
@@ -175,60 +175,76 @@ def cpu_slice_oracle(cfg, host_layers, plan, weights, n_tokens=6, seed=0):
     return 1.0 / per_token_full, sample
 
 
+def host_info():
+    """CPU model and the BLAS threads numpy uses (the reference path's matvecs)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = max((i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"), default=None)
+    except Exception:
+        pass
+    return {"cpu_model": model, "host_threads": os.cpu_count(), "blas_threads": blas}
+
+
+def build_workload(args, rank=0, world=1, keep_host_blocks=0):
+    """The benchmarked model and plan (shared by both arms): synthetic
+    init_model-law weights quantized on the device, DP plan with (l, h) pairs,
+    k=64 projection estimators built on the device, thresholds calibrated on
+    the engine so ~(target - l) of the decisions are high."""
+    from paper_2508_06041_b200 import synth
+    cfg, n_bits, b_min = model_config(args.config)
+    res = synth.random_device_model(cfg, n_bits, b_min, seed=1234, keep_host_blocks=keep_host_blocks,
+                                    shard=(world, rank) if world > 1 else None)
+    weights, store, host = res[:3]
+    sds = res[3] if world > 1 else None
+    pairs, prefill, high = pairs_for_target(store, args.target)
+    plan = synth.projection_plan(store, pairs, prefill, k=64, seed=0, target=args.target)
+    calib = np.random.default_rng(7).integers(0, cfg.vocab, 48)
+    synth.calibrate_thresholds(weights, store, plan, calib, high_rate=high, g_dtype=args.g_dtype)
+    return cfg, n_bits, b_min, weights, store, host, sds, pairs, plan
+
+
+def config_dict(args, cfg, n_bits, b_min, pairs, ids, world):
+    return {"workload": f"{args.config}-shaped batch-1 greedy decode of one sequence, DP plan {args.target}-bit "
+                        f"target, ({pairs[ids[0]][0]},{pairs[ids[0]][1]}) pairs, k=64 projection selector "
+                        f"({args.g_dtype} G)" + (f", tensor parallel over {world} GPUs" if world > 1 else ""),
+            "n_blocks": cfg.n_blocks, "d_model": cfg.d_model, "n_heads": cfg.n_heads,
+            "n_kv_heads": cfg.kv_heads, "d_ff": cfg.d_ff, "vocab": cfg.vocab,
+            "n_bits": n_bits, "b_min": b_min, "prompt": PROMPT,
+            "parallelism": (f"replicas{world}" if args.replicas else f"tp{world}") if world > 1 else "single"}
+
+
 def run_reference(args):
-    """--impl reference: the reference CPU implementation (oracle port) of the
-    path, timed on this host's cores, same metric/config."""
-    import torch  # noqa: F401
-    from oracle import dpq_oracle as O
-    from paper_2508_06041_b200 import estimator as E
-    from paper_2508_06041_b200 import model as M
-    from paper_2508_06041_b200 import runtime as R
+    """--impl reference: the reference CPU implementation of the path (the
+    oracle port: float64 dequantized matvecs, runtime.py:330-381) on this
+    host's cores, on the SAME model and calibrated plan as our arm (a 2-block
+    slice, extrapolated to the full depth), same metric and config keys."""
+    import torch
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg, n_bits, b_min = model_config(args.config)
-    nb = 2
-    rng = np.random.default_rng(0)
-    host, plan_layers = {}, {}
-    d = cfg.d_model
-    embed = rng.normal(0.0, 1.0, (cfg.vocab, d)).astype(np.float32)
-    lm = (rng.normal(0.0, 1.0, (cfg.vocab, d)) * (0.1 / np.sqrt(d))).astype(np.float32)
-    lo_b = int(np.floor(args.target))
-    for b in range(nb):
-        for k in M.KINDS:
-            lid = M.LayerId(b, k)
-            rows, cols = M.layer_shape(cfg, lid)
-            W = rng.standard_normal((rows, cols), dtype=np.float32) * np.float32(1 / np.sqrt(cols))
-            q = O.quantize_layer(W, n_bits, b_min)
-            host[lid] = q
-            Gs = rng.standard_normal((64, cols)) * 1e-3
-            est = E.ErrorEstimator(E.ProjectionEstimator(Gs, 64, 0), E.IMMEDIATE, (lo_b, lo_b + 1))
-            plan_layers[lid] = R.PlanLayer(lid, lo_b + 1, args.target, (lo_b, lo_b + 1), 0.0, 0.5, est)
-    scfg = M.ModelConfig(nb, d, cfg.n_heads, cfg.d_ff, cfg.vocab, cfg.seq_cap, cfg.norm_eps, cfg.n_kv_heads)
-    w = M.ModelWeights(scfg, embed, lm, {})
-    Ms = {l: int(np.prod(q.shape)) for l, q in host.items()}
-    eng = O.Engine(w, host, plan_layers, Ms)
-    toks = rng.integers(0, cfg.vocab, args.warmup + args.steps + 1)
-    eng.step(int(toks[0]), dynamic=False)
-    for t in toks[1:1 + args.warmup]:
-        eng.step(int(t))
-    t0 = time.perf_counter()
-    for t in toks[1 + args.warmup:]:
-        eng.step(int(t))
-    dt = (time.perf_counter() - t0) / max(args.steps, 1)
-    full = dt * cfg.n_blocks / nb
-    v = 1.0 / full
-    cores = os.cpu_count()
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    cfg, n_bits, b_min, weights, store, host, _, pairs, plan = build_workload(args, keep_host_blocks=2)
+    ids = store.ordered_ids()
+    steps = max(args.steps, 20)
+    v, sample = cpu_slice_oracle(cfg, host, plan, weights, n_tokens=steps)
+    full_ms = 1000.0 / v
+    hi = host_info()
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": full * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic random-init weights (init_model law), synthetic tokens",
-            "config": {"workload": f"{args.config}-shaped decode, batch 1, {args.target}-bit DP plan "
-                                   f"(2-block slice, extrapolated x{cfg.n_blocks // nb})",
-                       "n_blocks": cfg.n_blocks, "d_model": cfg.d_model, "d_ff": cfg.d_ff},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} decode steps of a 2-block slice after {args.warmup} "
-                                       f"warm-up steps, extrapolated x{cfg.n_blocks // nb}"},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: random-init weights (W ~ N(0,1/cols), init_model law), random prompt tokens",
+            "config": config_dict(args, cfg, n_bits, b_min, pairs, ids, 1),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": hi["host_threads"], "kind": "port",
+                             "sample": sample, **hi},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -272,7 +288,8 @@ def op_stage_times(eng, store, plan, ids, g_bytes):
     buf = np.zeros(n.value * G * rec, dtype=np.uint64)
     _lib.call("dpq_session_debug_times", eng._h, C.c_void_p(buf.ctypes.data), buf.size, C.byref(per))
     st = buf.reshape(n.value, G, rec)[..., :8].astype(np.float64)
-    last_end = st[..., 7].max(axis=1)
+    # end of a stage: op stages -> the reducer's last unit [7]; begin / head -> consumers done [4]
+    last_end = np.where((kinds == 1)[:, None], st[..., 7], st[..., 4]).max(axis=1)
     crit = np.diff(np.concatenate([[st[0, :, 0].min()], last_end])) / 1e3
     bits = [eng.trace.steps[-1].bits[l] for l in ids]
     by = op_bytes(store, plan, bits, ids, g_bytes)
@@ -286,31 +303,43 @@ def run_ours(args):
     import torch.distributed as dist
     from paper_2508_06041_b200 import _lib
     from paper_2508_06041_b200 import runtime as R
-    from paper_2508_06041_b200 import synth
+    from paper_2508_06041_b200 import tp as TP
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the multi-rank path on ONE GPU (CUDA MPS running):
+    # every rank on cuda:0 with n_sm / world CTAs, gloo for the host plumbing
+    one_gpu = os.environ.get("DPQ_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg, n_bits, b_min = model_config(args.config)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    tp = world if (world > 1 and not args.replicas) else 1
     t_build = time.perf_counter()
     keep = 2 if (rank == 0 and not args.no_cpu_baseline) else 0
-    weights, store, host = synth.random_device_model(cfg, n_bits, b_min, seed=1234, keep_host_blocks=keep)
-    pairs, prefill, high = pairs_for_target(store, args.target)
-    plan = synth.projection_plan(store, pairs, prefill, k=64, seed=0, target=args.target)
-    calib = np.random.default_rng(7).integers(0, cfg.vocab, 48)
-    synth.calibrate_thresholds(weights, store, plan, calib, high_rate=high, g_dtype=args.g_dtype)
+    cfg, n_bits, b_min, weights, store, host, sds, pairs, plan = build_workload(
+        args, rank, tp, keep_host_blocks=keep)
     build_s = time.perf_counter() - t_build
     g_bytes = {"f32": 4, "f16": 2, "e4m3": 1}[args.g_dtype]
 
     ids = store.ordered_ids()
-    eng = R.DecodeEngine(weights, store, plan, g_dtype=args.g_dtype)
+    if tp > 1:
+        # one sequence over the tp ranks: row shards, peer-memory exchange (CUDA IPC)
+        eng = TP.TPDecodeEngine.create(weights, store, plan, g_dtype=args.g_dtype, shard_store_=sds,
+                                       grid=(torch.cuda.get_device_properties(0).multi_processor_count // world
+                                             if one_gpu else 0))
+    else:
+        eng = R.DecodeEngine(weights, store, plan, g_dtype=args.g_dtype)
     engine_kind = _lib.load().dpq_session_is_persistent(eng._h)
     stream = torch.cuda.Stream()
     sp = C.c_void_p(stream.cuda_stream)
-    prompt = np.random.default_rng(11 + rank).integers(0, cfg.vocab, PROMPT)
+    seed = 11 if tp > 1 else 11 + rank
+    prompt = np.random.default_rng(seed).integers(0, cfg.vocab, PROMPT)
     eng.prefill(prompt)
     total = args.warmup + args.steps
     if PROMPT + total + 40 > cfg.seq_cap:
@@ -326,7 +355,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     e0.record(stream)
-    # timed: K greedy decode steps, ONE launch of the persistent engine kernel
+    # timed: K greedy decode steps, ONE launch of the persistent engine kernel per rank
     _lib.call("dpq_session_launch_steps", eng._h, args.steps, sp)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -334,24 +363,27 @@ def run_ours(args):
     clk = clocks.stop()
     eng.note_device_steps(total)
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cpu" if one_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = world * 1000.0 / ms_per_step
+    seqs = world // tp                       # independent sequences of the job
+    value = seqs * 1000.0 / ms_per_step
     recs = eng.trace.steps[-args.steps:]
     eff_bits = float(np.mean([s.effective_bits for s in recs]))
     high_frac = float(np.mean([[s.bits[l] == plan.layers[l].pair[1] for l in ids] for s in recs]))
-    # algorithmic bytes of the timed steps (realized bits per step, KV growing)
+    # algorithmic bytes of the timed steps (realized bits per step, KV growing),
+    # of the whole model (all tp ranks together) per sequence
     alg = sum(step_bytes(cfg, store, plan, [r.bits[l] for l in ids], ids, g_bytes, pos0 + i)
               for i, r in enumerate(recs))
-    achieved = alg / (ms * 1e-3) / 1e9
+    achieved = seqs * alg / (ms * 1e-3) / 1e9
     peak, peak_kind = measured_peak()
+    peak_job = peak * (1 if one_gpu else world)
 
     # per-op GB/s (critical path from stage stamps) on a separate instrumented
     # session; only the TMA engine (session kind 2) records stage stamps
     per_op, gemv_gbs = None, None
-    if engine_kind == 2:
+    if engine_kind == 2 and tp == 1:
         os.environ["DPQ_DEBUG_TIMES"] = "1"
         eng2 = R.DecodeEngine(weights, store, plan, g_dtype=args.g_dtype)
         del os.environ["DPQ_DEBUG_TIMES"]
@@ -370,7 +402,7 @@ def run_ours(args):
     # realized effective bits (same engine, same decode loop)
     overhead = None
     static_ms = {}
-    if not args.skip_static:
+    if not args.skip_static and tp == 1:
         from paper_2508_06041_b200.runtime import sentinel_static_plan
         for bit in sorted(set(p for pr in pairs.values() for p in pr)):
             sp_plan = sentinel_static_plan({l: bit for l in ids}, store.param_counts(), float(bit))
@@ -391,35 +423,42 @@ def run_ours(args):
             t_static = static_ms[bl[0]]
         overhead = (ms_per_step - t_static) / t_static
 
-    # e2e through the public step API: host token in, host logits out
+    # e2e through the public step API: host token in, host logits out, every
+    # step (all tp ranks step in lockstep); timed as the max over ranks
     n_e2e = min(32, cfg.seq_cap - eng._pos - 1)
     toks = np.random.default_rng(5).integers(0, cfg.vocab, n_e2e)
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for t in toks:
         eng.step(int(t), dynamic=True)
     e2e_s = (time.perf_counter() - t0) / n_e2e
-    e2e_value = world * 1.0 / e2e_s
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cpu" if one_gpu else "cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = seqs * 1.0 / e2e_s
 
+    conf = config_dict(args, cfg, n_bits, b_min, pairs, ids, world)
+    conf.update({"engine": {2: "persistent TMA engine", 1: "persistent flag kernel", 0: "multi-kernel"}.get(
+                     engine_kind, str(engine_kind)),
+                 "l2_policy": "weights (3.0-3.6 GB of bitplanes per step) >> 126 MB L2; no flush needed",
+                 "realized_effective_bits": eff_bits, "high_decision_rate": high_frac,
+                 "selector_overhead": overhead, "static_ms_per_step": static_ms,
+                 "per_op": per_op, "gemv_stage_GBps": gemv_gbs, "build_s": build_s})
+    if tp > 1:
+        conf["tp_exchange"] = ("row shards; o / up|gate / down rows, attention states, G.x partials (G "
+                               "sharded by k) and stage arrivals stored into every rank's arena over "
+                               "NVLink (CUDA IPC), fused in the producing epilogue; no NCCL on the data path")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "weak" if args.replicas else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: random-init weights (W ~ N(0,1/cols), init_model law), random prompt tokens",
-            "config": {"workload": f"{args.config}-shaped batch-1 greedy decode, DP plan {args.target}-bit "
-                                   f"target, ({pairs[ids[0]][0]},{pairs[ids[0]][1]}) pairs, k=64 projection "
-                                   f"selector ({args.g_dtype} G)",
-                       "n_blocks": cfg.n_blocks, "d_model": cfg.d_model, "n_heads": cfg.n_heads,
-                       "n_kv_heads": cfg.kv_heads, "d_ff": cfg.d_ff, "vocab": cfg.vocab,
-                       "n_bits": n_bits, "b_min": b_min, "prompt": PROMPT,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "engine": {2: "persistent TMA engine", 1: "persistent flag kernel", 0: "multi-kernel"}.get(
-                           engine_kind, str(engine_kind)),
-                       "l2_policy": "weights (3.0-3.6 GB of bitplanes per step) >> 126 MB L2; no flush needed",
-                       "realized_effective_bits": eff_bits, "high_decision_rate": high_frac,
-                       "selector_overhead": overhead, "static_ms_per_step": static_ms,
-                       "per_op": per_op, "gemv_stage_GBps": gemv_gbs, "build_s": build_s},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+            "config": conf,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_job, "unit": "GB/s",
+                         "frac": achieved / peak_job, "traffic": None, "peak_kind": peak_kind,
+                         "peak_per_gpu": peak,
                          "kernel": ("engine_kernel (whole decode step: fused selector + bitplane GEMVs, "
                                     "attention, lm_head; one launch per timed region)") if engine_kind == 2
                          else "session step kernels (the TMA engine declined this shape)",
@@ -430,89 +469,31 @@ def run_ours(args):
                     "d2h_bytes_per_step": 4 * cfg.vocab}}
     if rank == 0 and not args.no_cpu_baseline and host:
         v, sample = cpu_slice_oracle(cfg, host, plan, weights)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                                "sample": sample}
+        hi = host_info()
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": hi["host_threads"], "kind": "port",
+                                "sample": sample, **hi}
     traffic_path = os.path.join(ROOT, "profiles", "engine_traffic.json")
-    # the committed ncu DRAM figure is of the default workload only
-    if os.path.exists(traffic_path) and engine_kind == 2 and args.config == "llama3_8b" and args.target == 3.5:
+    # the committed ncu DRAM figure is of the default single-GPU workload only
+    if (os.path.exists(traffic_path) and engine_kind == 2 and args.config == "llama3_8b" and args.target == 3.5
+            and world == 1):
         try:
             line["roofline"]["traffic"] = json.load(open(traffic_path)).get("bytes_per_step")
+            line["roofline"]["traffic_source"] = "profiles/engine_traffic.json (ncu --set full capture)"
         except Exception:
             pass
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        if tp > 1:
+            eng.close()
         dist.destroy_process_group()
-
-
-def run_tp(args):
-    """Tensor-parallel decode of one sequence over WORLD_SIZE ranks:
-    row-sharded linears, NCCL all-gather per op group, host-driven steps."""
-    import torch
-    import torch.distributed as dist
-    from paper_2508_06041_b200 import runtime as R
-    from paper_2508_06041_b200 import synth
-    from paper_2508_06041_b200 import tp as TP
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29533")
-        dist.init_process_group("gloo", rank=0, world_size=1)
-    cfg, n_bits, b_min = model_config(args.config)
-    weights, store, _, sds = synth.random_device_model(cfg, n_bits, b_min, seed=1234, shard=(world, rank))
-    pairs, prefill, high = pairs_for_target(store, args.target)
-    plan = synth.projection_plan(store, pairs, prefill, k=64, seed=0, target=args.target)
-    calib = np.random.default_rng(7).integers(0, cfg.vocab, 48)
-    synth.calibrate_thresholds(weights, store, plan, calib, high_rate=high, g_dtype=args.g_dtype)
-    eng = TP.TPDecodeEngine(weights, store, plan, g_dtype=args.g_dtype, shard_store=sds)
-    prompt = np.random.default_rng(11).integers(0, cfg.vocab, PROMPT)
-    logits = eng.prefill(prompt)
-    tok = int(np.argmax(logits))
-    for _ in range(args.warmup):
-        tok = int(np.argmax(eng.step(tok)))
-    dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        tok = int(np.argmax(eng.step(tok)))       # logits reach the host every step (greedy)
-    torch.cuda.synchronize()
-    s = time.perf_counter() - t0
-    t = torch.tensor([s], dtype=torch.float64)
-    if world > 1:
-        t = t.cuda()
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_per_step = float(t.item()) * 1e3 / args.steps
-    eff = float(np.mean([r.effective_bits for r in eng.trace.steps[-args.steps:]]))
-    line = {"metric": METRIC, "value": 1000.0 / ms_per_step, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic: random-init weights, random prompt tokens",
-            "config": {"workload": f"{args.config}-shaped batch-1 greedy decode of ONE sequence, "
-                                   f"tensor parallel over {world} GPU(s), DP plan {args.target}-bit",
-                       "parallelism": f"tp{world}", "realized_effective_bits": eff,
-                       "path": "row-sharded dpq_select_gemv + NCCL all-gather per op group, host-driven"},
-            "gpu_launches": None,
-            "e2e": {"value": 1000.0 / ms_per_step, "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 8 * cfg.vocab}}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    dist.barrier()
-    dist.destroy_process_group()
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    elif args.tp:
-        run_tp(args)
     else:
         run_ours(args)
 
