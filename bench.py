@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=128)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="llama3_8b", choices=["llama3_8b", "llama2_7b", "cfg1", "llama2_70b_slice"])
+    ap.add_argument("--config", default="llama3_8b",
+                    choices=["llama3_8b", "llama2_7b", "cfg1", "llama2_70b", "llama2_70b_slice"])
     ap.add_argument("--target", type=float, default=3.5)
     ap.add_argument("--g-dtype", default="f16", choices=["f32", "f16", "e4m3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -58,6 +59,8 @@ def model_config(name):
         return M.ModelConfig(32, 4096, 32, 14336, vocab=256, seq_cap=1024, n_kv_heads=8), 4, 3
     if name == "llama2_7b":
         return M.ModelConfig(32, 4096, 32, 11008, vocab=256, seq_cap=1024), 6, 3
+    if name == "llama2_70b":        # BASELINE configs[4]: full depth, 3-6 bit overlay
+        return M.ModelConfig(80, 8192, 64, 28672, vocab=256, seq_cap=1024, n_kv_heads=8), 6, 3
     if name == "llama2_70b_slice":
         return M.ModelConfig(8, 8192, 64, 28672, vocab=256, seq_cap=1024, n_kv_heads=8), 6, 3
     return M.ModelConfig(2, 512, 8, 1792, vocab=256, seq_cap=1024), 4, 3
@@ -65,10 +68,20 @@ def model_config(name):
 
 def pairs_for_target(store, target):
     """(floor, ceil) pair per layer; prefill at the high bit; ~ (target - l)
-    of the decisions high (SURVEY 8d synthetic plans)."""
+    of the decisions high (SURVEY 8d synthetic plans). An integer target on a
+    store with bits on both sides (the 3-6 bit overlay at 4 bits) gets the
+    adjacent pairs (t-1, t) and (t, t+1) on alternate layers, with the high
+    rate that puts the parameter-weighted effective bits at t."""
     lo = int(np.floor(target))
-    hi = lo + 1 if target > lo else lo
     ids = store.ordered_ids()
+    if target == lo and store.b_min < lo < store.n_bits:
+        pairs = {l: ((lo - 1, lo) if i % 2 == 0 else (lo, lo + 1)) for i, l in enumerate(ids)}
+        Ms = store.param_counts()
+        base = sum(Ms[l] * pairs[l][0] for l in ids)
+        tot = sum(Ms[l] for l in ids)
+        rate = (target * tot - base) / tot
+        return pairs, {l: pairs[l][1] for l in ids}, float(rate)
+    hi = lo + 1 if target > lo else lo
     pairs = {l: (lo, hi) for l in ids}
     prefill = {l: hi for l in ids}
     return pairs, prefill, (target - lo) if hi > lo else 0.0
@@ -213,8 +226,9 @@ def build_workload(args, rank=0, world=1, keep_host_blocks=0):
 
 
 def config_dict(args, cfg, n_bits, b_min, pairs, ids, world):
+    pr = sorted({tuple(p) for p in pairs.values()})
     return {"workload": f"{args.config}-shaped batch-1 greedy decode of one sequence, DP plan {args.target}-bit "
-                        f"target, ({pairs[ids[0]][0]},{pairs[ids[0]][1]}) pairs, k=64 projection selector "
+                        f"target, {' / '.join(f'({a},{b})' for a, b in pr)} pairs, k=64 projection selector "
                         f"({args.g_dtype} G)" + (f", tensor parallel over {world} GPUs" if world > 1 else ""),
             "n_blocks": cfg.n_blocks, "d_model": cfg.d_model, "n_heads": cfg.n_heads,
             "n_kv_heads": cfg.kv_heads, "d_ff": cfg.d_ff, "vocab": cfg.vocab,
@@ -416,11 +430,13 @@ def run_ours(args):
             torch.cuda.synchronize()
             static_ms[bit] = e0.elapsed_time(e1) / args.steps
             e2.close()
+        # static time interpolated at the realized effective bits (bracketing bits)
         bl = sorted(static_ms)
-        if len(bl) == 2:
-            t_static = static_ms[bl[0]] + (static_ms[bl[1]] - static_ms[bl[0]]) * (eff_bits - bl[0]) / (bl[1] - bl[0])
-        else:
-            t_static = static_ms[bl[0]]
+        t_static = static_ms[bl[0]]
+        for b0, b1 in zip(bl, bl[1:]):
+            if b0 <= eff_bits <= b1 or b1 == bl[-1]:
+                t_static = static_ms[b0] + (static_ms[b1] - static_ms[b0]) * (eff_bits - b0) / (b1 - b0)
+                break
         overhead = (ms_per_step - t_static) / t_static
 
     # e2e through the public step API: host token in, host logits out, every

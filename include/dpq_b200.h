@@ -89,6 +89,10 @@ int dpq_device_info(int device, int* n_sm, int* cc_major, int* cc_minor);
  *      102-110); codes are repacked into MSB-first device bitplanes. ------- */
 int dpq_store_create(int device, int n_layers, const dpq_layer_desc* layers, dpq_store** out);
 int dpq_store_destroy(dpq_store* s);
+/* Streaming build of a large store: dpq_store_create with n_layers = 0, then
+ * layers appended in canonical order (each repacked on the device as it
+ * arrives, so the caller can free its codes before the next layer). */
+int dpq_store_append(dpq_store* s, int n_layers, const dpq_layer_desc* layers);
 /* Algorithmic bytes of the selected planes + (lo, span) for one GEMV at b. */
 int dpq_store_layer_bytes(const dpq_store* s, int layer, int b, int64_t* bytes);
 

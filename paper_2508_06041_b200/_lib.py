@@ -52,6 +52,7 @@ _SIGS = {
     "dpq_device_info": ([C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
     "dpq_store_create": ([C.c_int, C.c_int, C.POINTER(LayerDesc), C.POINTER(P)], C.c_int),
     "dpq_store_destroy": ([P], C.c_int),
+    "dpq_store_append": ([P, C.c_int, C.POINTER(LayerDesc)], C.c_int),
     "dpq_store_layer_bytes": ([P, C.c_int, C.c_int, C.POINTER(C.c_int64)], C.c_int),
     "dpq_quantize_device": ([C.c_int, P, C.c_int, C.c_int, C.c_int, P, P, P, P], C.c_int),
     "dpq_gemv": ([P, C.c_int, C.c_int, P, P, P], C.c_int),

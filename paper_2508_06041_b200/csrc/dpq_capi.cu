@@ -353,8 +353,95 @@ extern "C" int dpq_quantize_device(int device, const float* W_dev, int rows, int
 // ---------------------------------------------------------------------------
 // store
 // ---------------------------------------------------------------------------
+// One layer: codes (host or device; uint16 / uint8 / the .dpqs packed stream)
+// repacked into bitplanes on the device; lo / span / hi padded to whole tiles.
+static int store_add_layer(dpq_store* s, const dpq_layer_desc& d, int i) {
+  if (d.rows < 1 || d.cols < 1 || d.n_bits < 2 || d.n_bits > 8 || d.b_min < 1 || d.b_min > d.n_bits ||
+      (d.code_bytes < 0 || d.code_bytes > 2) || !d.codes || !d.lo || !d.hi)
+    return set_err(DPQ_ERR_ARG, "dpq_store_create: bad layer %d", i);
+  DevLayer L{};
+  L.rows = d.rows;
+  L.cols = d.cols;
+  L.n_bits = d.n_bits;
+  L.b_min = d.b_min;
+  L.n_tiles = cdiv(d.rows, kTileRows);
+  L.n_win = cdiv(d.cols, kWinCols);
+  L.plane_stride16 = (long long)L.n_win * L.n_tiles * (kTileBytes / 16);
+  const long long pbytes = dpq_planes_bytes(d.rows, d.cols, d.n_bits);
+  void* planes = nullptr;
+  if (s->arena.alloc(&planes, pbytes)) return DPQ_ERR_CUDA;
+  const void* codes_dev = d.codes;
+  void* tmp = nullptr;
+  const size_t cbytes = d.code_bytes ? (size_t)d.rows * d.cols * d.code_bytes
+                                     : ((size_t)d.rows * d.cols * d.n_bits + 7) / 8;   // .dpqs packed
+  if (!d.codes_on_device) {
+    if (cudaMalloc(&tmp, cbytes) != cudaSuccess ||
+        cudaMemcpy(tmp, d.codes, cbytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+      if (tmp) cudaFree(tmp);
+      return set_err(DPQ_ERR_CUDA, "dpq_store_create: code upload failed");
+    }
+    codes_dev = tmp;
+  }
+  const long long groups = (long long)L.n_tiles * 32 * L.n_win * kGroups;
+  const int blocks = (int)std::min<long long>((groups + 255) / 256, 65535LL * 16);
+  repack_kernel<<<blocks, 256>>>(codes_dev, d.code_bytes, d.rows, d.cols, d.n_bits, L.n_win, L.n_tiles,
+                                 reinterpret_cast<unsigned char*>(planes));
+  cudaError_t e = cudaDeviceSynchronize();
+  if (tmp) cudaFree(tmp);
+  if (e != cudaSuccess) return set_err(DPQ_ERR_CUDA, "repack: %s", cudaGetErrorString(e));
+  L.planes = reinterpret_cast<const uint4*>(planes);
+  const int rp = L.n_tiles * 32;
+  std::vector<float> lo(rp, 0.f), span(rp, 0.f), hi(rp, 0.f);
+  for (int r = 0; r < d.rows; ++r) {
+    lo[r] = d.lo[r];
+    hi[r] = d.hi[r];
+    span[r] = (float)((double)d.hi[r] - (double)d.lo[r]);
+  }
+  float *dlo, *dspan, *dhi;
+  if (s->arena.alloc_t(&dlo, rp) || s->arena.alloc_t(&dspan, rp) || s->arena.alloc_t(&dhi, rp))
+    return DPQ_ERR_CUDA;
+  if (cudaMemcpy(dlo, lo.data(), rp * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(dspan, span.data(), rp * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(dhi, hi.data(), rp * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+    return set_err(DPQ_ERR_CUDA, "dpq_store_create: lo/hi upload failed");
+  L.lo = dlo;
+  L.span = dspan;
+  s->layers.push_back(L);
+  s->hi.push_back(dhi);
+  s->plane_bytes.push_back(pbytes);
+  return DPQ_OK;
+}
+
+// Standalone-op scratch for the store's current largest layer (re-made when
+// appended layers grow it; the old scratch stays in the arena).
+static int store_make_scratch(dpq_store* s) {
+  int rp = 32, nw = 1, nt = 1, nc = 1;
+  for (const DevLayer& L : s->layers) {
+    rp = std::max(rp, L.n_tiles * 32);
+    nw = std::max(nw, L.n_win);
+    nt = std::max(nt, L.n_tiles);
+    nc = std::max(nc, L.cols);
+  }
+  if (s->ctl && rp <= s->max_rows_pad && nw <= s->max_win && nt <= s->max_tiles && nc <= s->max_cols) return DPQ_OK;
+  s->max_rows_pad = rp;
+  s->max_win = nw;
+  s->max_tiles = nt;
+  s->max_cols = nc;
+  if (s->scratch.make(s->arena, s->max_win, s->max_rows_pad, s->max_tiles) ||
+      s->arena.alloc_t(&s->ctl, 1) || s->arena.alloc_t(&s->sync, 2) || s->arena.alloc_t(&s->decision, 4) ||
+      s->arena.alloc_t(&s->ctr, 128) || s->arena.alloc_t(&s->gxa, kMaxOpLayers * kMaxK) ||
+      s->arena.alloc_t(&s->tr_bits, 4) || s->arena.alloc_t(&s->tr_est, 4) ||
+      s->arena.alloc_t(&s->tr_exact, 4) || s->arena.alloc_t(&s->est_buf, s->max_cols))
+    return DPQ_ERR_CUDA;
+  Control c{};
+  c.mode = MODE_DYNAMIC;
+  if (cudaMemcpy(s->ctl, &c, sizeof(c), cudaMemcpyHostToDevice) != cudaSuccess)
+    return set_err(DPQ_ERR_CUDA, "dpq_store_create: control init failed");
+  return DPQ_OK;
+}
+
 extern "C" int dpq_store_create(int device, int n_layers, const dpq_layer_desc* descs, dpq_store** out) {
-  if (!out || n_layers < 1 || !descs) return set_err(DPQ_ERR_ARG, "dpq_store_create: bad arguments");
+  if (!out || n_layers < 0 || (n_layers > 0 && !descs)) return set_err(DPQ_ERR_ARG, "dpq_store_create: bad arguments");
   *out = nullptr;
   CK(cudaSetDevice(device));
   TRY(set_kernel_attrs());
@@ -367,76 +454,22 @@ extern "C" int dpq_store_create(int device, int n_layers, const dpq_layer_desc* 
     return code;
   };
   for (int i = 0; i < n_layers; ++i) {
-    const dpq_layer_desc& d = descs[i];
-    if (d.rows < 1 || d.cols < 1 || d.n_bits < 2 || d.n_bits > 8 || d.b_min < 1 || d.b_min > d.n_bits ||
-        (d.code_bytes < 0 || d.code_bytes > 2) || !d.codes || !d.lo || !d.hi)
-      return fail(set_err(DPQ_ERR_ARG, "dpq_store_create: bad layer %d", i));
-    DevLayer L{};
-    L.rows = d.rows;
-    L.cols = d.cols;
-    L.n_bits = d.n_bits;
-    L.b_min = d.b_min;
-    L.n_tiles = cdiv(d.rows, kTileRows);
-    L.n_win = cdiv(d.cols, kWinCols);
-    L.plane_stride16 = (long long)L.n_win * L.n_tiles * (kTileBytes / 16);
-    const long long pbytes = dpq_planes_bytes(d.rows, d.cols, d.n_bits);
-    void* planes = nullptr;
-    if (s->arena.alloc(&planes, pbytes)) return fail(DPQ_ERR_CUDA);
-    const void* codes_dev = d.codes;
-    void* tmp = nullptr;
-    const size_t cbytes = d.code_bytes ? (size_t)d.rows * d.cols * d.code_bytes
-                                       : ((size_t)d.rows * d.cols * d.n_bits + 7) / 8;   // .dpqs packed
-    if (!d.codes_on_device) {
-      if (cudaMalloc(&tmp, cbytes) != cudaSuccess ||
-          cudaMemcpy(tmp, d.codes, cbytes, cudaMemcpyHostToDevice) != cudaSuccess)
-        return fail(set_err(DPQ_ERR_CUDA, "dpq_store_create: code upload failed"));
-      codes_dev = tmp;
-    }
-    const long long groups = (long long)L.n_tiles * 32 * L.n_win * kGroups;
-    const int blocks = (int)std::min<long long>((groups + 255) / 256, 65535LL * 16);
-    repack_kernel<<<blocks, 256>>>(codes_dev, d.code_bytes, d.rows, d.cols, d.n_bits, L.n_win, L.n_tiles,
-                                   reinterpret_cast<unsigned char*>(planes));
-    cudaError_t e = cudaDeviceSynchronize();
-    if (tmp) cudaFree(tmp);
-    if (e != cudaSuccess) return fail(set_err(DPQ_ERR_CUDA, "repack: %s", cudaGetErrorString(e)));
-    L.planes = reinterpret_cast<const uint4*>(planes);
-    // lo / span / hi, padded to whole tiles
-    const int rp = L.n_tiles * 32;
-    std::vector<float> lo(rp, 0.f), span(rp, 0.f), hi(rp, 0.f);
-    for (int r = 0; r < d.rows; ++r) {
-      lo[r] = d.lo[r];
-      hi[r] = d.hi[r];
-      span[r] = (float)((double)d.hi[r] - (double)d.lo[r]);
-    }
-    float *dlo, *dspan, *dhi;
-    if (s->arena.alloc_t(&dlo, rp) || s->arena.alloc_t(&dspan, rp) || s->arena.alloc_t(&dhi, rp))
-      return fail(DPQ_ERR_CUDA);
-    if (cudaMemcpy(dlo, lo.data(), rp * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(dspan, span.data(), rp * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(dhi, hi.data(), rp * 4, cudaMemcpyHostToDevice) != cudaSuccess)
-      return fail(set_err(DPQ_ERR_CUDA, "dpq_store_create: lo/hi upload failed"));
-    L.lo = dlo;
-    L.span = dspan;
-    s->layers.push_back(L);
-    s->hi.push_back(dhi);
-    s->plane_bytes.push_back(pbytes);
-    s->max_rows_pad = std::max(s->max_rows_pad, rp);
-    s->max_win = std::max(s->max_win, L.n_win);
-    s->max_tiles = std::max(s->max_tiles, L.n_tiles);
-    s->max_cols = std::max(s->max_cols, d.cols);
+    const int r = store_add_layer(s, descs[i], i);
+    if (r != DPQ_OK) return fail(r);
   }
-  if (s->scratch.make(s->arena, s->max_win, s->max_rows_pad, s->max_tiles) ||
-      s->arena.alloc_t(&s->ctl, 1) || s->arena.alloc_t(&s->sync, 2) || s->arena.alloc_t(&s->decision, 4) ||
-      s->arena.alloc_t(&s->ctr, 128) || s->arena.alloc_t(&s->gxa, kMaxOpLayers * kMaxK) ||
-      s->arena.alloc_t(&s->tr_bits, 4) || s->arena.alloc_t(&s->tr_est, 4) ||
-      s->arena.alloc_t(&s->tr_exact, 4) || s->arena.alloc_t(&s->est_buf, s->max_cols))
-    return fail(DPQ_ERR_CUDA);
-  Control c{};
-  c.mode = MODE_DYNAMIC;
-  if (cudaMemcpy(s->ctl, &c, sizeof(c), cudaMemcpyHostToDevice) != cudaSuccess)
-    return fail(set_err(DPQ_ERR_CUDA, "dpq_store_create: control init failed"));
+  if (n_layers > 0) {
+    const int r = store_make_scratch(s);
+    if (r != DPQ_OK) return fail(r);
+  }
   *out = s;
   return DPQ_OK;
+}
+
+extern "C" int dpq_store_append(dpq_store* s, int n_layers, const dpq_layer_desc* descs) {
+  if (!s || n_layers < 1 || !descs) return set_err(DPQ_ERR_ARG, "dpq_store_append: bad arguments");
+  CK(cudaSetDevice(s->device));
+  for (int i = 0; i < n_layers; ++i) TRY(store_add_layer(s, descs[i], (int)s->layers.size()));
+  return store_make_scratch(s);
 }
 
 extern "C" int dpq_store_destroy(dpq_store* s) {

@@ -83,6 +83,36 @@ class DeviceStore:
         self._fin = weakref.finalize(self, _destroy, "dpq_store_destroy", h.value)
         return self
 
+    @staticmethod
+    def empty(device=None):
+        """A store filled layer by layer with ``append`` (streaming build: the
+        caller frees each layer's codes before generating the next)."""
+        import torch
+        self = DeviceStore.__new__(DeviceStore)
+        self.device = torch.device(device if device is not None else _lib.torch_device())
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.call("dpq_store_create", self.device.index, 0, None, C.byref(h))
+        self.handle = h
+        self.shapes, self.bits = [], []
+        self._fin = weakref.finalize(self, _destroy, "dpq_store_destroy", h.value)
+        return self
+
+    def append(self, codes, lo, hi, n_bits: int, b_min: int):
+        """Append one layer from device-resident codes (uint16 / uint8 / int16
+        torch tensor); repacked into bitplanes on the device right away."""
+        import torch
+        lo = np.ascontiguousarray(lo, dtype=np.float32)
+        hi = np.ascontiguousarray(hi, dtype=np.float32)
+        rows, cols = codes.shape
+        d = (_lib.LayerDesc * 1)()
+        d[0] = _lib.LayerDesc(rows, cols, n_bits, b_min, codes.element_size(), 1, codes.data_ptr(),
+                              lo.ctypes.data, hi.ctypes.data)
+        with torch.cuda.device(self.device):
+            _lib.call("dpq_store_append", self.handle, 1, d)
+        self.shapes.append((rows, cols))
+        self.bits.append((b_min, n_bits))
+
     def close(self):
         self._fin()
 

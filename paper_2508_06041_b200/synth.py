@@ -43,7 +43,11 @@ def random_device_model(cfg: M.ModelConfig, n_bits: int, b_min: int, seed: int =
     lm_head = (rng.normal(0.0, 1.0, (cfg.vocab, d)) * (0.1 / np.sqrt(d))).astype(np.float32)
     gen = torch.Generator(device=dev)
     gen.manual_seed(seed)
-    specs, shapes, host, sspecs = [], {}, {}, []
+    shapes, host = {}, {}
+    # streaming build: each layer is generated, quantized and repacked into the
+    # store's bitplanes before the next one exists (full-depth 70B fits)
+    ds = Q.DeviceStore.empty(dev)
+    sds = Q.DeviceStore.empty(dev) if shard is not None else None
     for lid in M.layer_ids(cfg):
         rows, cols = M.layer_shape(cfg, lid)
         W = torch.randn((rows, cols), generator=gen, device=dev, dtype=torch.float32)
@@ -54,6 +58,8 @@ def random_device_model(cfg: M.ModelConfig, n_bits: int, b_min: int, seed: int =
         _lib.call("dpq_quantize_device", dev.index, C.c_void_p(W.data_ptr()), rows, cols, n_bits,
                   C.c_void_p(codes.data_ptr()), C.c_void_p(lo.data_ptr()), C.c_void_p(hi.data_ptr()),
                   _lib.stream_ptr())
+        del W
+        lo_h, hi_h = lo.cpu().numpy(), hi.cpu().numpy()
         if shard is not None:
             from . import tp as TP
             world, rank = shard
@@ -62,24 +68,19 @@ def random_device_model(cfg: M.ModelConfig, n_bits: int, b_min: int, seed: int =
             sc[: r1 - r0] = codes[r0:r1]
             slo = np.zeros(per, dtype=np.float32)
             shi = np.zeros(per, dtype=np.float32)
-            slo[: r1 - r0] = lo[r0:r1].cpu().numpy()
-            shi[: r1 - r0] = hi[r0:r1].cpu().numpy()
-            sspecs.append((sc, slo, shi, n_bits, b_min))
-        del W
-        lo_h, hi_h = lo.cpu().numpy(), hi.cpu().numpy()
-        specs.append((codes, lo_h, hi_h, n_bits, b_min))
+            slo[: r1 - r0] = lo_h[r0:r1]
+            shi[: r1 - r0] = hi_h[r0:r1]
+            sds.append(sc, slo, shi, n_bits, b_min)
+            del sc
+        ds.append(codes, lo_h, hi_h, n_bits, b_min)
         shapes[lid] = (rows, cols)
         if lid.block < keep_host_blocks:
             host[lid] = Q.QuantizedLayer(codes.cpu().numpy().view(np.uint16), n_bits, b_min, lo_h, hi_h)
+        del codes
     torch.cuda.synchronize()
-    ds = Q.DeviceStore.from_device_codes(specs, dev)
-    del specs
     torch.cuda.empty_cache()
     store = Q.DeviceBitPlaneStore(cfg.hash(), n_bits, b_min, shapes, ds)
     if shard is not None:
-        sds = Q.DeviceStore.from_device_codes(sspecs, dev)
-        del sspecs
-        torch.cuda.empty_cache()
         return M.ModelWeights(cfg, embed, lm_head, {}), store, host, sds
     return M.ModelWeights(cfg, embed, lm_head, {}), store, host
 

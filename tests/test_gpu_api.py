@@ -4,6 +4,7 @@ selector, forced bits and projection shapes are validated before any device
 work, and the public API's G defaults to f32 (the reference's G is float64)."""
 
 import copy
+import os
 import pickle
 
 import numpy as np
@@ -97,3 +98,39 @@ def test_projection_shape_checked(small):
 def test_public_api_defaults_to_f32_G(small):
     import inspect
     assert inspect.signature(R.DecodeEngine).parameters["g_dtype"].default == "f32"
+
+
+def test_integration_stub_runs_on_reference_shaped_objects(tmp_path):
+    """The ctypes stub of INTEGRATION.md §2, executed as written against
+    reference-shaped objects (BitPlaneStore.layers: LayerId -> QuantizedLayer
+    with codes / n_bits / b_min / lo / hi), gives the oracle's gemv."""
+    import re
+    import sys
+    import types
+    import ctypes as C
+    import torch
+    from oracle import dpq_oracle as O
+    from paper_2508_06041_b200 import _lib
+    text = open(os.path.join(os.path.dirname(__file__), "..", "INTEGRATION.md")).read()
+    code = re.search(r"```python\n(# dpq/_b200\.py.*?)```", text, re.S).group(1)
+    code = code.replace('C.CDLL("libdpq_b200.so")', f'C.CDLL({_lib.LIB_PATH!r})')
+    fake = types.ModuleType("dpq")
+    fake.model = types.ModuleType("dpq.model")
+    fake.model.KINDS = M.KINDS
+    sys.modules.setdefault("dpq", fake)
+    sys.modules.setdefault("dpq.model", fake.model)
+    ns = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    cfg = M.ModelConfig(n_blocks=2, d_model=64, n_heads=4, d_ff=96, seq_cap=16)
+    store = Q.quantize_model(M.init_model(1, cfg), 5, 3)
+    handle, index = ns["device_store"](store)
+    rng = np.random.default_rng(2)
+    for lid in list(store.layers)[::3]:
+        q = store.layers[lid]
+        x = torch.as_tensor(rng.standard_normal(q.shape[1]), dtype=torch.float32, device="cuda")
+        y = torch.empty(q.shape[0], dtype=torch.float32, device="cuda")
+        ns["gemv"](handle, index, lid, 4, x.data_ptr(), y.data_ptr())
+        torch.cuda.synchronize()
+        ref = O.gemv(O.as_layer(q), 4, x.double().cpu().numpy())
+        np.testing.assert_allclose(y.cpu().numpy(), ref, rtol=0, atol=1e-5 * np.abs(ref).max())
+    _lib.load().dpq_store_destroy(handle)
