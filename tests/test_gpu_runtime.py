@@ -468,3 +468,61 @@ def test_trace_pulled_lazily_keeps_positions(report_setup):
     assert [s.step for s in b.steps] == [4, 5, 6, 8, 9]
     assert [s.bits for s in a.steps] == [s.bits for s in b.steps]
     assert a.estimator_ops == b.estimator_ops > 0
+
+
+@pytest.mark.parametrize("kind", ["flag_kernel", "per_op_graph"])
+def test_non_engine_session_kinds_match_oracle(monkeypatch, kind):
+    """The decode paths used when the TMA engine declines a shape
+    (DPQ_ENGINE=0 here): the persistent flag-linked step_kernel (session kind
+    1) and the multi-kernel op graph (kind 0). Logits vs the oracle under
+    forced replay, free-run decisions under the eps rule."""
+    from paper_2508_06041_b200 import _lib
+    monkeypatch.setenv("DPQ_ENGINE", "0")
+    cfg = M.ModelConfig(n_blocks=2, d_model=256, n_heads=4, d_ff=512, vocab=256, seq_cap=64, n_kv_heads=2)
+    w = M.init_model(5, cfg)
+    store = Q.quantize_model(w, 5, 3)
+    plan = synthetic_projection_plan(store, {l: (3, 4) for l in store.layers}, k=32, seed=2)
+    toks = np.random.default_rng(3).integers(0, 256, 16)
+    calibrate_T(w, store, plan, toks[:8])
+    ids = canon(store.layers)
+    eng = R.DecodeEngine(w, store, plan, g_dtype="f32", use_persistent=(kind == "flag_kernel"))
+    assert _lib.load().dpq_session_is_persistent(eng._h) == (1 if kind == "flag_kernel" else 0)
+    lg = [eng.step(int(toks[0]), dynamic=False)] + [eng.step(int(t)) for t in toks[1:]]
+    bits_d, _ = trace_arrays(eng.trace.steps, ids)
+    eo = oracle_engine(w, store, plan)
+    ref_free = [eo.step(int(toks[0]), dynamic=False)] + [eo.step(int(t)) for t in toks[1:]]
+    bits_o, est_o = trace_arrays(eo.records, ids)
+    assert not decision_mismatches(bits_d, bits_o, est_o, Ts(plan, ids), EPS_DECISION["f32"])
+    eo2 = oracle_engine(w, store, plan)
+    eo2.forced = [{O.key(l): int(b) for l, b in zip(ids, row)} for row in bits_d]
+    ref = [eo2.step(int(toks[0]), dynamic=False)] + [eo2.step(int(t)) for t in toks[1:]]
+    assert np.max(np.abs(np.array(lg) - np.array(ref))) <= LOGIT_TOL * np.max(np.abs(ref))
+    eng.close()
+
+
+def test_engine_e4m3_projection():
+    """fp8-e4m3 G (per-row scale) on the TMA engine: estimates within the e4m3
+    rounding of the oracle's, decisions under the e4m3 eps rule."""
+    from paper_2508_06041_b200 import _lib
+    cfg = M.ModelConfig(n_blocks=2, d_model=256, n_heads=4, d_ff=512, vocab=256, seq_cap=64, n_kv_heads=2)
+    w = M.init_model(6, cfg)
+    store = Q.quantize_model(w, 5, 3)
+    plan = synthetic_projection_plan(store, {l: (3, 4) for l in store.layers}, k=32, seed=4)
+    toks = np.random.default_rng(5).integers(0, 256, 16)
+    calibrate_T(w, store, plan, toks[:8])
+    ids = canon(store.layers)
+    eng = R.DecodeEngine(w, store, plan, g_dtype="e4m3")
+    assert _lib.load().dpq_session_is_persistent(eng._h) == 2
+    eo = oracle_engine(w, store, plan)
+    bits_o = []
+    eng.step(int(toks[0]), dynamic=False)
+    eo.step(int(toks[0]), dynamic=False)
+    for t in toks[1:]:
+        eo.step(int(t))
+        row = np.array([eo.records[-1].bits[O.key(l)] for l in ids], dtype=np.int8)
+        eng.step(int(t), forced_bits=row)             # same inputs: compare the estimates
+        bits_o.append(row)
+    _, est_d = trace_arrays(eng.trace.steps, ids)
+    _, est_o = trace_arrays(eo.records, ids)
+    np.testing.assert_allclose(est_d, est_o, rtol=3e-2)
+    eng.close()
