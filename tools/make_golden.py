@@ -232,8 +232,46 @@ def cfg1_vectors():
     np.savez_compressed(os.path.join(OUT, "cfg1_vectors.npz"), **out)
 
 
+def calib_vectors():
+    """Offline calibration on the reference:
+    collect_error_samples (estimator.py:132-165) on a small GQA-free model
+    at max bits 5 with (3,4) / (4,5) pairs, and calibrate_projection
+    (estimator.py:208-264) of two layers' projections on those samples."""
+    mc = M.ModelConfig(n_blocks=2, d_model=64, n_heads=4, d_ff=128, vocab=256, seq_cap=64)
+    w = M.init_model(3, mc)
+    store = Q.quantize_model(w, 6, 3)
+    ids = M.layer_ids(mc)
+    pairs = {lid: ((3, 4) if i % 2 == 0 else (4, 5)) for i, lid in enumerate(ids)}
+    max_bits = {lid: 5 for lid in ids}
+    toks = np.frombuffer(generate_text(1, 4096).encode(), dtype=np.uint8).astype(np.int64)
+    calib = sample_chunks(toks, 12, 4, seed=2)
+    samples = E.collect_error_samples(w, store, pairs, max_bits, calib)
+    out = {"calib": np.array(calib)}
+    for lid in ids:
+        s = samples[lid]
+        out[f"{lid.name}/errors"] = s.errors
+        out[f"{lid.name}/norms"] = s.norms
+        out[f"{lid.name}/inputs"] = s.inputs
+    for lid in (ids[0], ids[6]):
+        l, h = pairs[lid]
+        est = E.build_projection(store.layers[lid], l, h, 8, 5)
+        cal, hist, warn = E.calibrate_projection(est, samples[lid].inputs, samples[lid].errors, epochs=40)
+        out[f"{lid.name}/G0"] = est.G
+        out[f"{lid.name}/G"] = cal.G
+        out[f"{lid.name}/history"] = np.array(hist)
+        out[f"{lid.name}/warning"] = np.array([int(warn)])
+        lin = E.fit_linear(samples[lid].errors, samples[lid].norms)
+        out[f"{lid.name}/linear"] = (np.array([lin.slope, lin.intercept, lin.r2]) if lin is not None
+                                     else np.array([np.nan, np.nan, np.nan]))
+    np.savez_compressed(os.path.join(OUT, "calib_vectors.npz"), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "calib":
+        calib_vectors()
+        sys.exit(0)
     quant_vectors()
     cfg1_vectors()
     toy_pipeline()
+    calib_vectors()
