@@ -63,7 +63,7 @@ def model_config(name):
         return M.ModelConfig(80, 8192, 64, 28672, vocab=256, seq_cap=1024, n_kv_heads=8), 6, 3
     if name == "llama2_70b_slice":
         return M.ModelConfig(8, 8192, 64, 28672, vocab=256, seq_cap=1024, n_kv_heads=8), 6, 3
-    return M.ModelConfig(2, 512, 8, 1792, vocab=256, seq_cap=1024), 4, 3
+    return M.ModelConfig(2, 512, 8, 1792, vocab=256, seq_cap=512), 4, 3
 
 
 def pairs_for_target(store, target):
@@ -214,6 +214,18 @@ def build_workload(args, rank=0, world=1, keep_host_blocks=0):
     the engine so ~(target - l) of the decisions are high."""
     from paper_2508_06041_b200 import synth
     cfg, n_bits, b_min = model_config(args.config)
+    if args.config == "cfg1":
+        # the reference's own cfg1 (SURVEY 8d): init_model(0), quantize_model(4, 3)
+        # and the plan its planner built (tests/golden/plans/cfg1_dp_t3.5.json)
+        from paper_2508_06041_b200 import model as M, quant as Q, runtime as R, tp as TP
+        weights = M.init_model(0, cfg)
+        store = Q.quantize_model(weights, n_bits, b_min)
+        plan = R.load_plan(os.path.join(ROOT, "tests", "golden", "plans", "cfg1_dp_t3.5.json"), store)
+        ids = store.ordered_ids()
+        pairs = {l: tuple(plan.layers[l].pair) for l in ids}
+        host = {l: store.layers[l] for l in ids} if keep_host_blocks else {}
+        sds = TP.shard_store(store, world, rank) if world > 1 else None
+        return cfg, n_bits, b_min, weights, store, host, sds, pairs, plan
     res = synth.random_device_model(cfg, n_bits, b_min, seed=1234, keep_host_blocks=keep_host_blocks,
                                     shard=(world, rank) if world > 1 else None)
     weights, store, host = res[:3]

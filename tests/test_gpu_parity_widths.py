@@ -136,3 +136,39 @@ def test_device_greedy_loop_matches_oracle(width_setup):
         assert not decision_mismatches(bits_d[s:s + 1], bits_o[s:s + 1], est_o[s:s + 1], T, EPS_DECISION["f32"])
         if not np.array_equal(bits_d[s], bits_o[s]):
             break
+
+
+def test_cfg1_reference_planned_decode():
+    """cfg1 with the plan the REFERENCE planner built
+    (tools/make_golden.py cfg1_plan: build_dp_plan(budget 4.0, target 3.5,
+    hybrid, k=64, calibrate=True)): the device's greedy decode (f32 G)
+    equals the reference DecodeEngine's tokens and effective bits up to the
+    first eps-tie of a decision (decisions checked against the oracle's)."""
+    import os
+    from conftest import GOLDEN
+    from paper_2508_06041_b200 import quant as Q
+    g = np.load(os.path.join(GOLDEN, "cfg1_plan_decode.npz"))
+    cfg = M.ModelConfig(n_blocks=2, d_model=512, n_heads=8, d_ff=1792, vocab=256, seq_cap=512)
+    w = M.init_model(0, cfg)
+    store = Q.quantize_model(w, 4, 3)
+    plan = R.load_plan(os.path.join(GOLDEN, "plans", "cfg1_dp_t3.5.json"), store)
+    prompt = g["prompt"]
+    out, tr = R.decode(w, store, plan, prompt, 64, store_hash=str(g["store_hash"][0]), g_dtype="f32")
+    ref = g["tokens"].tolist()
+    ids = store.ordered_ids()
+    # the oracle's decisions and estimates along the device's own trajectory
+    eo = O.Engine(w, store.layers, plan.layers, plan.M)
+    O.decode(eo, prompt, 64)
+    bits_o, est_o = trace_arrays(eo.records, ids)
+    bits_d, _ = trace_arrays(tr.steps, ids)
+    T = np.array([plan.layers[l].T for l in ids])
+    n_same = 0
+    for s in range(64):
+        assert not decision_mismatches(bits_d[s:s + 1], bits_o[s:s + 1], est_o[s:s + 1], T, EPS_DECISION["f32"])
+        if not np.array_equal(bits_d[s], bits_o[s]):
+            break
+        assert out[s] == ref[s], (s, out[:s + 1], ref[:s + 1])
+        n_same += 1
+    assert n_same >= 8
+    eff = np.array([s.effective_bits for s in tr.steps])
+    np.testing.assert_allclose(eff[:n_same], g["eff"][:n_same], rtol=0, atol=1e-12)

@@ -266,12 +266,46 @@ def calib_vectors():
     np.savez_compressed(os.path.join(OUT, "calib_vectors.npz"), **out)
 
 
+def cfg1_plan():
+    """cfg1 with the reference's own planner: init_model(0),
+    quantize_model(4, 3), corpus generate_text(0, 16384), calib
+    sample_chunks(32, 8, seed 0), sensitivity profile, build_dp_plan(budget
+    4.0, target 3.5, hybrid, k=64, seed 0, calibrate=True) with the toy
+    config's fit hyper-parameters; the plan JSON plus the reference
+    DecodeEngine's greedy decode of 64 tokens from toks[:16]."""
+    from dpq.cli import default_alpha
+    from dpq import fitter as F
+    mc = M.ModelConfig(n_blocks=2, d_model=512, n_heads=8, d_ff=1792, vocab=256, seq_cap=512)
+    weights = M.init_model(0, mc)
+    store = Q.quantize_model(weights, 4, 3)
+    tmp = "/tmp/_golden_cfg1.dpqs"
+    Q.save_store(store, tmp)
+    store_hash = Q.file_hash(tmp)
+    tokens = np.frombuffer(generate_text(0, 16384).encode(), dtype=np.uint8).astype(np.int64)
+    calib = sample_chunks(tokens, 32, 8, 0)
+    prof = S.profile(weights, store, calib, store_hash=store_hash)
+    hyper = F.FitConfig(epochs=5, lr=0.01, alpha=default_alpha(3.5), batch_size=2, seed=0)
+    plan, _, _ = P.build_dp_plan(weights, store, prof, calib, 4.0, 3.5, estimator_mode="hybrid",
+                                 use_async=False, k=64, seed=0, calibrate=True, hyper=hyper,
+                                 store_hash=store_hash)
+    os.makedirs(os.path.join(OUT, "plans"), exist_ok=True)
+    R.save_plan(plan, os.path.join(OUT, "plans", "cfg1_dp_t3.5.json"))
+    out, tr = R.decode(weights, store, plan, tokens[:16], 64, store_hash=store_hash)
+    np.savez_compressed(os.path.join(OUT, "cfg1_plan_decode.npz"), tokens=np.array(out),
+                        prompt=tokens[:16], eff=np.array([s.effective_bits for s in tr.steps]),
+                        store_hash=np.array([store_hash]), avg_p=np.array([P.plan_effective_bits(plan)]))
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     if len(sys.argv) > 1 and sys.argv[1] == "calib":
         calib_vectors()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "cfg1_plan":
+        cfg1_plan()
+        sys.exit(0)
     quant_vectors()
     cfg1_vectors()
     toy_pipeline()
     calib_vectors()
+    cfg1_plan()
