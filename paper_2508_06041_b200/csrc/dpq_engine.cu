@@ -212,10 +212,18 @@ struct Prog {
 
 __device__ __forceinline__ void st_tag_all(const Prog& P, u64* p, float v, unsigned e) {
   const u64 w = ((u64)e << 32) | __float_as_uint(v);
+  if (P.tp_size == 1) {
+    __stcg(p, w);
+    return;
+  }
   for (int q = 0; q < P.tp_size; ++q)
     __stcg(reinterpret_cast<u64*>(reinterpret_cast<char*>(p) + P.peer_off[q]), w);
 }
 __device__ __forceinline__ void red_all(const Prog& P, u64* p, u64 v) {
+  if (P.tp_size == 1) {      // single GPU: gpu scope
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+    return;
+  }
   for (int q = 0; q < P.tp_size; ++q)
     asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" :: "l"(reinterpret_cast<char*>(p) + P.peer_off[q]), "l"(v)
                  : "memory");
