@@ -222,3 +222,21 @@ def load_weights(manifest_path: str) -> ModelWeights:
     lm_head = expect("lm_head", (config.vocab, config.d_model))
     linears = {lid: expect(lid.name, layer_shape(config, lid)) for lid in layer_ids(config)}
     return ModelWeights(config, embed, lm_head, linears)
+
+
+def forward(weights, tokens, provider=None, want_tape: bool = False):
+    """model.py:286-345 (fp64 device graph: graph.forward)."""
+    from . import graph
+    return graph.forward(weights, tokens, provider, want_tape)
+
+
+def backward(weights, tokens, provider=None):
+    """model.py:382-460 (fp64 device graph: graph.backward)."""
+    from . import graph
+    return graph.backward(weights, tokens, provider)
+
+
+def teacher_forced_loss(weights, tokens, provider=None):
+    """model.py:363-372 (graph.teacher_forced_loss)."""
+    from . import graph
+    return graph.teacher_forced_loss(weights, tokens, provider)

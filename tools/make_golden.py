@@ -296,8 +296,37 @@ def cfg1_plan():
                         store_hash=np.array([store_hash]), avg_p=np.array([P.plan_effective_bits(plan)]))
 
 
+def model_vectors():
+    """model.forward / teacher_forced_loss / backward (model.py:286-460) on a
+    toy config, full-precision and 4-bit dequantized providers."""
+    mc = M.ModelConfig(n_blocks=2, d_model=32, n_heads=4, d_ff=64, vocab=256, seq_cap=64)
+    w = M.init_model(0, mc)
+    store = Q.quantize_model(w, 6, 3)
+    toks = np.random.default_rng(4).integers(0, 256, 10)
+    out = {"tokens": toks}
+    for name, prov in (("fp", None), ("q4", lambda lid: Q.dequantize(store.layers[lid], 4))):
+        lg, tape = M.forward(w, toks, prov, want_tape=True)
+        out[f"{name}/logits"] = lg
+        out[f"{name}/x_final"] = tape.x_final
+        for b, bt in enumerate(tape.blocks):
+            for f in ("n1", "attn_cat", "h", "probs", "x_mid"):
+                out[f"{name}/b{b}/{f}"] = getattr(bt, f)
+        loss, ppl, per = M.teacher_forced_loss(w, toks, prov)
+        out[f"{name}/tfl"] = np.array([loss, ppl])
+        out[f"{name}/per_token"] = per
+        bl, bundle, _ = M.backward(w, toks, prov)
+        out[f"{name}/bwd_loss"] = np.array([bl])
+        for lid in M.layer_ids(mc):
+            out[f"{name}/wg/{lid.name}"] = bundle.weight_grads[lid]
+            out[f"{name}/og/{lid.name}"] = bundle.output_grads[lid]
+    np.savez_compressed(os.path.join(OUT, "model_vectors.npz"), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "model":
+        model_vectors()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "calib":
         calib_vectors()
         sys.exit(0)
@@ -309,3 +338,4 @@ if __name__ == "__main__":
     toy_pipeline()
     calib_vectors()
     cfg1_plan()
+    model_vectors()
