@@ -134,3 +134,18 @@ def test_integration_stub_runs_on_reference_shaped_objects(tmp_path):
         ref = O.gemv(O.as_layer(q), 4, x.double().cpu().numpy())
         np.testing.assert_allclose(y.cpu().numpy(), ref, rtol=0, atol=1e-5 * np.abs(ref).max())
     _lib.load().dpq_store_destroy(handle)
+
+
+def test_fixed_point_range_is_flagged(small):
+    """Activations far outside the fixed-point range of the engine's packed
+    partial sums / estimator words (|S_w| >= 2^33, |G.x| 2^fb >= 2^47) raise
+    DeviceError (DPQ_ERR_RANGE) instead of wrapping silently."""
+    from paper_2508_06041_b200 import _lib
+    w, store, plan = small
+    big = M.ModelWeights(w.config, w.embed * np.float32(1e9), w.lm_head, w.linears)
+    eng = R.DecodeEngine(big, store, plan)
+    assert _lib.load().dpq_session_is_persistent(eng._h) == 2
+    with pytest.raises(_lib.DeviceError, match="range"):
+        eng.step(1, dynamic=False)
+        eng.step(2, dynamic=True)
+    eng.close()
