@@ -179,6 +179,7 @@ struct dpq_store {
   float* tr_exact = nullptr;
   float* est_buf = nullptr;          // exact-estimator input copy
   int max_rows_pad = 0, max_win = 0, max_tiles = 0, max_cols = 0;
+  std::vector<void*> gemv_progs;     // single-op engine programs per layer (dpq_gemv)
 };
 
 struct dpq_plan {
@@ -188,7 +189,13 @@ struct dpq_plan {
   Arena arena;
   int any_prev = 0;
   std::vector<int> gt_fb;            // per layer: fixed-point fraction bits of the engine's G.x sums
+  std::vector<void*> gemv_progs;     // single-op engine programs per layer (dpq_select_gemv)
 };
+
+int gemv_engine_run(dpq_store* s, dpq_plan* p, int li, int b, const float* x, float* y, int32_t* bit_out,
+                    float* est_out, cudaStream_t st, bool* used);
+void gemv_progs_release(std::vector<void*>& cache);
+
 
 struct OpStep {
   enum Kind { OP, FINALIZE, DECIDE_EXACT, PREP_EST } kind;
@@ -476,6 +483,7 @@ extern "C" int dpq_store_destroy(dpq_store* s) {
   if (!s) return DPQ_OK;
   cudaSetDevice(s->device);
   cudaDeviceSynchronize();
+  gemv_progs_release(s->gemv_progs);
   s->arena.release();
   delete s;
   return DPQ_OK;
@@ -558,6 +566,9 @@ extern "C" int dpq_gemv(dpq_store* s, int layer, int b, const float* x_dev, floa
   S.l = S.h = S.prefill_bit = b;
   S.sentinel = 1;
   S.T = INFINITY;
+  bool used = false;
+  TRY(gemv_engine_run(s, nullptr, layer, b, x_dev, y_dev, nullptr, nullptr, (cudaStream_t)stream, &used));
+  if (used) return DPQ_OK;
   OpDesc D = single_op(s, layer, S, x_dev, y_dev);
   D.layer[0].trace_idx = -1;
   D.n_trace = 0;
@@ -697,6 +708,7 @@ extern "C" int dpq_plan_destroy(dpq_plan* p) {
   if (!p) return DPQ_OK;
   cudaSetDevice(p->store->device);
   cudaDeviceSynchronize();
+  gemv_progs_release(p->gemv_progs);
   p->arena.release();
   delete p;
   return DPQ_OK;
@@ -713,6 +725,11 @@ extern "C" int dpq_select_gemv(dpq_plan* p, int layer, const float* x_dev, const
   DevSel S = p->sel[layer];
   const bool exact_est = S.sentinel == 0 && S.est_kind == EST_EXACT;
   const bool want_exact = exact_out_dev != nullptr && S.l != S.h;
+  if (!exact_est && !want_exact && (est_in_dev == nullptr || est_in_dev == x_dev)) {
+    bool used = false;
+    TRY(gemv_engine_run(s, p, layer, 0, x_dev, y_dev, bit_out_dev, est_out_dev, st, &used));
+    if (used) return DPQ_OK;
+  }
   reset_trace1<<<1, 32, 0, st>>>(s->tr_bits, s->tr_est, s->tr_exact);
   CK(cudaGetLastError());
   if (exact_est && est_in_dev) {

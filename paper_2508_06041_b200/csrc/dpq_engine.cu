@@ -73,7 +73,7 @@ constexpr int kCntShift = 56;
 constexpr long long kFxBias = 1ll << 47;
 constexpr uint32_t kLut = 0x20000;        // the window LUT (absolute shared address)
 
-enum { ST_BEGIN = 0, ST_OP = 1, ST_HEAD = 3 };
+enum { ST_BEGIN = 0, ST_OP = 1, ST_HEAD = 3, ST_OUT = 4 };
 enum { SRC_IMM = 0, SRC_PREV_STEP = 1, SRC_PREV_BLOCK = 2 };
 enum { FEED_CUR = 0, FEED_CURFB = 1, FEED_PREV = 2 };
 enum { ERR_RANGE = 1 };
@@ -118,6 +118,7 @@ struct alignas(16) Op {
   int add;                 // residual add: out = res_in + y
   int attn_in;             // input = attention of the q|k|v op (out of stage in_stage)
   int push;                // output published to every tensor-parallel rank (row-shard all-gather)
+  int plain_io;            // single-op programs: input = plain floats at Prog.embed, output = plain floats at Prog.y_out
   int in_stage;            // stage (index in the step) publishing `in`
   int res_stage;           // stage publishing res_in
   int inst;                // input instance: statistics + estimator feeds
@@ -184,6 +185,16 @@ struct Prog {
   const u64* xfinal;       // tagged residual after the last block
   int final_stage;
   float* logits;
+  // single-op programs (dpq_gemv / dpq_select_gemv): BEGIN reads the plain
+  // input from `embed` (token 0), ST_OUT writes the op's output rows as plain
+  // floats to y_out and the decision / estimate to bit_out / est_out
+  float* y_out;
+  int32_t* bit_out;
+  float* est_out;
+  int out_rows, out_op_stage;
+  int gemv_mode;           // > 0: single-op program; the step runs in this mode (MODE_*)
+  int gemv_force;          // 1: the op's bit is gemv_bit (dpq_gemv); 0: the selector decides
+  int gemv_bit;
   float* const* kc;        // [n_blocks] -> [seq_cap][dkv]
   float* const* vc;
   u64* slot;               // [2 (stage parity)][slot_half]: per op row (hi, lo) packed fixed-point
@@ -393,6 +404,7 @@ struct Smem {
   unsigned slot_off[kMaxSlots];
   volatile int dec_op;               // decisions of ops < dec_op are published
   int dec_fin[kDecRing][kMaxOpLayers];
+  float dec_est[kDecRing];           // first layer's estimate of the op (single-op programs)
   volatile int cons_ops;             // ops finished by the consumers
   volatile unsigned cons_gs;         // consumer stages finished (global stage number + 1)
   volatile int step_ready;           // steps whose control block is in ctl[]
@@ -403,6 +415,7 @@ struct Smem {
   alignas(16) float attn_q[128];     // RoPE'd q of the current attention unit
   alignas(16) float attn_m[4][132];  // per-warp (o[hd], m, l) of the unit
   alignas(16) float xw[kWinCols];    // the op's input window
+  signed char gemv_bits[4];          // single-op programs: the forced bit (ECtl.forced_bits -> here)
   uint2 ctask[2][kMaxTasks];         // consumer task lists (by op parity)
   uint2 ptask[kMaxTasks];            // producer task list
   const uint4* psrc[kMaxTasks];      // producer: plane-0 address of each task's tile
@@ -1122,7 +1135,7 @@ __device__ __forceinline__ Epi op_epi(const Prog& P, const Op& O, unsigned epoch
 // the same decisions without another exchange).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op& O, const I3& nb, I3& fin,
-                                          int cta, unsigned step_base, u64* rdbg) {
+                                          int cta, unsigned step_base, u64* rdbg, float* est0) {
   const int lane = threadIdx.x & 31;
   const bool dyn = C.mode == MODE_DYNAMIC;
   // every estimating layer's words in one poll: lane holds packed G.x words
@@ -1208,6 +1221,7 @@ __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op
       if (!C.force) bit = est > L.T ? L.h : L.l;                                              // strict > (runtime.py:192)
     }
     fin.set(li, bit);
+    if (li == 0) *est0 = has ? (float)est : CUDART_NAN_F;
     if (lane == 0 && dyn && cta == 0 && L.trace >= 0 && P.n_trace > 0 && C.trace_step < P.max_steps) {
       const size_t o = (size_t)C.trace_step * P.n_trace + L.trace;
       P.tr_bits[o] = (signed char)bit;
@@ -1386,7 +1400,19 @@ __device__ __forceinline__ void cons_op(const Prog& P, Smem& sm, int oi, int op_
     attn_merge(P, C, W.w, e_in, sm.xw);
   } else {
     feed_prefetch(P, C, O, W, fp);
-    load_window(O.in, O.cols, W.w, e_in, sm.xw);
+    if (O.plain_io) {                    // the caller's x (complete before the launch)
+      if (tid < 128) {
+        const int c0 = W.w * kWinCols + 4 * tid;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c0 + 4 <= O.cols) v = *reinterpret_cast<const float4*>(P.embed + c0);
+        else
+          for (int j = 0; j < 4; ++j)
+            if (c0 + j < O.cols) (&v.x)[j] = P.embed[c0 + j];
+        *reinterpret_cast<float4*>(sm.xw + 4 * tid) = v;
+      }
+    } else {
+      load_window(O.in, O.cols, W.w, e_in, sm.xw);
+    }
   }
   CSYNC();
   if (dbg && tid == 0) dbg[1] = gclock();
@@ -1466,12 +1492,14 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
         I3 fin = nb;
         u64* rdbg = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr;
         if (rdbg && lane == 0) rdbg[16] = gclock();
-        decide_op(P, C, O, nb, fin, cta, step_base, rdbg);
+        float est0 = CUDART_NAN_F;
+        decide_op(P, C, O, nb, fin, cta, step_base, rdbg, &est0);
         if (rdbg && lane == 0) rdbg[17] = gclock();
         if (lane == 0) {
           sm.dec_fin[oi % kDecRing][0] = fin.v0;
           sm.dec_fin[oi % kDecRing][1] = fin.v1;
           sm.dec_fin[oi % kDecRing][2] = fin.v2;
+          sm.dec_est[oi % kDecRing] = est0;
           __threadfence_block();
           sm.dec_op = oi + 1;
         }
@@ -1524,7 +1552,8 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
                   res = __uint_as_float((unsigned)xr);
                   v = res + v;
                 }
-                if (O.push) st_tag_all(P, O.out + o, v, epoch);
+                if (O.plain_io) P.y_out[o] = v;
+                else if (O.push) st_tag_all(P, O.out + o, v, epoch);
                 else st_tag(O.out + o, v, epoch);
               }
             }
@@ -1642,6 +1671,15 @@ __device__ __forceinline__ void begin_stage(const Prog& P, Smem& sm, int cta, in
     if (tid < (int)(sizeof(ECtl) / 4)) dst[tid] = __ldcg(src + tid);
   }
   CSYNC();
+  if (P.gemv_mode > 0 && tid == 0) {      // single-op program: this call's mode / bit
+    Cw.mode = P.gemv_mode;
+    Cw.force = P.gemv_force;
+    Cw.token = 0;
+    Cw.trace_step = 0;
+    sm.gemv_bits[0] = (signed char)P.gemv_bit;
+    Cw.forced_bits = sm.gemv_bits;
+  }
+  CSYNC();
   if (tid == 0) {
     __threadfence_block();
     sm.step_ready = step + 1;                   // the producer and reducer may run this step
@@ -1653,6 +1691,33 @@ __device__ __forceinline__ void begin_stage(const Prog& P, Smem& sm, int cta, in
     for (long long i = cta * NT + tid; i < P.set_stride; i += G * NT) { a[i] = 0; z[i] = 0; }
   }
   for (int i = cta * NT + tid; i < P.d; i += G * NT) st_tag(P.xe + i, __ldg(P.embed + (size_t)C.token * P.d + i), gs + 1u);
+}
+
+// ST_OUT (single-op programs): the op's tagged output -> plain floats, the
+// decision / estimate of its first layer, then the step count (last CTA).
+__device__ __noinline__ void out_stage(const Prog& P, const ECtl& C, Smem& sm, int cta, int G, unsigned e_out,
+                                       int oi_last) {
+  const int tid = threadIdx.x;
+  const u64* out = P.ops[0].out;
+  if (!P.ops[0].plain_io)
+    for (int i = cta * NT + tid; i < P.out_rows; i += G * NT) {
+      u64 x;
+      SPIN_UNTIL((x = ld_relaxed64(out + i), (unsigned)(x >> 32) == e_out), "gemv output", i, e_out);
+      P.y_out[i] = __uint_as_float((unsigned)x);
+    }
+  if (cta == 0 && tid == 0) {
+    const int e = (oi_last + kDecRing) % kDecRing;
+    if (P.bit_out) *P.bit_out = sm.dec_fin[e][0];
+    if (P.est_out) *P.est_out = sm.dec_est[e];
+  }
+  __threadfence();
+  CSYNC();
+  if (tid == 0) sm.head_last = atomicAdd(P.head_cnt, 1u) == (unsigned)G - 1;
+  CSYNC();
+  if (!sm.head_last || tid != 0) return;
+  __threadfence();
+  P.head_cnt[0] = 0u;
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" :: "l"(&P.ctl->n_steps_done), "r"(C.n_steps_done + 1) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -1714,6 +1779,7 @@ extern "C" __global__ void __maxnreg__(168) engine_kernel(const Prog Pk, int n_s
       } else {
         if (dbg && tid == 0) dbg[0] = gclock();
         if (st.x == ST_BEGIN) begin_stage(P, sm, cta, G, step, s0 + step, gs);
+        else if (st.x == ST_OUT) out_stage(P, sm.ctl[step & 1], sm, cta, G, step_base + (unsigned)P.out_op_stage + 1u, oi - 1);
         else head_stage(P, sm.ctl[step & 1], sm, lut, cta, G, step_base + (unsigned)P.final_stage + 1u);
         CSYNC();
         if (tid == 0) sm.cons_gs = gs + 1;

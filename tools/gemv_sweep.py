@@ -46,7 +46,8 @@ def timed(launch, n_launch, reps):
     try:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
-            launch(C.c_void_p(s.cuda_stream), 0, 1)          # warm (outside capture)
+            for i in range(n_launch):                          # warm every copy outside capture
+                launch(C.c_void_p(s.cuda_stream), i, 1)        # (first use builds its program)
             torch.cuda.synchronize()
             with torch.cuda.graph(g, stream=s):
                 for i in range(n_launch):
