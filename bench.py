@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--g-dtype", default="f16", choices=["f32", "f16", "e4m3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-static", action="store_true")
+    ap.add_argument("--async-estimators", dest="async_est", action="store_true",
+                    help="residual-fed layers past block 0 estimate from the previous step's input "
+                         "(build_dp_plan(use_async=True), estimator.py:267-272)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: N independent sequences, one per GPU (weak scaling); default N>1 is tensor "
                          "parallel decode of ONE sequence over the N ranks (strong scaling)")
@@ -231,7 +234,7 @@ def build_workload(args, rank=0, world=1, keep_host_blocks=0):
     weights, store, host = res[:3]
     sds = res[3] if world > 1 else None
     pairs, prefill, high = pairs_for_target(store, args.target)
-    plan = synth.projection_plan(store, pairs, prefill, k=64, seed=0, target=args.target)
+    plan = synth.projection_plan(store, pairs, prefill, k=64, seed=0, target=args.target, use_async=args.async_est)
     calib = np.random.default_rng(7).integers(0, cfg.vocab, 48)
     synth.calibrate_thresholds(weights, store, plan, calib, high_rate=high, g_dtype=args.g_dtype)
     return cfg, n_bits, b_min, weights, store, host, sds, pairs, plan
@@ -241,7 +244,9 @@ def config_dict(args, cfg, n_bits, b_min, pairs, ids, world):
     pr = sorted({tuple(p) for p in pairs.values()})
     return {"workload": f"{args.config}-shaped batch-1 greedy decode of one sequence, DP plan {args.target}-bit "
                         f"target, {' / '.join(f'({a},{b})' for a, b in pr)} pairs, k=64 projection selector "
-                        f"({args.g_dtype} G)" + (f", tensor parallel over {world} GPUs" if world > 1 else ""),
+                        f"({args.g_dtype} G)" + (", async (previous-step) estimators for residual-fed layers"
+                                                 if getattr(args, "async_est", False) else "")
+                        + (f", tensor parallel over {world} GPUs" if world > 1 else ""),
             "n_blocks": cfg.n_blocks, "d_model": cfg.d_model, "n_heads": cfg.n_heads,
             "n_kv_heads": cfg.kv_heads, "d_ff": cfg.d_ff, "vocab": cfg.vocab,
             "n_bits": n_bits, "b_min": b_min, "prompt": PROMPT,

@@ -86,9 +86,11 @@ def random_device_model(cfg: M.ModelConfig, n_bits: int, b_min: int, seed: int =
 
 
 def projection_plan(store, pairs: dict, prefill_bits: dict, k: int = E.DEFAULT_K, seed: int = 0,
-                    method: str = "dp", target: float = float("nan")) -> R.PrecisionPlan:
+                    method: str = "dp", target: float = float("nan"), use_async: bool = False) -> R.PrecisionPlan:
     """Projection estimator per dynamic layer, G = A (W_h - W_l), A ~ N(0,1)/sqrt(k)
-    seeded per layer; thresholds start at +inf (calibrate_thresholds sets them)."""
+    seeded per layer; thresholds start at +inf (calibrate_thresholds sets them).
+    use_async: residual-fed layers past block 0 estimate from the previous
+    input (estimator.py:267-272, 286; build_dp_plan(use_async=True))."""
     import torch
     ds = store.device_store()
     ids = store.ordered_ids()
@@ -105,7 +107,8 @@ def projection_plan(store, pairs: dict, prefill_bits: dict, k: int = E.DEFAULT_K
         dW -= ds.dequantize(i, l)
         G = (A @ dW).cpu().numpy()
         del dW
-        est = E.ErrorEstimator(E.ProjectionEstimator(G, k, seed), E.IMMEDIATE, (l, h))
+        src = E.resolve_input_source(lid) if use_async else E.IMMEDIATE
+        est = E.ErrorEstimator(E.ProjectionEstimator(G, k, seed), src, (l, h))
         layers[lid] = R.PlanLayer(lid, prefill_bits[lid], l + 0.5, (l, h), np.inf, 0.5, est)
     torch.cuda.empty_cache()
     return R.PrecisionPlan(method, target, float("nan"), layers, store.param_counts())
