@@ -52,7 +52,10 @@
 namespace dpq {
 namespace eng {
 
-constexpr int NCW = 10;            // consumer warps (12 warps per CTA: 3 per SMSP -> 168 registers)
+#ifndef DPQ_NCW
+#define DPQ_NCW 10
+#endif
+constexpr int NCW = DPQ_NCW;       // consumer warps (12 warps per CTA: 3 per SMSP -> 168 registers)
 constexpr int NW = NCW;
 constexpr int NT = NCW * 32;       // consumer threads
 constexpr int kRedWarp = NCW;      // reducer warp
@@ -529,6 +532,16 @@ __device__ __forceinline__ float4 ld_keep(const float* p, unsigned long long pol
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(policy));
   return r;
 }
+__device__ __forceinline__ uint4 ld_nc16_half(const void* p) {   // 8 bytes (x, y)
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return make_uint4(r.x, r.y, 0u, 0u);
+}
+__device__ __forceinline__ unsigned ld_nc4(const void* p) {
+  unsigned r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ uint4 ld_nc16(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -581,58 +594,70 @@ struct GRow {
   uint4 g[2];
   float scale;
 };
+// Lane l takes columns 4 l + 128 q + j (q, j < 4) of the window: the G loads
+// are coalesced per q and the window reads (xw) are conflict-free LDS.128.
 __device__ __forceinline__ void feed_row_load(const Feed& F, int w, int r, GRow& R) {
   const int lane = threadIdx.x & 31;
-  const size_t base = ((size_t)w * F.k + r) * kWinCols + 16 * lane;
+  const size_t base = ((size_t)w * F.k + r) * kWinCols + 4 * lane;
   R.scale = 1.f;
   if (F.dtype == G_F16) {
-    const uint4* g = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(F.G) + base);
-    R.g[0] = ld_nc16(g);
-    R.g[1] = ld_nc16(g + 1);
+    const __half* g = reinterpret_cast<const __half*>(F.G) + base;
+    uint2 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 t = ld_nc16_half(g + 128 * q);
+      v[q] = make_uint2(t.x, t.y);
+    }
+    R.g[0] = make_uint4(v[0].x, v[0].y, v[1].x, v[1].y);
+    R.g[1] = make_uint4(v[2].x, v[2].y, v[3].x, v[3].y);
   } else if (F.dtype == G_F32) {
     // 16 floats per lane: loaded in feed_row_dot (not held across the input wait)
   } else {   // e4m3 with a per-row scale
-    R.g[0] = ld_nc16(reinterpret_cast<const unsigned char*>(F.G) + base);
+    const unsigned char* g = reinterpret_cast<const unsigned char*>(F.G) + base;
+    R.g[0] = make_uint4(ld_nc4(g), ld_nc4(g + 128), ld_nc4(g + 256), ld_nc4(g + 384));
     R.scale = __ldg(F.gscale + r);
   }
 }
 // Window partial G[w][r] . x[w] from the loaded row (fp32 lanes + double warp sum).
 __device__ __forceinline__ double feed_row_dot(const Feed& F, int w, int r, const GRow& R, const float* xw) {
   const int lane = threadIdx.x & 31;
-  const float* xl = xw + 16 * lane;
   float s = 0.f;
-  if (F.dtype == G_F16) {
-    const __half2* ha = reinterpret_cast<const __half2*>(&R.g[0]);
-    const __half2* hb = reinterpret_cast<const __half2*>(&R.g[1]);
+  float4 x[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 u = __half22float2(ha[i]), v = __half22float2(hb[i]);
-      s = fmaf(u.x, xl[2 * i], s);
-      s = fmaf(u.y, xl[2 * i + 1], s);
-      s = fmaf(v.x, xl[8 + 2 * i], s);
-      s = fmaf(v.y, xl[8 + 2 * i + 1], s);
-    }
-  } else if (F.dtype == G_F32) {
-    const uint4* g = reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(F.G) +
-                                                    ((size_t)w * F.k + r) * kWinCols + 16 * lane);
+  for (int q = 0; q < 4; ++q) x[q] = *reinterpret_cast<const float4*>(xw + 4 * lane + 128 * q);
+  if (F.dtype == G_F16) {
+    const unsigned hw[8] = {R.g[0].x, R.g[0].y, R.g[0].z, R.g[0].w, R.g[1].x, R.g[1].y, R.g[1].z, R.g[1].w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const uint4 a = ld_nc16(g + q);
-      s = fmaf(__uint_as_float(a.x), xl[4 * q], s);
-      s = fmaf(__uint_as_float(a.y), xl[4 * q + 1], s);
-      s = fmaf(__uint_as_float(a.z), xl[4 * q + 2], s);
-      s = fmaf(__uint_as_float(a.w), xl[4 * q + 3], s);
+      const float2 u = __half22float2(*reinterpret_cast<const __half2*>(&hw[2 * q]));
+      const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&hw[2 * q + 1]));
+      s = fmaf(u.x, x[q].x, s);
+      s = fmaf(u.y, x[q].y, s);
+      s = fmaf(v.x, x[q].z, s);
+      s = fmaf(v.y, x[q].w, s);
+    }
+  } else if (F.dtype == G_F32) {
+    const float* g = reinterpret_cast<const float*>(F.G) + ((size_t)w * F.k + r) * kWinCols + 4 * lane;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 a = ld_nc16(g + 128 * q);
+      s = fmaf(__uint_as_float(a.x), x[q].x, s);
+      s = fmaf(__uint_as_float(a.y), x[q].y, s);
+      s = fmaf(__uint_as_float(a.z), x[q].z, s);
+      s = fmaf(__uint_as_float(a.w), x[q].w, s);
     }
   } else {
     const unsigned wd[4] = {R.g[0].x, R.g[0].y, R.g[0].z, R.g[0].w};
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 4; ++q) {
+      const float xv[4] = {x[q].x, x[q].y, x[q].z, x[q].w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         __nv_fp8_e4m3 e;
         e.__x = (unsigned char)(wd[q] >> (8 * j));
-        s = fmaf((float)e, xl[4 * q + j], s);
+        s = fmaf((float)e, xv[j], s);
       }
+    }
     s *= R.scale;
   }
   return wsum((double)s);
@@ -713,10 +738,14 @@ __device__ __forceinline__ void feed_finish(const Prog& P, const ECtl& C, const 
     // sum x, sum x^2 of the window: op statistics + the feeds' sum x^2 words
     double s = 0.0, q = 0.0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const double v = (double)xw[16 * lane + i];
-      s += v;
-      q += v * v;
+    for (int i = 0; i < 4; ++i) {          // columns 4 lane + 128 i .. + 3 (conflict-free LDS.128)
+      const float4 v4 = *reinterpret_cast<const float4*>(xw + 4 * lane + 128 * i);
+      const double vv[4] = {(double)v4.x, (double)v4.y, (double)v4.z, (double)v4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        s += vv[j];
+        q += vv[j] * vv[j];
+      }
     }
     s = wsum(s);
     q = wsum(q);
@@ -1724,7 +1753,10 @@ __device__ __noinline__ void out_stage(const Prog& P, const ECtl& C, Smem& sm, i
 // The kernel: n_steps decode steps (greedy token feedback on the device when
 // n_steps > 1; the host writes the token / mode of a single step).
 // ---------------------------------------------------------------------------
-extern "C" __global__ void __maxnreg__(168) engine_kernel(const Prog Pk, int n_steps) {
+#ifndef DPQ_MAXNREG
+#define DPQ_MAXNREG 168
+#endif
+extern "C" __global__ void __maxnreg__(DPQ_MAXNREG) engine_kernel(const Prog Pk, int n_steps) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int cta = blockIdx.x, G = gridDim.x, tid = threadIdx.x, warp = tid >> 5;
