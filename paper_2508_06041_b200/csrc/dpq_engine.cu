@@ -41,6 +41,9 @@
 #include "dpq_common.cuh"
 
 // Consumer-only CTA barrier (the producer and reducer warps never join).
+#ifndef DPQ_ATTN_WARPS
+#define DPQ_ATTN_WARPS 8           // warps per attention unit (kAttnChunk / this = positions per warp)
+#endif
 #ifndef DPQ_RING_SLOTS
 #define DPQ_RING_SLOTS 64          // ring slots (2 KB): bytes in flight per SM = the queueing depth
 #endif
@@ -416,7 +419,7 @@ struct Smem {
   int head_i[NW];
   double red[32];
   alignas(16) float attn_q[128];     // RoPE'd q of the current attention unit
-  alignas(16) float attn_m[4][132];  // per-warp (o[hd], m, l) of the unit
+  alignas(16) float attn_m[DPQ_ATTN_WARPS][132];  // per-warp (o[hd], m, l) of the unit
   alignas(16) float xw[kWinCols];    // the op's input window
   signed char gemv_bits[4];          // single-op programs: the forced bit (ECtl.forced_bits -> here)
   uint2 ctask[2][kMaxTasks];         // consumer task lists (by op parity)
@@ -840,7 +843,9 @@ __device__ __forceinline__ float dot4(float4 a, float4 b) { return a.x * b.x + a
 //    and published unnormalised as tagged words (epoch e). o's input load
 //    merges the chunks of a head (attn_merge).
 constexpr int kAttnChunk = 64;
-constexpr int kAttnWarps = 4;
+constexpr int kAttnWarps = DPQ_ATTN_WARPS;           // warps per attention unit
+constexpr int kRowsPerWarp = kAttnChunk / kAttnWarps;   // chunk rows (positions) per warp
+constexpr int kLanesPerRow = 32 / kRowsPerWarp;         // lanes sharing a row's score
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
@@ -937,38 +942,47 @@ __device__ __forceinline__ void attn_unit(const Prog& P, const ECtl& C, const Op
   asm volatile("cp.async.wait_all;" ::: "memory");
   asm volatile("bar.sync 2, %0;" :: "n"(32 * kAttnWarps) : "memory");
   if (stamp) { dbg[10] = gclock(); dbg[14] = clock64() - ck0; }
-  // scores: row r of the chunk, half hf of the dims
+  // scores: row r of the chunk, slice part of its dims (kLanesPerRow lanes per
+  // row); float4 chunks rotated by lane so a quarter warp hits 8 bank groups
   const float scale = 1.0f / sqrtf((float)hd);
-  const int r = 16 * kw + (lane >> 1), hf = lane & 1;
+  const int r = kRowsPerWarp * kw + lane / kLanesPerRow, part = lane % kLanesPerRow;
   const bool valid = s0 + r < s1;
   float a0 = 0.f, a1 = 0.f;
   {
-    const float* kr = Ks + r * hd + hf * half;
-    const float* qr = sm.attn_q + hf * half;
-    const int rot = 4 * ((lane >> 1) & 7);
-    for (int j = 0; j < half; j += 8) {
-      const int c0 = (j + rot) & (half - 1), c1 = (j + 4 + rot) & (half - 1);
-      a0 += dot4(*reinterpret_cast<const float4*>(qr + c0), *reinterpret_cast<const float4*>(kr + c0));
-      if (half >= 8) a1 += dot4(*reinterpret_cast<const float4*>(qr + c1), *reinterpret_cast<const float4*>(kr + c1));
+    const int dpl = hd / kLanesPerRow;          // dims per lane (>= 4)
+    const int nch = dpl / 4;                    // float4 chunks per lane
+    const float* kr = Ks + r * hd + part * dpl;
+    const float* qr = sm.attn_q + part * dpl;
+    if (nch == 0) {                             // head_dim < 4 kLanesPerRow: scalar dims
+      for (int i = 0; i < dpl; ++i) a0 += qr[i] * kr[i];
+    } else {
+      const int rot = lane % nch;
+      for (int c = 0; c < nch; c += 2) {
+        const int c0 = (c + rot) % nch, c1 = (c + 1 + rot) % nch;
+        a0 += dot4(*reinterpret_cast<const float4*>(qr + 4 * c0), *reinterpret_cast<const float4*>(kr + 4 * c0));
+        if (c + 1 < nch)
+          a1 += dot4(*reinterpret_cast<const float4*>(qr + 4 * c1), *reinterpret_cast<const float4*>(kr + 4 * c1));
+      }
     }
   }
   float a = a0 + a1;
-  a += __shfl_xor_sync(0xffffffffu, a, 1);
+#pragma unroll
+  for (int off = 1; off < kLanesPerRow; off <<= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
   const float sc = valid ? a * scale : -CUDART_INF_F;
   float m = sc;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
   const float p = valid ? expf(sc - m) : 0.f;                            // runtime.py:359-361
-  const float l = wsum(hf == 0 ? p : 0.f);
+  const float l = wsum(part == 0 ? p : 0.f);
   if (stamp) dbg[15] = clock64() - ck0;
   float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-  const int n = max(0, min(16, s1 - s0 - 16 * kw));
+  const int n = max(0, min(kRowsPerWarp, s1 - s0 - kRowsPerWarp * kw));
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
+  for (int j = 0; j < kRowsPerWarp; ++j) {
     if (j < n) {
-      const float pj = __shfl_sync(0xffffffffu, p, 2 * j);
+      const float pj = __shfl_sync(0xffffffffu, p, kLanesPerRow * j);
       if (act) {
-        const float4 vv = *reinterpret_cast<const float4*>(Vs + (16 * kw + j) * hd + i0);
+        const float4 vv = *reinterpret_cast<const float4*>(Vs + (kRowsPerWarp * kw + j) * hd + i0);
         o.x += pj * vv.x; o.y += pj * vv.y; o.z += pj * vv.z; o.w += pj * vv.w;
       }
     }
@@ -1612,13 +1626,40 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
 __device__ __noinline__ void head_stage(const Prog& P, const ECtl& C, Smem& sm, float* xs, int cta, int G,
                                         unsigned e_final) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // the final residual (tagged) -> shared memory, sum of squares in fixed order
+  // the final residual (tagged) -> shared memory (every pair of words of a
+  // thread polled in one round trip), then the sum of squares in fixed order
+  {
+    const int npair = P.d / 2;
+    for (int p0 = tid; p0 < npair; p0 += NT * 8) {
+      uint4 v[8];
+      bool ok;
+      SPIN_UNTIL((ok = true, [&]() {
+                    for (int k = 0; k < 8; ++k) {
+                      const int p = p0 + k * NT;
+                      if (p < npair) {
+                        v[k] = ld_tag2(P.xfinal + 2 * p);
+                        ok &= v[k].y == e_final && v[k].w == e_final;
+                      }
+                    }
+                  }(), ok), "final x", p0, e_final);
+      for (int k = 0; k < 8; ++k) {
+        const int p = p0 + k * NT;
+        if (p < npair) {
+          xs[2 * p] = __uint_as_float(v[k].x);
+          xs[2 * p + 1] = __uint_as_float(v[k].z);
+        }
+      }
+    }
+    if ((P.d & 1) && tid == 0) {
+      u64 x;
+      SPIN_UNTIL((x = ld_relaxed64(P.xfinal + P.d - 1), (unsigned)(x >> 32) == e_final), "final x", P.d - 1, e_final);
+      xs[P.d - 1] = __uint_as_float((unsigned)x);
+    }
+  }
+  CSYNC();
   double q = 0.0;
   for (int i = tid; i < P.d; i += NT) {
-    u64 x;
-    SPIN_UNTIL((x = ld_relaxed64(P.xfinal + i), (unsigned)(x >> 32) == e_final), "final x", i, e_final);
-    const float v = __uint_as_float((unsigned)x);
-    xs[i] = v;
+    const float v = xs[i];
     q += (double)v * v;
   }
   q = wsum(q);
