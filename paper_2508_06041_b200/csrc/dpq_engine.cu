@@ -94,6 +94,9 @@ struct Layer {
   int rows, n_tiles, tile_off, out_off;
   int l, h, prefill_bit;
   int sentinel;            // 0 estimate, 1 low (T = +inf), 2 high (T = -inf)
+  int xread;               // dual: all h planes streamed in dynamic steps (exact estimator / track_exact):
+                           // y_l and y_h from the shared planes, ||y_h - y_l|| into exact set xset
+  int xset, xcnt;          // exact set index; CTAs contributing to it (units of this layer)
   int est;                 // EST_NONE / EST_LINEAR / EST_PROJECTION
   int src;                 // SRC_*
   int k;                   // projection rank (0: linear)
@@ -218,6 +221,10 @@ struct Prog {
   unsigned* err;           // sticky error flags (ERR_RANGE: fixed-point range exceeded)
   signed char* tr_bits;
   float* tr_est;
+  float* tr_exact;         // [max_steps][n_trace] exact errors (dual layers)
+  u64* xerr;               // [kCurSlots][n_xsets][2] packed (hi, lo) sums of (y_h - y_l)^2
+  const int2* xsets;       // [n_xsets] (trace column, contributing CTAs)
+  int n_xsets;
   int n_trace, max_steps;
   int* tok_log;
   ECtl* ctl;
@@ -411,6 +418,7 @@ struct Smem {
   volatile int dec_op;               // decisions of ops < dec_op are published
   int dec_fin[kDecRing][kMaxOpLayers];
   float dec_est[kDecRing];           // first layer's estimate of the op (single-op programs)
+  float4 xraw[8][32];                // dual ops: per unit and lane (S_base, S_extra) of up to two tiles
   volatile int cons_ops;             // ops finished by the consumers
   volatile unsigned cons_gs;         // consumer stages finished (global stage number + 1)
   volatile int step_ready;           // steps whose control block is in ctl[]
@@ -448,6 +456,7 @@ struct I3 {
 // Base planes per layer for the step mode (known before the decision).
 __device__ __forceinline__ int base_bit(const Layer& L, const ECtl& C) {
   if (C.mode == MODE_PREFILL) return L.prefill_bit;
+  if (L.xread) return L.l;              // dual: base l planes, then the h - l extras regardless of the decision
   if (C.force && L.trace >= 0) return C.forced_bits[L.trace];
   if (L.sentinel == 2) return L.h;
   return L.l;
@@ -1111,7 +1120,7 @@ __device__ __forceinline__ double partial_total(uint4 q) {
 // read (this warp is their only reader; the stage parity reuses them two
 // stages later).
 __device__ __forceinline__ float2 tiles_S(const Prog& P, const Op& O, int t0, int ex0, int t1, int ex1,
-                                         unsigned epoch) {
+                                         unsigned epoch, double* raw = nullptr) {
   const int lane = threadIdx.x & 31;
   const size_t par = (size_t)((epoch - 1u) & 1u) * P.slot_half;   // parity of the stage (epoch = gs + 1)
   u64* b0 = P.slot + par + ((size_t)t0 * 32 + lane) * 2;
@@ -1143,6 +1152,12 @@ __device__ __forceinline__ float2 tiles_S(const Prog& P, const Op& O, int t0, in
   if (e0) *reinterpret_cast<uint4*>(x0) = z;
   if (two) *reinterpret_cast<uint4*>(b1) = z;
   if (e1) *reinterpret_cast<uint4*>(x1) = z;
+  if (raw) {       // (S_base, S_extra) of both tiles, uncombined (dual layers)
+    raw[0] = partial_total(q0);
+    raw[1] = e0 ? partial_total(q1) : 0.0;
+    raw[2] = two ? partial_total(q2) : 0.0;
+    raw[3] = e1 ? partial_total(q3) : 0.0;
+  }
   const double s0 = e0 ? ldexp(partial_total(q0), ex0) + partial_total(q1) : partial_total(q0);
   const double s1 = e1 ? ldexp(partial_total(q2), ex1) + partial_total(q3) : partial_total(q2);
   return make_float2((float)s0, (float)s1);
@@ -1178,7 +1193,7 @@ __device__ __forceinline__ Epi op_epi(const Prog& P, const Op& O, unsigned epoch
 // the same decisions without another exchange).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op& O, const I3& nb, I3& fin,
-                                          int cta, unsigned step_base, u64* rdbg, float* est0) {
+                                          int cta, unsigned step_base, u64* rdbg, float* est0, I3& real) {
   const int lane = threadIdx.x & 31;
   const bool dyn = C.mode == MODE_DYNAMIC;
   // every estimating layer's words in one poll: lane holds packed G.x words
@@ -1191,7 +1206,7 @@ __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op
   for (int li = 0; li < kMaxOpLayers; ++li) {
     if (li >= O.n_layers) break;
     const Layer& L = O.L[li];
-    if (!(dyn && L.sentinel == 0 && L.est != EST_NONE)) continue;
+    if (!(dyn && L.sentinel == 0 && L.est != EST_NONE && L.est != EST_EXACT)) continue;
     const bool prev = L.src == SRC_PREV_STEP && C.has_prev;
     const int slot = prev ? kCurSlots + ((C.rot - 1) & (kPrevSlots - 1)) : (C.n_steps_done & (kCurSlots - 1));
     base[li] = P.fpart + (size_t)slot * P.set_stride + L.set;
@@ -1241,6 +1256,12 @@ __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op
     int bit = nb[li];
     double est = CUDART_NAN;
     const bool has = base[li] != nullptr;
+    if (L.xread && dyn) {      // dual: the real bit (the stream always reads h planes)
+      if (C.force && L.trace >= 0) bit = C.forced_bits[L.trace];
+      else if (L.sentinel == 1) bit = L.l;
+      else if (L.sentinel == 2) bit = L.h;
+      else if (L.est == EST_EXACT) bit = -1;                 // decided from ||y_h - y_l|| after the reduction
+    }
     if (has) {
       double q = 0.0, sq = 0.0;
 #pragma unroll
@@ -1263,9 +1284,10 @@ __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op
       else est = L.slope * (sq > 0.0 ? sc * sq * rsqrt_d(sq) : 0.0) + L.intercept;           // estimator.py:41-42
       if (!C.force) bit = est > L.T ? L.h : L.l;                                              // strict > (runtime.py:192)
     }
-    fin.set(li, bit);
+    real.set(li, bit);
+    fin.set(li, L.xread && dyn ? L.h : bit);                // the streaming bits (producer / consumers)
     if (li == 0) *est0 = has ? (float)est : CUDART_NAN_F;
-    if (lane == 0 && dyn && cta == 0 && L.trace >= 0 && P.n_trace > 0 && C.trace_step < P.max_steps) {
+    if (bit >= 0 && lane == 0 && dyn && cta == 0 && L.trace >= 0 && P.n_trace > 0 && C.trace_step < P.max_steps) {
       const size_t o = (size_t)C.trace_step * P.n_trace + L.trace;
       P.tr_bits[o] = (signed char)bit;
       P.tr_est[o] = has ? (float)est : CUDART_NAN_F;
@@ -1506,6 +1528,132 @@ __device__ __forceinline__ void cons_op(const Prog& P, Smem& sm, int oi, int op_
 }
 
 // ---------------------------------------------------------------------------
+// Dual ops (exact estimators, track_exact; estimator.py:30-32, 63-73,
+// runtime.py:322-324): every h plane is streamed, so each row has S_l (the l
+// base planes) and S_x (the h - l extras) with S_h = 2^(h-l) S_l + S_x, and
+// y_h - y_l = s_in span (2^-h S_x + sum x / 2 (2^-h - 2^-l)) (lo cancels,
+// quant.py:74-78). Phase 1: every unit's raw sums -> shared memory and the
+// CTA's sum of (y_h - y_l)^2 per dual layer -> the layer's packed exact set;
+// exact estimators then wait for the full set and decide est > T with est =
+// ||y_h - y_l||; phase 2: the outputs with the real bits.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void add_packed_d(u64* w, double v, unsigned* err) {
+  long long x = 0;
+  if (fabs(v) < 8.0e9) x = llrint(v * kFxPart);
+  else atomicOr(err, (unsigned)ERR_RANGE);
+  const long long hi = x >> 24, lo = x & 0xffffff;
+  const u64 one = 1ull << kCntShift;
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(w), "l"(one + (u64)(hi + kFxBias)) : "memory");
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" :: "l"(w + 1), "l"(one + (u64)(lo + kFxBias)) : "memory");
+}
+
+__device__ __forceinline__ void dual_units(const Prog& P, const ECtl& C, const Op& O, Smem& sm, int cta, int G,
+                                           const I3& nb, const I3& fin, I3 real, const Epi& E, unsigned epoch,
+                                           unsigned e_res) {
+  const int lane = threadIdx.x & 31;
+  const int half = O.L[0].n_tiles;
+  const int n_u = (O.n_units - cta + G - 1) / G;
+  double xs[kMaxOpLayers] = {0.0, 0.0, 0.0};
+  // phase 1
+  for (int i = 0; i < n_u; ++i) {
+    const int u = cta + i * G;
+    double raw[4];
+    if (O.pair) {
+      tiles_S(P, O, u, fin.v0 - nb.v0, u + half, fin.v1 - nb.v1, epoch, raw);
+    } else {
+      const int li = layer_of(O, u);
+      tiles_S(P, O, u, fin[li] - nb[li], -1, 0, epoch, raw);
+    }
+    sm.xraw[i][lane] = make_float4((float)raw[0], (float)raw[1], (float)raw[2], (float)raw[3]);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (t == 1 && !O.pair) break;
+      const int li = O.pair ? t : layer_of(O, u);
+      const Layer& L = O.L[li];
+      if (!L.xread) continue;
+      const int r = (O.pair ? u : u - L.tile_off) * 32 + lane;
+      if (r >= L.rows) continue;
+      const double sp = (double)__ldg(L.span + r);
+      const double dy = (double)E.scale * sp *
+                        (ldexp(raw[2 * t + 1], -L.h) + 0.5 * (double)E.sx * (ldexp(1.0, -L.h) - ldexp(1.0, -L.l)));
+      const double d2 = dy * dy;
+      if (li == 0) xs[0] += d2; else if (li == 1) xs[1] += d2; else xs[2] += d2;
+    }
+  }
+  u64* xw = P.xerr + (size_t)(C.n_steps_done & (kCurSlots - 1)) * P.n_xsets * 2;
+#pragma unroll
+  for (int li = 0; li < kMaxOpLayers; ++li) {
+    if (li >= O.n_layers || !O.L[li].xread) continue;
+    // this CTA's units of the layer: contribute (possibly 0) iff it has any
+    bool mine = false;
+    for (int i = 0; i < n_u && !mine; ++i) {
+      const int u = cta + i * G;
+      mine = O.pair || (u >= O.L[li].tile_off && u < O.L[li].tile_off + O.L[li].n_tiles);
+    }
+    const double t = wsum(xs[li]);
+    if (mine && lane == 0) add_packed_d(xw + 2 * O.L[li].xset, t, P.err);
+  }
+  // exact estimators: the full set, then est > T (estimator.py:63-73, runtime.py:192)
+#pragma unroll
+  for (int li = 0; li < kMaxOpLayers; ++li) {
+    if (li >= O.n_layers || real[li] >= 0) continue;
+    const Layer& L = O.L[li];
+    const u64* w = xw + 2 * L.xset;
+    uint4 q;
+    SPIN_UNTIL((q = ld_tag2(w), (int)(q.y >> 24) == L.xcnt && (int)(q.w >> 24) == L.xcnt), "exact set", L.trace, L.xcnt);
+    const double est = sqrt(fmax(partial_total(q), 0.0));
+    const int bit = est > L.T ? L.h : L.l;
+    real.set(li, bit);
+    if (lane == 0 && cta == 0 && L.trace >= 0 && P.n_trace > 0 && C.trace_step < P.max_steps) {
+      const size_t o = (size_t)C.trace_step * P.n_trace + L.trace;
+      P.tr_bits[o] = (signed char)bit;
+      P.tr_est[o] = (float)est;
+    }
+  }
+  __syncwarp();
+  // phase 2: the outputs with the real bits
+  for (int i = 0; i < n_u; ++i) {
+    const int u = cta + i * G;
+    const float4 rw = sm.xraw[i][lane];
+    auto S_of = [&](int li, float sb, float sx) -> float {
+      const Layer& L = O.L[li];
+      if (L.xread) return real[li] == L.h ? (float)(ldexp((double)sb, L.h - L.l) + (double)sx) : sb;
+      const int ex = fin[li] - nb[li];
+      return ex > 0 ? (float)(ldexp((double)sb, ex) + (double)sx) : sb;
+    };
+    auto bit_of = [&](int li) { const Layer& L = O.L[li]; return L.xread ? (real[li] == L.h ? L.h : L.l) : fin[li]; };
+    if (O.pair) {
+      const int r = u * 32 + lane;
+      if (r < O.L[0].rows) {
+        const float S0 = S_of(0, rw.x, rw.y), S1 = S_of(1, rw.z, rw.w);
+        const int b0 = bit_of(0), b1 = bit_of(1);
+        const float up = E.scale * (__ldg(O.L[0].lo + r) * E.sx + ldexpf(__ldg(O.L[0].span + r), -b0) * (S0 + 0.5f * E.sx));
+        const float gt = E.scale * (__ldg(O.L[1].lo + r) * E.sx + ldexpf(__ldg(O.L[1].span + r), -b1) * (S1 + 0.5f * E.sx));
+        const float hv = up * (gt / (1.0f + expf(-gt)));                 // runtime.py:368
+        if (O.push) st_tag_all(P, O.out + O.L[0].out_off + r, hv, epoch);
+        else st_tag(O.out + O.L[0].out_off + r, hv, epoch);
+      }
+    } else {
+      const int li = layer_of(O, u);
+      const Layer& L = O.L[li];
+      const int r = (u - L.tile_off) * 32 + lane;
+      if (r < L.rows) {
+        const int o = L.out_off + r;
+        const float S = S_of(li, rw.x, rw.y);
+        float v = E.scale * (__ldg(L.lo + r) * E.sx + ldexpf(__ldg(L.span + r), -bit_of(li)) * (S + 0.5f * E.sx));
+        if (O.add) {                                                            // runtime.py:364, 370
+          u64 xr;
+          SPIN_UNTIL((xr = ld_relaxed64(O.res_in + o), (unsigned)(xr >> 32) == e_res), "residual", o, e_res);
+          v = __uint_as_float((unsigned)xr) + v;
+        }
+        if (O.push) st_tag_all(P, O.out + o, v, epoch);
+        else st_tag(O.out + o, v, epoch);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // The reducer warp: every stage in order; the units of op stages as their
 // partials arrive, then one arrival on the stage counter once the consumers
 // are done with the stage too.
@@ -1536,7 +1684,8 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
         u64* rdbg = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr;
         if (rdbg && lane == 0) rdbg[16] = gclock();
         float est0 = CUDART_NAN_F;
-        decide_op(P, C, O, nb, fin, cta, step_base, rdbg, &est0);
+        I3 real = nb;
+        decide_op(P, C, O, nb, fin, cta, step_base, rdbg, &est0, real);
         if (rdbg && lane == 0) rdbg[17] = gclock();
         if (lane == 0) {
           sm.dec_fin[oi % kDecRing][0] = fin.v0;
@@ -1554,8 +1703,11 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
           __syncwarp();
           const unsigned epoch = gs + 1u;
           const unsigned e_res = O.add ? step_base + (unsigned)O.res_stage + 1u : 0u;
+          const bool dual = C.mode == MODE_DYNAMIC && (O.L[0].xread || (O.n_layers > 1 && O.L[1].xread) ||
+                                                       (O.n_layers > 2 && O.L[2].xread));
+          if (dual) dual_units(P, C, O, sm, cta, G, nb, fin, real, E, epoch, e_res);
           // the affine epilogue (quant.py:74-78): y = s_in (lo sum x + span 2^-b (S + sum x / 2))
-          for (int u = cta; u < O.n_units; u += G) {
+          for (int u = cta; !dual && u < O.n_units; u += G) {
             if (O.pair) {
               // unit u: up tile u and gate tile u (runtime.py:366-368)
               const int half = O.L[0].n_tiles;
@@ -1683,6 +1835,19 @@ __device__ __noinline__ void head_stage(const Prog& P, const ECtl& C, Smem& sm, 
     a = wsum(a);
     if (lane == 0) P.logits[v] = a * inv;
   }
+  // exact errors of the step's dual layers (track_exact / exact estimators) -> trace
+  if (cta == 0 && C.mode == MODE_DYNAMIC && P.n_trace > 0 && C.trace_step < P.max_steps) {
+    const u64* xw = P.xerr + (size_t)(C.n_steps_done & (kCurSlots - 1)) * P.n_xsets * 2;
+    for (int j = tid; j < P.n_xsets; j += NT) {
+      const int2 xs = P.xsets[j];
+      uint4 q;
+      SPIN_UNTIL((q = ld_tag2(xw + 2 * j), (int)(q.y >> 24) == xs.y && (int)(q.w >> 24) == xs.y), "exact set (head)", j, xs.y);
+      const float xe = (float)sqrt(fmax(partial_total(q), 0.0));
+      const size_t o = (size_t)C.trace_step * P.n_trace + (xs.x & 0xffff);
+      P.tr_exact[o] = xe;
+      if (xs.x >> 16) P.tr_est[o] = xe;         // exact estimators: the estimate is the exact error
+    }
+  }
   __threadfence();
   CSYNC();
   if (tid == 0) sm.head_last = atomicAdd(P.head_cnt, 1u) == (unsigned)G - 1;
@@ -1759,6 +1924,8 @@ __device__ __forceinline__ void begin_stage(const Prog& P, Smem& sm, int cta, in
     u64* a = P.fpart + (size_t)((C.n_steps_done + 2) & (kCurSlots - 1)) * P.set_stride;
     u64* z = P.fpart + (size_t)(kCurSlots + ((C.rot + 1) & (kPrevSlots - 1))) * P.set_stride;
     for (long long i = cta * NT + tid; i < P.set_stride; i += G * NT) { a[i] = 0; z[i] = 0; }
+    u64* xz = P.xerr + (size_t)((C.n_steps_done + 2) & (kCurSlots - 1)) * P.n_xsets * 2;
+    for (int i = cta * NT + tid; i < 2 * P.n_xsets; i += G * NT) xz[i] = 0;
   }
   for (int i = cta * NT + tid; i < P.d; i += G * NT) st_tag(P.xe + i, __ldg(P.embed + (size_t)C.token * P.d + i), gs + 1u);
 }

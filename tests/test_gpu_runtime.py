@@ -526,3 +526,59 @@ def test_engine_e4m3_projection():
     _, est_o = trace_arrays(eo.records, ids)
     np.testing.assert_allclose(est_d, est_o, rtol=3e-2)
     eng.close()
+
+
+def _dual_setup(kind):
+    cfg = M.ModelConfig(n_blocks=2, d_model=256, n_heads=4, d_ff=512, vocab=256, seq_cap=64, n_kv_heads=2)
+    w = M.init_model(9, cfg)
+    store = Q.quantize_model(w, 5, 3)
+    pairs = {l: (3, 4) for l in store.layers}
+    if kind == "projection":
+        plan = synthetic_projection_plan(store, pairs, k=32, seed=3)
+    else:
+        layers = {}
+        for lid in store.layers:
+            est = R.E.ErrorEstimator(R.E.ExactEstimator(store.layers[lid], 3, 4), R.E.IMMEDIATE, (3, 4))
+            layers[lid] = R.PlanLayer(lid, 4, 3.5, (3, 4), 1.0, 0.5, est)
+        plan = R.PrecisionPlan("dp", 3.5, 4.0, layers, store.param_counts())
+    toks = np.random.default_rng(21).integers(0, 256, 16)
+    calibrate_T(w, store, plan, toks[:8])
+    return w, store, plan, toks
+
+
+@pytest.mark.parametrize("kind", ["projection", "exact"])
+def test_engine_dual_layers_match_oracle(kind):
+    """Exact estimators (estimator.py:63-73, decision from ||(W_h - W_l) x||)
+    and track_exact (runtime.py:322-324) on the TMA engine (dual units: all h
+    planes, y_l and y_h from the shared planes): forced replay of the
+    oracle's decisions gives its logits, estimates and exact errors; the free
+    run's decisions follow the oracle under the eps rule."""
+    from paper_2508_06041_b200 import _lib
+    w, store, plan, toks = _dual_setup(kind)
+    ids = canon(store.layers)
+    eo = oracle_engine(w, store, plan, track_exact=True)
+    ref = [eo.step(int(toks[0]), dynamic=False)] + [eo.step(int(t)) for t in toks[1:]]
+    bits_o, est_o = trace_arrays(eo.records, ids)
+    xerr_o = np.array([[r.exact_errors[O.key(l)] for l in ids] for r in eo.records])
+    eng = R.DecodeEngine(w, store, plan, g_dtype="f32", track_exact=True)
+    assert _lib.load().dpq_session_is_persistent(eng._h) == 2, "not on the TMA engine"
+    lg = [eng.step(int(toks[0]), dynamic=False)]
+    for i, t in enumerate(toks[1:]):
+        lg.append(eng.step(int(t), forced_bits=bits_o[i].astype(np.int8)))
+    lg = np.array(lg)
+    assert np.max(np.abs(lg - np.array(ref))) <= LOGIT_TOL * np.max(np.abs(ref))
+    bits_d, est_d = trace_arrays(eng.trace.steps, ids)
+    np.testing.assert_array_equal(bits_d, bits_o)
+    np.testing.assert_allclose(est_d, est_o, rtol=1e-4, atol=1e-9)
+    xerr_d = np.array([[s.exact_errors[l] for l in ids] for s in eng.trace.steps])
+    np.testing.assert_allclose(xerr_d, xerr_o, rtol=1e-4, atol=1e-9)
+    eng.close()
+    # free run: the device's own decisions
+    eng = R.DecodeEngine(w, store, plan, g_dtype="f32", track_exact=True)
+    eng.step(int(toks[0]), dynamic=False)
+    for t in toks[1:]:
+        eng.step(int(t))
+    bits_f, _ = trace_arrays(eng.trace.steps, ids)
+    assert not decision_mismatches(bits_f, bits_o, est_o, Ts(plan, ids), EPS_DECISION["f32"])
+    assert 0.1 < np.mean(bits_f == 4) < 0.9
+    eng.close()
