@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libdpq_b200.so")
-SOURCES = ["dpq_capi.cu", "dpq_kernels.cu", "dpq_engine.cu", "dpq_common.cuh", "dpq_session.inc"]
+SOURCES = ["dpq_capi.cu", "dpq_kernels.cu", "dpq_engine.cu", "dpq_gemv.cu", "dpq_common.cuh", "dpq_session.inc"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

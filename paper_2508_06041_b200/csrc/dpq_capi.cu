@@ -2,6 +2,7 @@
 // per-step kernel schedule and its CUDA graph. C-ABI in include/dpq_b200.h.
 #include "dpq_kernels.cu"
 #include "dpq_engine.cu"
+#include "dpq_gemv.cu"
 
 #include <cmath>
 #include <cstdarg>
@@ -180,6 +181,11 @@ struct dpq_store {
   float* est_buf = nullptr;          // exact-estimator input copy
   int max_rows_pad = 0, max_win = 0, max_tiles = 0, max_cols = 0;
   std::vector<void*> gemv_progs;     // single-op engine programs per layer (dpq_gemv)
+  // bitplane_gemv_kernel scratch (dpq_gemv.cu; self-resetting, sized for the largest layer seen)
+  Arena gv_arena;
+  gv::Args gv{};
+  size_t gv_part = 0, gv_tiles = 0, gv_win = 0;
+  int gv_smem = 0;
 };
 
 struct dpq_plan {
@@ -194,6 +200,93 @@ struct dpq_plan {
 
 int gemv_engine_run(dpq_store* s, dpq_plan* p, int li, int b, const float* x, float* y, int32_t* bit_out,
                     float* est_out, cudaStream_t st, bool* used);
+
+// One layer through bitplane_gemv_kernel (dpq_gemv.cu): static b (p == nullptr)
+// or the plan's selector. *used = false when the layer does not fit it (a CTA
+// range over > 2 windows, an exact estimator): the caller falls back.
+int gv_run(dpq_store* s, const dpq_plan* p, int li, int b, const float* x, float* y, int32_t* bit_out,
+           float* est_out, cudaStream_t st, bool* used) {
+  *used = false;
+  const char* env = getenv("DPQ_GEMV_KERNEL");
+  if (env && env[0] == '0') return DPQ_OK;
+  const DevLayer& L = s->layers[li];
+  const long long T = (long long)L.n_win * L.n_tiles;
+  const int G = (int)std::min<long long>(s->n_sm, T);
+  if (G <= 0 || (T + G - 1) / G > L.n_tiles + 1) return DPQ_OK;      // <= 2 windows per CTA
+  gv::Args A{};
+  A.l = A.h = b;
+  A.sentinel = 1;
+  if (p) {
+    const DevSel& S = p->sel[li];
+    if (S.sentinel == 0 && S.est_kind != EST_LINEAR && !(S.est_kind == EST_PROJECTION && S.G && S.k <= kMaxK))
+      return DPQ_OK;
+    // the selector here decides after the base planes are issued and streams the
+    // extra planes at the end (their latency is exposed); the single-op engine
+    // program overlaps them, which wins once the base stream is long
+    // (tools/gemv_sweep.py: 4096x4096 13.7 vs 16.6 us, 14336x4096 21.6 vs 20.6)
+    const char* dyn_env = getenv("DPQ_GEMV_KERNEL_DYNAMIC");
+    const long long max_dyn = dyn_env ? atoll(dyn_env) : (8ll << 20);
+    if (S.l != S.h && (long long)L.rows * L.cols * S.l / 8 > max_dyn) return DPQ_OK;
+    A.l = S.l;
+    A.h = S.h;
+    A.sentinel = S.sentinel;
+    A.est_kind = S.est_kind;
+    A.k = S.est_kind == EST_PROJECTION ? S.k : 0;
+    A.g_dtype = S.g_dtype;
+    A.G = S.G;
+    A.g_scale = S.g_scale;
+    A.T = S.T;
+    A.slope = S.slope;
+    A.intercept = S.intercept;
+    A.fbscale = std::ldexp(1.0, -p->gt_fb[li]);
+    A.fxscale = std::ldexp(1.0, p->gt_fb[li]);
+    if (A.l == A.h) A.sentinel = 1;
+  }
+  const size_t part = (size_t)L.n_win * L.n_tiles * 32;
+  if (part > s->gv_part || (size_t)L.n_tiles > s->gv_tiles || (size_t)L.n_win > s->gv_win || !s->gv.sync) {
+    CK(cudaStreamSynchronize(st));
+    s->gv_arena.release();
+    s->gv_part = std::max(part, s->gv_part);
+    s->gv_tiles = std::max((size_t)L.n_tiles, s->gv_tiles);
+    s->gv_win = std::max((size_t)L.n_win, s->gv_win);
+    gv::Args& S = s->gv;
+    TRY(s->gv_arena.alloc_t(&S.part, s->gv_part));
+    TRY(s->gv_arena.alloc_t(&S.cnt, s->gv_tiles));
+    TRY(s->gv_arena.alloc_t(&S.sx, s->gv_win));
+    TRY(s->gv_arena.alloc_t(&S.sq, s->gv_win));
+    TRY(s->gv_arena.alloc_t(&S.acc, (size_t)kMaxK));
+    TRY(s->gv_arena.alloc_t(&S.sync, 4));
+    TRY(s->gv_arena.alloc_t(&S.err, 1));
+  }
+  if (!s->gv_smem) {
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->device));
+    s->gv_smem = optin - 1024;
+    CK(cudaFuncSetAttribute(gv::bitplane_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, s->gv_smem));
+  }
+  A.part = s->gv.part;
+  A.cnt = s->gv.cnt;
+  A.sx = s->gv.sx;
+  A.sq = s->gv.sq;
+  A.acc = s->gv.acc;
+  A.sync = s->gv.sync;
+  A.err = s->gv.err;
+  A.planes = L.planes;
+  A.pstride16 = L.plane_stride16;
+  A.lo = L.lo;
+  A.span = L.span;
+  A.rows = L.rows;
+  A.cols = L.cols;
+  A.n_win = L.n_win;
+  A.n_tiles = L.n_tiles;
+  A.x = x;
+  A.y = y;
+  A.bit_out = bit_out;
+  A.est_out = est_out;
+  TRY(launch(gv::bitplane_gemv_kernel, dim3(G), dim3(gv::kNT), (size_t)s->gv_smem, st, false, A));
+  *used = true;
+  return DPQ_OK;
+}
 void gemv_progs_release(std::vector<void*>& cache);
 
 
@@ -484,6 +577,7 @@ extern "C" int dpq_store_destroy(dpq_store* s) {
   cudaSetDevice(s->device);
   cudaDeviceSynchronize();
   gemv_progs_release(s->gemv_progs);
+  s->gv_arena.release();
   s->arena.release();
   delete s;
   return DPQ_OK;
@@ -555,6 +649,13 @@ int run_op(const OpDesc& D, Control* ctl, int n_sm, cudaStream_t st, bool pdl) {
 
 }  // namespace
 
+// Diagnostics (not in the public header): per-CTA globaltimer stamps of
+// bitplane_gemv_kernel into dev_buf [grid][8] (nullptr: off). tools/gv_stamps.py.
+extern "C" int dpq_debug_gemv_stamps(unsigned long long* dev_buf) {
+  CK(cudaMemcpyToSymbol(gv::g_gv_dbg, &dev_buf, sizeof(dev_buf)));
+  return DPQ_OK;
+}
+
 extern "C" int dpq_gemv(dpq_store* s, int layer, int b, const float* x_dev, float* y_dev, void* stream) {
   if (!s || layer < 0 || layer >= (int)s->layers.size() || !x_dev || !y_dev)
     return set_err(DPQ_ERR_ARG, "dpq_gemv: bad arguments");
@@ -567,6 +668,8 @@ extern "C" int dpq_gemv(dpq_store* s, int layer, int b, const float* x_dev, floa
   S.sentinel = 1;
   S.T = INFINITY;
   bool used = false;
+  TRY(gv_run(s, nullptr, layer, b, x_dev, y_dev, nullptr, nullptr, (cudaStream_t)stream, &used));
+  if (used) return DPQ_OK;
   TRY(gemv_engine_run(s, nullptr, layer, b, x_dev, y_dev, nullptr, nullptr, (cudaStream_t)stream, &used));
   if (used) return DPQ_OK;
   OpDesc D = single_op(s, layer, S, x_dev, y_dev);
@@ -727,6 +830,8 @@ extern "C" int dpq_select_gemv(dpq_plan* p, int layer, const float* x_dev, const
   const bool want_exact = exact_out_dev != nullptr && S.l != S.h;
   if (!exact_est && !want_exact && (est_in_dev == nullptr || est_in_dev == x_dev)) {
     bool used = false;
+    TRY(gv_run(s, p, layer, 0, x_dev, y_dev, bit_out_dev, est_out_dev, st, &used));
+    if (used) return DPQ_OK;
     TRY(gemv_engine_run(s, p, layer, 0, x_dev, y_dev, bit_out_dev, est_out_dev, st, &used));
     if (used) return DPQ_OK;
   }

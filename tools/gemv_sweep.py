@@ -77,12 +77,18 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default="")
+    ap.add_argument("--quick", action="store_true", help="static 3 / 4 / 8 bits and dynamic (3, 4) only")
+    ap.add_argument("--shape", default="", help="ROWSxCOLS: this shape only")
+    ap.add_argument("--bits", default="", help="comma list of static bits (default 3..8)")
+    ap.add_argument("--no-dynamic", action="store_true")
+    ap.add_argument("--copies", type=int, default=0, help="layer copies (default: > 300 MB in total)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     dev = torch.device("cuda:0")
     out = []
-    for rows, cols in SHAPES:
-        n_copy = max(8, int(np.ceil(300e6 / (rows * cols * 3 / 8))))
+    shapes = [tuple(int(v) for v in args.shape.split("x"))] if args.shape else SHAPES
+    for rows, cols in shapes:
+        n_copy = args.copies or max(8, int(np.ceil(300e6 / (rows * cols * 3 / 8))))
         gen = torch.Generator(device=dev).manual_seed(rows + cols)
         specs = []
         rng = np.random.default_rng(0)
@@ -100,7 +106,8 @@ def main():
         base = rows * cols
         small = 8 * rows + 4 * cols + 4 * rows
         stat = {}
-        for b in range(3, 9):
+        sbits = [int(v) for v in args.bits.split(",")] if args.bits else ((3, 4, 8) if args.quick else range(3, 9))
+        for b in sbits:
             def launch(sp, i, warm, b=b):
                 _lib.call("dpq_gemv", ds.handle, i % n_copy, b, C.c_void_p(x.data_ptr()),
                           C.c_void_p(y.data_ptr()), sp)
@@ -112,7 +119,7 @@ def main():
             print(json.dumps(out[-1]), flush=True)
         # dynamic: projection selector, pair (b, b+1), half the copies high
         xs = x.double().cpu().numpy()
-        for b in range(3, 8):
+        for b in (() if args.no_dynamic else (3,) if args.quick else range(3, 8)):
             pls, n_high = [], 0
             for i in range(n_copy):
                 G = np.random.default_rng(100 + i).standard_normal((K, cols)) / np.sqrt(cols)
