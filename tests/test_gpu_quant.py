@@ -210,3 +210,56 @@ def test_build_projection_on_device_matches_oracle(shape, pair):
     G_ref = O.build_projection_G(O.as_layer(q), l, h, 64, 9)
     assert G.shape == (64, shape[1])
     np.testing.assert_allclose(G, G_ref, rtol=1e-10, atol=1e-12 * np.abs(G_ref).max())
+
+
+@pytest.mark.parametrize("shape", [(45, 700), (100, 512), (1000, 96), (4128, 1500), (96, 40 * 512 + 7),
+                                   (33, 9000)])
+def test_gemv_kernel_ragged_shapes(shape, monkeypatch):
+    """bitplane_gemv_kernel (csrc/dpq_gemv.cu) on ragged shapes: fewer tasks
+    than CTAs, rows not a multiple of 32, partial windows, CTA ranges over two
+    windows (few tiles per window): equal to the oracle at every b, and to the
+    single-op engine program (DPQ_GEMV_KERNEL=0); repeated calls (the
+    self-resetting tile counters) give identical results."""
+    rows, cols = shape
+    rng = np.random.default_rng(rows * 7 + cols)
+    W = rng.normal(0.0, 1.0 / np.sqrt(cols), shape)
+    q = Q.quantize_layer(W, 6, 3)
+    x = rng.normal(size=cols).astype(np.float32)
+    ol = O.as_layer(q)
+    xt = torch.as_tensor(x, device="cuda")
+    for b in range(3, 7):
+        y1 = Q.gemv(q, b, xt).double().cpu().numpy()
+        y2 = Q.gemv(q, b, xt).double().cpu().numpy()
+        assert np.array_equal(y1, y2)
+        close_y(y1, O.plane_sum_gemv(ol, b, x.astype(np.float64)))
+    monkeypatch.setenv("DPQ_GEMV_KERNEL", "0")
+    y3 = Q.gemv(q, 5, xt).double().cpu().numpy()
+    monkeypatch.delenv("DPQ_GEMV_KERNEL")
+    close_y(Q.gemv(q, 5, xt).double().cpu().numpy(), y3)
+
+
+@pytest.mark.parametrize("cols", [700, 4100])
+def test_gemv_kernel_selector_matches_engine_program(cols, monkeypatch):
+    """dpq_select_gemv through bitplane_gemv_kernel (projection selector, f32
+    G, pair (3, 5)) and through the single-op engine program: same bit, same
+    estimate (the same fixed-point G.x sums), outputs within the GEMV tolerance."""
+    rng = np.random.default_rng(cols)
+    rows = 300
+    W = rng.normal(0.0, 1.0 / np.sqrt(cols), (rows, cols))
+    q = Q.quantize_layer(W, 6, 3)
+    G = rng.normal(size=(64, cols)) / np.sqrt(cols)
+    x = rng.normal(size=cols)
+    ref_est = float(np.linalg.norm(G @ x.astype(np.float32).astype(np.float64)))
+    est_obj = E.ErrorEstimator(E.ProjectionEstimator(G, 64, 0), E.IMMEDIATE, (3, 5))
+    for T, want in ((ref_est * 0.99, 5), (ref_est * 1.01, 3)):
+        pl = R.PlanLayer(LayerId(0, "o"), 6, 4.0, (3, 5), T, 0.5, est_obj)
+        outs = []
+        for env in ("1", "0"):
+            monkeypatch.setenv("DPQ_GEMV_KERNEL", env)
+            outs.append(_select(q, pl, x, "f32"))
+        monkeypatch.delenv("DPQ_GEMV_KERNEL")
+        (y1, b1, e1, _), (y2, b2, e2, _) = outs
+        assert b1 == b2 == want
+        assert e1 == e2 and e1 == pytest.approx(ref_est, rel=1e-5)
+        close_y(y1, np.asarray(y2, dtype=np.float64))
+        close_y(y1, O.gemv(O.as_layer(q), want, x.astype(np.float32)))
