@@ -50,6 +50,9 @@
 #ifndef DPQ_PF_ITEMS
 #define DPQ_PF_ITEMS 0             // (measured slower at 64-256) next op's first base items prefetched into L2 per CTA
 #endif
+#ifndef DPQ_EXTRA_PREFETCH
+#define DPQ_EXTRA_PREFETCH 0       // extra planes of deciding layers prefetched into L2 while the decision is pending
+#endif
 #define CSYNC() asm volatile("bar.sync 1, %0;" :: "n"(dpq::eng::NT) : "memory")
 
 namespace dpq {
@@ -1364,6 +1367,22 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
       }
       const int n_base = W.cnt[0] * nb.v0 + W.cnt[1] * nb.v1 + W.cnt[2] * nb.v2;
       if (pdbg && lane == 0) pdbg[5] = gclock();
+#if DPQ_EXTRA_PREFETCH
+      // while the decision is pending (HBM is idle on the small ops), the
+      // extra planes of the op's deciding layers go to L2 speculatively: a
+      // high decision then streams them from L2
+      if (C.mode == MODE_DYNAMIC && !C.force)
+        for (int k = lane; k < W.n_tasks; k += 32) {
+          const uint2 tk = sm.ptask[k];
+          const int li = task_layer(tk);
+          const Layer& L = O.L[li];
+          if (L.sentinel != 0 || L.xread || nb[li] >= L.h) continue;
+          const long long ps = li == 0 ? ps0 : li == 1 ? ps1 : ps2;
+          const unsigned char* src = reinterpret_cast<const unsigned char*>(sm.psrc[k]) + (long long)nb[li] * ps;
+          for (int q = nb[li]; q < L.h; ++q, src += ps)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"((unsigned)kItemBytes) : "memory");
+        }
+#endif
       // the op's decisions (taken by the reducer warp)
       if (lane == 0) SPIN_UNTIL_NS(sm.dec_op >= oi + 1, "producer decision", oi, 0, 12000000000ull);
       __syncwarp();
@@ -1462,6 +1481,7 @@ __device__ __forceinline__ void cons_op(const Prog& P, Smem& sm, int oi, int op_
   if (warp == NW - 1) load_op(P, (op_idx + 1) % n_ops, cta, &sm.cop[b ^ 1], &sm.cw[b ^ 1], sm.ctask[b ^ 1]);
   // input window (other ops: the estimator G rows are loaded while it is awaited)
   if (O.attn_in) {
+    feed_prefetch(P, C, O, W, fp);       // G rows in flight while the head states are merged
     attn_merge(P, C, W.w, e_in, sm.xw);
   } else {
     feed_prefetch(P, C, O, W, fp);
