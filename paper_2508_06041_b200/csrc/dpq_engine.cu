@@ -70,7 +70,7 @@ constexpr int NTB = NT + 64;
 constexpr int kItemBytes = 2048;   // one (tile, plane) item = kTileBytes
 constexpr int kMaxSlots = DPQ_RING_SLOTS;      // ring slots (2 KB); the host checks they fit
 constexpr int kDecRing = 4;        // op decision entries in flight
-constexpr int kDbgRec = 24;        // debug stamps per (stage, CTA)
+constexpr int kDbgRec = 28;        // debug stamps per (stage, CTA)
 constexpr unsigned kPrevTag = 0x80000000u;   // previous-step sum x^2 words: tag = kPrevTag | rotation
 constexpr int kCurSlots = 4;       // estimator-set slots of the current step (step % 4)
 constexpr int kPrevSlots = 4;      // previous-step slots (rotation % 4)
@@ -429,6 +429,9 @@ struct Smem {
   float head_v[NW];
   int head_i[NW];
   double red[32];
+  double dred[kMaxOpLayers][2][32];  // reducer: per-lane estimator partials (decide_op)
+  double dest[kMaxOpLayers];         // reducer: the op's estimates, real and streaming bits
+  int dbit[kMaxOpLayers], dfin[kMaxOpLayers];
   alignas(16) float attn_q[128];     // RoPE'd q of the current attention unit
   alignas(16) float attn_m[DPQ_ATTN_WARPS][132];  // per-warp (o[hd], m, l) of the unit
   alignas(16) float xw[kWinCols];    // the op's input window
@@ -1195,27 +1198,59 @@ __device__ __forceinline__ Epi op_epi(const Prog& P, const Op& O, unsigned epoch
 // estimator accumulators (identical integers on every CTA, so every CTA takes
 // the same decisions without another exchange).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op& O, const I3& nb, I3& fin,
+__device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op& O, Smem& sm, const I3& nb, I3& fin,
                                           int cta, unsigned step_base, u64* rdbg, float* est0, I3& real) {
   const int lane = threadIdx.x & 31;
   const bool dyn = C.mode == MODE_DYNAMIC;
   // every estimating layer's words in one poll: lane holds packed G.x words
   // r = lane + 32 q and the sum x^2 word of window lane (+ 32); complete when
-  // every packed count is n_win and every sum x^2 word carries its tag
+  // every packed count is n_win and every sum x^2 word carries its tag.
+  // The descriptor fields (shared memory) are read before the poll: after it
+  // they would queue behind the consumer warps' LUT loads in the MIO pipe
+  // (~1-2 us per op, measured).
   constexpr int NQ = kMaxK / 32;
+  const int n_l = O.n_layers, n_win = O.n_win;
   const u64* base[kMaxOpLayers] = {nullptr, nullptr, nullptr};
   unsigned tag[kMaxOpLayers] = {0u, 0u, 0u};
+  int kq[kMaxOpLayers] = {0, 0, 0};
+  double fbs[kMaxOpLayers] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int li = 0; li < kMaxOpLayers; ++li) {
-    if (li >= O.n_layers) break;
+    if (li >= n_l) break;
     const Layer& L = O.L[li];
+    kq[li] = L.k;
+    fbs[li] = L.fbscale;
     if (!(dyn && L.sentinel == 0 && L.est != EST_NONE && L.est != EST_EXACT)) continue;
     const bool prev = L.src == SRC_PREV_STEP && C.has_prev;
     const int slot = prev ? kCurSlots + ((C.rot - 1) & (kPrevSlots - 1)) : (C.n_steps_done & (kCurSlots - 1));
     base[li] = P.fpart + (size_t)slot * P.set_stride + L.set;
     tag[li] = prev ? (kPrevTag | ((unsigned)(C.rot - 1) & 0x7fffffffu)) : step_base + (unsigned)L.feed_stage + 1u;
   }
+  // lane li < n_l: layer li's decision parameters
+  int d_est = 0, d_l = 0, d_h = 0, d_sent = 0, d_tr = -1, d_nb = 0, d_forced = 0;
+  bool d_xr = false;
+  double d_T = 0.0, d_slope = 0.0, d_icpt = 0.0;
+  if (lane < n_l) {
+    const Layer& L = O.L[lane];
+    d_est = L.est;
+    d_l = L.l;
+    d_h = L.h;
+    d_sent = L.sentinel;
+    d_tr = L.trace;
+    d_xr = L.xread != 0;
+    d_T = L.T;
+    d_slope = L.slope;
+    d_icpt = L.intercept;
+    d_nb = nb[lane];
+    if (C.force && d_tr >= 0) d_forced = C.forced_bits[d_tr];
+  }
+  const bool force = C.force != 0, rms = O.rms != 0;
+  const double cols = (double)O.cols, eps = (double)P.eps;
+  const bool trace_ok = dyn && cta == 0 && P.n_trace > 0 && C.trace_step < P.max_steps;
+  signed char* const tr_bits = P.tr_bits + (size_t)C.trace_step * P.n_trace;
+  float* const tr_est = P.tr_est + (size_t)C.trace_step * P.n_trace;
   u64 g[kMaxOpLayers][NQ], sw[kMaxOpLayers][2];
+  u64 t_g = 0, t_s = 0;
   {
     bool ok;
     unsigned n_ = 0;
@@ -1224,79 +1259,107 @@ __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op
       ok = true;
 #pragma unroll
       for (int li = 0; li < kMaxOpLayers; ++li) {
-        const int k = O.L[li].k;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
           const int r = q * 32 + lane;
-          g[li][q] = (base[li] && r < k) ? ld_relaxed64(base[li] + r) : ((u64)O.n_win << kCntShift);
+          g[li][q] = (base[li] && r < kq[li]) ? ld_relaxed64(base[li] + r) : ((u64)n_win << kCntShift);
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int w = q * 32 + lane;
-          sw[li][q] = (base[li] && w < O.n_win) ? ld_relaxed64(base[li] + k + w) : ((u64)tag[li] << 32);
+          sw[li][q] = (base[li] && w < n_win) ? ld_relaxed64(base[li] + kq[li] + w) : ((u64)tag[li] << 32);
         }
       }
+      bool okg = true, oks = true;
 #pragma unroll
       for (int li = 0; li < kMaxOpLayers; ++li) {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) ok &= (int)(g[li][q] >> kCntShift) == O.n_win;
+        for (int q = 0; q < NQ; ++q) okg &= (int)(g[li][q] >> kCntShift) == n_win;
 #pragma unroll
-        for (int q = 0; q < 2; ++q) ok &= (unsigned)(sw[li][q] >> 32) == tag[li];
+        for (int q = 0; q < 2; ++q) oks &= (unsigned)(sw[li][q] >> 32) == tag[li];
+      }
+      ok = okg && oks;
+      if (rdbg) {
+        const bool ag = __all_sync(0xffffffffu, okg), as = __all_sync(0xffffffffu, oks);
+        if (ag && t_g == 0) t_g = gclock();
+        if (as && t_s == 0) t_s = gclock();
       }
       if (rdbg && n_ == 0 && (threadIdx.x & 31) == 0) rdbg[22] = gclock();
       if ((++n_ & 1023u) == 0) {
         const u64 t_ = gclock();
         if (t0_ == 0) t0_ = t_;
-        else if (t_ - t0_ > 4000000000ull) hang("estimator feeds", O.L[0].trace, O.n_layers);
+        else if (t_ - t0_ > 4000000000ull) hang("estimator feeds", n_l, n_win);
       }
     } while (!__all_sync(0xffffffffu, ok));
-    if (rdbg && (threadIdx.x & 31) == 0) rdbg[23] = n_;
+    if (rdbg && (threadIdx.x & 31) == 0) {
+      rdbg[23] = n_;
+      rdbg[24] = t_g;
+      rdbg[25] = t_s;
+      rdbg[26] = gclock();
+    }
   }
+  // per-lane partials -> shared memory; lane li sums layer li's in lane order
+  // and takes its decision (no shuffle chains)
 #pragma unroll
   for (int li = 0; li < kMaxOpLayers; ++li) {
-    if (li >= O.n_layers) break;
-    const Layer& L = O.L[li];
-    int bit = nb[li];
+    if (base[li] == nullptr) continue;
+    double q = 0.0, sq = 0.0;
+#pragma unroll
+    for (int qq = 0; qq < NQ; ++qq) {
+      const int r = qq * 32 + lane;
+      if (r < kq[li]) {
+        const long long c = (long long)(g[li][qq] >> kCntShift);
+        const long long v = (long long)(g[li][qq] & ((1ull << kCntShift) - 1)) - c * kFxBias;
+        const double gv = (double)v * fbs[li];
+        q += gv * gv;
+      }
+    }
+#pragma unroll
+    for (int qq = 0; qq < 2; ++qq)
+      if (qq * 32 + lane < n_win) sq += (double)__uint_as_float((unsigned)sw[li][qq]);
+    sm.dred[li][0][lane] = q;
+    sm.dred[li][1][lane] = sq;
+  }
+  __syncwarp();
+  if (lane < n_l) {
+    const bool has = (lane == 0 ? base[0] : lane == 1 ? base[1] : base[2]) != nullptr;
+    int bit = d_nb;
     double est = CUDART_NAN;
-    const bool has = base[li] != nullptr;
-    if (L.xread && dyn) {      // dual: the real bit (the stream always reads h planes)
-      if (C.force && L.trace >= 0) bit = C.forced_bits[L.trace];
-      else if (L.sentinel == 1) bit = L.l;
-      else if (L.sentinel == 2) bit = L.h;
-      else if (L.est == EST_EXACT) bit = -1;                 // decided from ||y_h - y_l|| after the reduction
+    if (d_xr && dyn) {         // dual: the real bit (the stream always reads h planes)
+      if (force && d_tr >= 0) bit = d_forced;
+      else if (d_sent == 1) bit = d_l;
+      else if (d_sent == 2) bit = d_h;
+      else if (d_est == EST_EXACT) bit = -1;                 // decided from ||y_h - y_l|| after the reduction
     }
     if (has) {
       double q = 0.0, sq = 0.0;
-#pragma unroll
-      for (int qq = 0; qq < NQ; ++qq) {
-        const int r = qq * 32 + lane;
-        if (r < L.k) {
-          const long long c = (long long)(g[li][qq] >> kCntShift);
-          const long long v = (long long)(g[li][qq] & ((1ull << kCntShift) - 1)) - c * kFxBias;
-          const double gv = (double)v * L.fbscale;
-          q += gv * gv;
-        }
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) {
+        q += sm.dred[lane][0][i];
+        sq += sm.dred[lane][1][i];
       }
-#pragma unroll
-      for (int qq = 0; qq < 2; ++qq)
-        if (qq * 32 + lane < O.n_win) sq += (double)__uint_as_float((unsigned)sw[li][qq]);
-      q = wsum(q);
-      sq = wsum(sq);
-      const double sc = O.rms ? rsqrt_d(sq / (double)O.cols + (double)P.eps) : 1.0;
-      if (L.est == EST_PROJECTION) est = q > 0.0 ? sc * q * rsqrt_d(q) : 0.0;                 // estimator.py:56-57
-      else est = L.slope * (sq > 0.0 ? sc * sq * rsqrt_d(sq) : 0.0) + L.intercept;           // estimator.py:41-42
-      if (!C.force) bit = est > L.T ? L.h : L.l;                                              // strict > (runtime.py:192)
+      const double sc = rms ? rsqrt_d(sq / cols + eps) : 1.0;
+      if (d_est == EST_PROJECTION) est = q > 0.0 ? sc * q * rsqrt_d(q) : 0.0;                  // estimator.py:56-57
+      else est = d_slope * (sq > 0.0 ? sc * sq * rsqrt_d(sq) : 0.0) + d_icpt;                 // estimator.py:41-42
+      if (!force) bit = est > d_T ? d_h : d_l;                                               // strict > (runtime.py:192)
     }
-    real.set(li, bit);
-    fin.set(li, L.xread && dyn ? L.h : bit);                // the streaming bits (producer / consumers)
-    if (li == 0) *est0 = has ? (float)est : CUDART_NAN_F;
-    if (bit >= 0 && lane == 0 && dyn && cta == 0 && L.trace >= 0 && P.n_trace > 0 && C.trace_step < P.max_steps) {
-      const size_t o = (size_t)C.trace_step * P.n_trace + L.trace;
-      P.tr_bits[o] = (signed char)bit;
-      P.tr_est[o] = has ? (float)est : CUDART_NAN_F;
+    sm.dbit[lane] = bit;
+    sm.dfin[lane] = d_xr && dyn ? d_h : bit;              // the streaming bits (producer / consumers)
+    sm.dest[lane] = has ? est : CUDART_NAN;
+    if (bit >= 0 && trace_ok && d_tr >= 0) {
+      tr_bits[d_tr] = (signed char)bit;
+      tr_est[d_tr] = has ? (float)est : CUDART_NAN_F;
     }
   }
   __syncwarp();
+#pragma unroll
+  for (int li = 0; li < kMaxOpLayers; ++li)
+    if (li < n_l) {
+      real.set(li, sm.dbit[li]);
+      fin.set(li, sm.dfin[li]);
+    }
+  *est0 = n_l > 0 ? (float)sm.dest[0] : CUDART_NAN_F;
+  if (rdbg && lane == 0) rdbg[27] = gclock();
 }
 
 // ---------------------------------------------------------------------------
@@ -1705,7 +1768,7 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
         if (rdbg && lane == 0) rdbg[16] = gclock();
         float est0 = CUDART_NAN_F;
         I3 real = nb;
-        decide_op(P, C, O, nb, fin, cta, step_base, rdbg, &est0, real);
+        decide_op(P, C, O, sm, nb, fin, cta, step_base, rdbg, &est0, real);
         if (rdbg && lane == 0) rdbg[17] = gclock();
         if (lane == 0) {
           sm.dec_fin[oi % kDecRing][0] = fin.v0;

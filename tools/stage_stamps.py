@@ -104,7 +104,8 @@ def main():
               + " | mean " + " ".join(f"{v:6.2f}" for v in mn / c))
     if rec >= 20:
         # reducer warp phases: [16] decide start, [17] decided, [18] statistics, [19] first unit out, [7] done
-        print("reducer (max | mean over CTAs, us rel. prev stage end): decide-start first-poll feeds-done(CTA) decided stats first-unit done")
+        print("reducer (max | mean over CTAs, us rel. prev stage end): decide-start first-poll feeds-done(CTA) decided stats first-unit done"
+              + (" G.x-words-complete sumsq-words-complete poll-exit decide-return" if rec >= 28 else ""))
         oi = 0
         ragg = {}
         for k in range(n.value):
@@ -114,10 +115,10 @@ def main():
             oi += 1
             s = st[k]
             ref = last_end[k - 1]
-            cols_r = (16, 22, 20, 17, 18, 19, 7)
+            cols_r = (16, 22, 20, 17, 18, 19, 7) + ((24, 25, 26, 27) if rec >= 28 else ())
             mx = np.array([(s[:, j][s[:, j] > 0].max() - ref) / 1e3 if np.any(s[:, j] > 0) else 0 for j in cols_r])
             mn = np.array([(s[:, j][s[:, j] > 0].mean() - ref) / 1e3 if np.any(s[:, j] > 0) else 0 for j in cols_r])
-            a_ = ragg.setdefault(nm, [0, np.zeros(7), np.zeros(7), 0.0])
+            a_ = ragg.setdefault(nm, [0, np.zeros(len(cols_r)), np.zeros(len(cols_r)), 0.0])
             a_[3] += float(np.mean(buf.reshape(n.value, G, rec)[k][:, 23].astype(np.float64)))
             a_[0] += 1
             a_[1] += mx
