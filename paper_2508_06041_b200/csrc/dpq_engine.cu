@@ -429,7 +429,7 @@ struct Smem {
   float head_v[NW];
   int head_i[NW];
   double red[32];
-  double dred[kMaxOpLayers][2][32];  // reducer: per-lane estimator partials (decide_op)
+  alignas(16) double dred[kMaxOpLayers][2][32];  // reducer: per-lane estimator partials (decide_op)
   double dest[kMaxOpLayers];         // reducer: the op's estimates, real and streaming bits
   int dbit[kMaxOpLayers], dfin[kMaxOpLayers];
   alignas(16) float attn_q[128];     // RoPE'd q of the current attention unit
@@ -1245,7 +1245,7 @@ __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op
     if (C.force && d_tr >= 0) d_forced = C.forced_bits[d_tr];
   }
   const bool force = C.force != 0, rms = O.rms != 0;
-  const double cols = (double)O.cols, eps = (double)P.eps;
+  const double inv_cols = 1.0 / (double)O.cols, eps = (double)P.eps;
   const bool trace_ok = dyn && cta == 0 && P.n_trace > 0 && C.trace_step < P.max_steps;
   signed char* const tr_bits = P.tr_bits + (size_t)C.trace_step * P.n_trace;
   float* const tr_est = P.tr_est + (size_t)C.trace_step * P.n_trace;
@@ -1332,13 +1332,18 @@ __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op
       else if (d_est == EST_EXACT) bit = -1;                 // decided from ||y_h - y_l|| after the reduction
     }
     if (has) {
-      double q = 0.0, sq = 0.0;
-#pragma unroll 8
-      for (int i = 0; i < 32; ++i) {
-        q += sm.dred[lane][0][i];
-        sq += sm.dred[lane][1][i];
+      double qa[4] = {0.0, 0.0, 0.0, 0.0}, sa[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const double2 a = *reinterpret_cast<const double2*>(&sm.dred[lane][0][i]);
+        const double2 b = *reinterpret_cast<const double2*>(&sm.dred[lane][0][i + 2]);
+        const double2 c = *reinterpret_cast<const double2*>(&sm.dred[lane][1][i]);
+        const double2 d = *reinterpret_cast<const double2*>(&sm.dred[lane][1][i + 2]);
+        qa[0] += a.x; qa[1] += a.y; qa[2] += b.x; qa[3] += b.y;
+        sa[0] += c.x; sa[1] += c.y; sa[2] += d.x; sa[3] += d.y;
       }
-      const double sc = rms ? rsqrt_d(sq / cols + eps) : 1.0;
+      const double q = (qa[0] + qa[1]) + (qa[2] + qa[3]), sq = (sa[0] + sa[1]) + (sa[2] + sa[3]);
+      const double sc = rms ? rsqrt_d(sq * inv_cols + eps) : 1.0;
       if (d_est == EST_PROJECTION) est = q > 0.0 ? sc * q * rsqrt_d(q) : 0.0;                  // estimator.py:56-57
       else est = d_slope * (sq > 0.0 ? sc * sq * rsqrt_d(sq) : 0.0) + d_icpt;                 // estimator.py:41-42
       if (!force) bit = est > d_T ? d_h : d_l;                                               // strict > (runtime.py:192)
