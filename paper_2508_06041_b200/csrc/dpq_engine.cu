@@ -516,6 +516,17 @@ __device__ __forceinline__ void load_op(const Prog& P, int oi, int cta, Op* O, C
 // TMA / mbarrier helpers
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// Ring slot sl's offset in the dynamic shared memory (the layout the kernel
+// prologue builds in sm.slot_off: below the LUT after Smem, then above its zero
+// row), computed in registers: a shared-memory table read per item queues
+// behind the consumers' LUT loads.
+__device__ __forceinline__ uint32_t slot_offset(const void* smem0, int sl) {
+  const uint32_t base = smem_u32(smem0);
+  const uint32_t lo = (base + (uint32_t)sizeof(Smem) + 127u) & ~127u;
+  const int n_lo = lo + kItemBytes <= kLut ? (int)((kLut - lo) / kItemBytes) : 0;
+  return (sl < n_lo ? lo + (uint32_t)sl * kItemBytes : kLut + kLutBytes + (uint32_t)(sl - n_lo) * kItemBytes) - base;
+}
+
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count));
 }
@@ -1398,7 +1409,7 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
       }
       sm.seq[slot] = j;
       mbar_expect_tx(&sm.full[slot], (unsigned)kItemBytes);
-      tma_load_1d(const_cast<unsigned char*>(dyn0) + sm.slot_off[slot], src0 + (long long)p * pstride,
+      tma_load_1d(const_cast<unsigned char*>(dyn0) + slot_offset(&sm, slot), src0 + (long long)p * pstride,
                   (unsigned)kItemBytes, &sm.full[slot], l2pol);
     }
   };
@@ -1516,7 +1527,7 @@ __device__ __forceinline__ float stream_task(Smem& sm, int j0, int n, uint32_t l
     const uint32_t fa = smem_u32(&sm.full[sl]);
     const unsigned fpar = (unsigned)((j / kMaxSlots) & 1);
     SPIN_UNTIL_NS(mbar_test(fa, fpar), "ring slot", j, fpar, 4000000000ull);
-    const uint4* d = reinterpret_cast<const uint4*>(dyn0 + sm.slot_off[sl]) + lane;
+    const uint4* d = reinterpret_cast<const uint4*>(dyn0 + slot_offset(&sm, sl)) + lane;
     const uint4 d0 = d[0], d1 = d[32], d2 = d[64], d3 = d[96];
     __syncwarp();
     if (lane == 0) mbar_arrive_n(&sm.empty[sl], 1u);
@@ -1795,23 +1806,34 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
                                                        (O.n_layers > 2 && O.L[2].xread));
           if (dual) dual_units(P, C, O, sm, cta, G, nb, fin, real, E, epoch, e_res);
           // the affine epilogue (quant.py:74-78): y = s_in (lo sum x + span 2^-b (S + sum x / 2))
+          // descriptor fields in registers before the unit polls: shared-memory
+          // reads after a poll queue behind the consumers' LUT loads (MIO)
+          const bool o_pair = O.pair != 0, o_push = O.push != 0, o_add = O.add != 0, o_plain = O.plain_io != 0;
+          const bool tp1 = P.tp_size == 1;
+          u64* const o_out = O.out;
+          float* const y_out = P.y_out;
+          auto store_out = [&](u64* dst, float v) {
+            if (o_push && !tp1) st_tag_all(P, dst, v, epoch);
+            else __stcg(dst, ((u64)epoch << 32) | __float_as_uint(v));
+          };
           for (int u = cta; !dual && u < O.n_units; u += G) {
-            if (O.pair) {
+            if (o_pair) {
               // unit u: up tile u and gate tile u (runtime.py:366-368)
               const int half = O.L[0].n_tiles;
               const int r = u * 32 + lane;
               float lo0 = 0.f, sp0 = 0.f, lo1 = 0.f, sp1 = 0.f;
-              if (r < O.L[0].rows) {
+              const bool ok = r < O.L[0].rows;
+              u64* const dst = o_out + O.L[0].out_off + r;
+              if (ok) {
                 lo0 = __ldg(O.L[0].lo + r); sp0 = __ldg(O.L[0].span + r);
                 lo1 = __ldg(O.L[1].lo + r); sp1 = __ldg(O.L[1].span + r);
               }
               const float2 S = tiles_S(P, O, u, fin.v0 - nb.v0, u + half, fin.v1 - nb.v1, epoch);
-              if (r < O.L[0].rows) {
+              if (ok) {
                 const float up = E.scale * (lo0 * E.sx + ldexpf(sp0, -fin.v0) * (S.x + 0.5f * E.sx));
                 const float gt = E.scale * (lo1 * E.sx + ldexpf(sp1, -fin.v1) * (S.y + 0.5f * E.sx));
                 const float hv = up * (gt / (1.0f + expf(-gt)));                 // runtime.py:368
-                if (O.push) st_tag_all(P, O.out + O.L[0].out_off + r, hv, epoch);
-                else st_tag(O.out + O.L[0].out_off + r, hv, epoch);
+                store_out(dst, hv);
               }
             } else {
               const int li = layer_of(O, u);
@@ -1819,25 +1841,26 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
               const int r = (u - L.tile_off) * 32 + lane;
               const bool ok = r < L.rows;
               const int o = L.out_off + r;
+              const int bl = fin[li];
+              const u64* const res_p = O.res_in + o;
               float lo = 0.f, sp = 0.f, res = 0.f;
               if (ok) {
                 lo = __ldg(L.lo + r);
                 sp = __ldg(L.span + r);
               }
               u64 xr = 0;
-              if (O.add && ok) xr = ld_relaxed64(O.res_in + o);
-              const float S = tiles_S(P, O, u, fin[li] - nb[li], -1, 0, epoch).x;
+              if (o_add && ok) xr = ld_relaxed64(res_p);
+              const float S = tiles_S(P, O, u, bl - nb[li], -1, 0, epoch).x;
               if (ok) {
-                float v = E.scale * (lo * E.sx + ldexpf(sp, -fin[li]) * (S + 0.5f * E.sx));
-                if (O.add) {                                                            // runtime.py:364, 370
+                float v = E.scale * (lo * E.sx + ldexpf(sp, -bl) * (S + 0.5f * E.sx));
+                if (o_add) {                                                            // runtime.py:364, 370
                   if ((unsigned)(xr >> 32) != e_res)
-                    SPIN_UNTIL((xr = ld_relaxed64(O.res_in + o), (unsigned)(xr >> 32) == e_res), "residual", o, e_res);
+                    SPIN_UNTIL((xr = ld_relaxed64(res_p), (unsigned)(xr >> 32) == e_res), "residual", o, e_res);
                   res = __uint_as_float((unsigned)xr);
                   v = res + v;
                 }
-                if (O.plain_io) P.y_out[o] = v;
-                else if (O.push) st_tag_all(P, O.out + o, v, epoch);
-                else st_tag(O.out + o, v, epoch);
+                if (o_plain) y_out[o] = v;
+                else store_out(o_out + o, v);
               }
             }
             if (rdbg && lane == 0 && u == cta) rdbg[19] = gclock();
