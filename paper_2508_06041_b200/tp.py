@@ -113,7 +113,8 @@ def shard_plan_layers(plan: PrecisionPlan, ids, world: int, rank: int):
         pl = plan.layers[lid]
         est = pl.estimator
         if est is not None and not math.isinf(pl.T) and isinstance(est.kind, E.ExactEstimator):
-            raise NotImplementedError("exact estimators need a partial-norm all-reduce; not on the TP engine")
+            raise NotImplementedError("exact estimators under tensor parallelism: the engine keeps the "
+                                      "||y_h - y_l|| sets per rank (no partial-norm exchange)")
         if est is not None and hasattr(est.kind, "G") and not math.isinf(pl.T):
             G = np.ascontiguousarray(est.kind.G, dtype=np.float64)
             k = G.shape[0]
@@ -161,7 +162,8 @@ class TPDecodeEngine(DecodeEngine):
         if store.config_hash != weights.config.hash():
             raise ProvenanceError("store/model config mismatch")
         if track_exact:
-            raise NotImplementedError("track_exact needs the per-op graph; not on the TP engine")
+            raise NotImplementedError("track_exact under tensor parallelism: the engine keeps the "
+                                      "||y_h - y_l|| sets per rank (no partial-norm exchange)")
         if async_rule not in ("prev_step", "prev_block"):
             raise ValueError(f"unknown async rule {async_rule!r}")
         cfg = weights.config

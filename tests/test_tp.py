@@ -171,3 +171,14 @@ def test_tp2_device_greedy_loop():
     ids = store.ordered_ids()
     assert [[s.bits[l] for l in ids] for s in grp.trace.steps] == [[s.bits[l] for l in ids] for s in tr1.steps]
     grp.close()
+
+
+@pytest.mark.gpu
+def test_tp_rejects_exact_sets():
+    """track_exact (and exact estimators) keep their ||y_h - y_l|| sets per
+    rank, so a tensor-parallel session with them is refused with the reason
+    instead of running with partial norms (host check in tp.py; the C-ABI
+    session refuses them too)."""
+    w, store, plan, _ = _model_and_plan()
+    with pytest.raises(NotImplementedError, match="tensor parallelism"):
+        TP.LocalTPGroup(w, store, plan, 2, track_exact=True)
