@@ -283,7 +283,9 @@ int gv_run(dpq_store* s, const dpq_plan* p, int li, int b, const float* x, float
   A.y = y;
   A.bit_out = bit_out;
   A.est_out = est_out;
-  TRY(launch(gv::bitplane_gemv_kernel, dim3(G), dim3(gv::kNT), (size_t)s->gv_smem, st, false, A));
+  const char* pdl_env = getenv("DPQ_GEMV_PDL");
+  const bool pdl = !(pdl_env && pdl_env[0] == '0');
+  TRY(launch(gv::bitplane_gemv_kernel, dim3(G), dim3(gv::kNT), (size_t)s->gv_smem, st, pdl, A));
   *used = true;
   return DPQ_OK;
 }

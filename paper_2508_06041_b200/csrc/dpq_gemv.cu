@@ -242,6 +242,11 @@ extern "C" __global__ void __launch_bounds__(kNT, 1) bitplane_gemv_kernel(const 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // programmatic dependent launch: the next call's grid may be scheduled now
+  // (its CTAs take an SM as this grid's CTAs exit and stream their weights);
+  // everything that reads the previous call's results (x, the scratch sums)
+  // waits for it below (griddepcontrol.wait)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (tid == 0) GV_STAMP(1);
   if (warp == kCW) {
     // ---- TMA producer (lane 0): base planes 0..l-1 of every group, then (high) l..h-1
@@ -289,6 +294,7 @@ extern "C" __global__ void __launch_bounds__(kNT, 1) bitplane_gemv_kernel(const 
     // the decision: every CTA from the same fixed-point sums
     int bit = A.sentinel == 2 ? A.h : A.l;
     double est = CUDART_NAN;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (A.sentinel == 0) {
       const int n_jobs = A.n_win * (A.est_kind == EST_PROJECTION ? A.k : 1);
       if (lane == 0) SPIN_UNTIL(eng::ld_acq_s32(A.sync) >= n_jobs, "gemv estimator", n_jobs, 0);
@@ -329,6 +335,7 @@ extern "C" __global__ void __launch_bounds__(kNT, 1) bitplane_gemv_kernel(const 
   }
   // ---- consumers
   if (nt <= 0) return;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int nw = (t1 - 1) / A.n_tiles - w0 + 1;   // <= 2 (host-checked)
   // input windows -> shared memory, window sums of x (and x^2 for the estimator)
   if (tid < 128 * nw) {
