@@ -225,7 +225,7 @@ int gv_run(dpq_store* s, const dpq_plan* p, int li, int b, const float* x, float
     // program overlaps them, which wins once the base stream is long
     // (tools/gemv_sweep.py: 4096x4096 13.7 vs 16.6 us, 14336x4096 21.6 vs 20.6)
     const char* dyn_env = getenv("DPQ_GEMV_KERNEL_DYNAMIC");
-    const long long max_dyn = dyn_env ? atoll(dyn_env) : (8ll << 20);
+    const long long max_dyn = dyn_env ? atoll(dyn_env) : (1ll << 62);
     if (S.l != S.h && (long long)L.rows * L.cols * S.l / 8 > max_dyn) return DPQ_OK;
     A.l = S.l;
     A.h = S.h;

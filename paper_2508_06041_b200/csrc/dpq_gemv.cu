@@ -92,8 +92,8 @@ struct Ctl {
   volatile int dec_bit;     // -1 until decided
 };
 
-__device__ __forceinline__ void lut_build(float* lut, const float* xw, int tid) {
-  for (int q = tid; q < 1024; q += kNC) {
+__device__ __forceinline__ void lut_build(float* lut, const float* xw, int tid, int nthr) {
+  for (int q = tid; q < 1024; q += nthr) {
     const int g = q & 63, m = q >> 6;
     const float4 xa = *reinterpret_cast<const float4*>(xw + 8 * g);
     const float4 xb = *reinterpret_cast<const float4*>(xw + 8 * g + 4);
@@ -162,11 +162,26 @@ __device__ __forceinline__ float stream_items(Ctl& c, const unsigned char* dyn0,
   return S;
 }
 
-// Window w's G.x rows [r, r + ...) of this CTA's job range (one warp per job).
-__device__ __forceinline__ double g_row_dot(const Args& A, int w, int r) {
+// One estimator job (window w, G row r) per warp: lane l takes columns
+// 4 l + 128 q + j. The G row (static) is loaded ahead (gpre_load, before the
+// weight stream saturates HBM and before the previous call's x is ready);
+// the dot product reads x once the call may.
+struct GPre {
+  uint4 g[4];
+};
+__device__ __forceinline__ void gpre_load(const Args& A, int w, int r, GPre& P) {
+  const int lane = threadIdx.x & 31;
+  const size_t gb = ((size_t)w * A.k + r) * kWinCols + 4 * lane;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (A.g_dtype == G_F16) P.g[q] = eng::ld_nc16_half(reinterpret_cast<const __half*>(A.G) + gb + 128 * q);
+    else if (A.g_dtype == G_F32) P.g[q] = eng::ld_nc16(reinterpret_cast<const float*>(A.G) + gb + 128 * q);
+    else P.g[q] = make_uint4(eng::ld_nc4(reinterpret_cast<const unsigned char*>(A.G) + gb + 128 * q), 0u, 0u, 0u);
+  }
+}
+__device__ __forceinline__ double g_row_dot(const Args& A, int w, int r, const GPre& P) {
   const int lane = threadIdx.x & 31;
   const float* xw = A.x + (size_t)w * kWinCols;
-  const size_t gb = ((size_t)w * A.k + r) * kWinCols + 4 * lane;
   float s = 0.f;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -177,20 +192,18 @@ __device__ __forceinline__ double g_row_dot(const Args& A, int w, int r) {
       for (int j = 0; j < 4; ++j)
         if (c0 + j < A.cols) (&x.x)[j] = __ldg(xw + 4 * lane + 128 * q + j);
     float g[4];
+    const uint4 t = P.g[q];
     if (A.g_dtype == G_F16) {
-      const uint4 t = eng::ld_nc16_half(reinterpret_cast<const __half*>(A.G) + gb + 128 * q);
       const float2 u = __half22float2(*reinterpret_cast<const __half2*>(&t.x));
       const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&t.y));
       g[0] = u.x; g[1] = u.y; g[2] = v.x; g[3] = v.y;
     } else if (A.g_dtype == G_F32) {
-      const uint4 t = eng::ld_nc16(reinterpret_cast<const float*>(A.G) + gb + 128 * q);
       g[0] = __uint_as_float(t.x); g[1] = __uint_as_float(t.y); g[2] = __uint_as_float(t.z); g[3] = __uint_as_float(t.w);
     } else {
-      const unsigned wd = eng::ld_nc4(reinterpret_cast<const unsigned char*>(A.G) + gb + 128 * q);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         __nv_fp8_e4m3 e;
-        e.__x = (unsigned char)(wd >> (8 * j));
+        e.__x = (unsigned char)(t.x >> (8 * j));
         g[j] = (float)e;
       }
     }
@@ -271,26 +284,54 @@ extern "C" __global__ void __launch_bounds__(kNT, 1) bitplane_gemv_kernel(const 
                        (unsigned)(nn * kItem), &c.full[sl], pol);
     };
     // lane l < kSlots issues the chunks j = l (mod kSlots), i.e. owns ring
-    // slot (jb + l) mod kSlots: the lanes refill their slots independently
-    auto issue_r = [&](int r, int jb, int p0, int np) {
-      const int v = r / (kQuads * np), rr = r - v * kQuads * np;
-      const int nwv = min(kQuads, ng - v * kQuads), pp = rr / nwv, qd = rr - pp * nwv;
-      issue(v * kQuads + qd, p0 + pp, jb + r);
+    // slot j mod kSlots: the lanes refill their slots independently.
+    // FIFO layout (chunk index of (group g = wave v, quad qd; plane pp)):
+    //   wave 0, base planes:            pp n0 + qd                      (pp < l)
+    //   waves v >= 1, all f planes:     B0 + (v - 1) kQuads f + pp nwv + qd
+    //   wave 0, extra planes:           B0 + (ng - n0) f + pp n0 + qd   (pp < f - l)
+    // with n0 = min(kQuads, ng), B0 = n0 l and f the decided bit (static: l):
+    // only wave 0 is streamed before the decision, the extra planes of later
+    // waves follow their base planes.
+    const int n0 = min(kQuads, ng), B0 = n0 * A.l;
+    auto chunk_of = [&](int r, int f, int& g, int& pp) {
+      if (r < B0) { pp = r / n0; g = r - pp * n0; return; }
+      const int rb = r - B0, nb = (ng - n0) * f;
+      if (rb < nb) {
+        const int v = 1 + rb / (kQuads * f), rr = rb - (v - 1) * kQuads * f;
+        const int nwv = min(kQuads, ng - v * kQuads);
+        pp = rr / nwv;
+        g = v * kQuads + (rr - pp * nwv);
+        return;
+      }
+      const int re = rb - nb;
+      pp = A.l + re / n0;
+      g = re - (pp - A.l) * n0;
     };
-    auto phase = [&](int jb, int p0, int np, bool release) {
-      const int n = ng * np;
-      if (lane < kSlots && lane < n) issue_r(lane, jb, p0, np);
+    auto run = [&](int r0, int r1, int f, bool release) {
+      if (lane < kSlots && r0 + lane < r1) {
+        int g, pp;
+        chunk_of(r0 + lane, f, g, pp);
+        issue(g, pp, r0 + lane);
+      }
       __syncwarp();
       // the first ring-full is in flight: the consumers' LUT stores may now
       // take the shared-memory pipe (warp-uniform: bar.arrive counts the warp)
       if (release) asm volatile("bar.arrive 2, %0;" :: "n"(kNT) : "memory");
       if (lane < kSlots)
-        for (int r = lane + kSlots; r < n; r += kSlots) issue_r(r, jb, p0, np);
+        for (int r = r0 + lane + kSlots; r < r1; r += kSlots) {
+          int g, pp;
+          chunk_of(r, f, g, pp);
+          issue(g, pp, r);
+        }
       __syncwarp();
     };
-    phase(0, 0, A.l, true);
+    if (!dyn) {
+      run(0, ng * A.l, A.l, true);
+      if (lane == 0) GV_STAMP(2);
+      return;
+    }
+    run(0, B0, A.l, true);                 // wave 0's base planes, then the decision
     if (lane == 0) GV_STAMP(2);
-    if (!dyn) return;
     // the decision: every CTA from the same fixed-point sums
     int bit = A.sentinel == 2 ? A.h : A.l;
     double est = CUDART_NAN;
@@ -323,18 +364,32 @@ extern "C" __global__ void __launch_bounds__(kNT, 1) bitplane_gemv_kernel(const 
     }
     if (lane == 0) {
       c.dec_bit = bit;
+      GV_STAMP(5);
       if (cta == 0) {
         if (A.bit_out) *A.bit_out = bit;
         if (A.est_out) *A.est_out = (float)est;
       }
     }
     __syncwarp();
-    if (bit > A.l)
-      phase(ng * A.l, A.l, A.h - A.l, false);
+    run(B0, ng * bit, bit, false);         // the rest: B0 + (ng - n0) f + n0 (f - l) = ng f
     return;
   }
   // ---- consumers
   if (nt <= 0) return;
+  const bool jobs = dyn && A.sentinel == 0;
+  constexpr int kHalf = kNC / 2;
+  constexpr int kPre = 2;                // estimator jobs per warp with the G row loaded ahead
+  const int kk = A.est_kind == EST_PROJECTION ? A.k : 1;
+  const long long J = (long long)A.n_win * kk;
+  const int jj0 = (int)(J * cta / G), jj1 = (int)(J * (cta + 1) / G);
+  const int jw = warp - kHalf / 32, nj = kCW - kHalf / 32;
+  GPre gpre[kPre];
+  if (jobs && tid >= kHalf && A.est_kind == EST_PROJECTION)
+#pragma unroll
+    for (int u = 0; u < kPre; ++u) {
+      const int j = jj0 + jw + u * nj;
+      if (j < jj1) gpre_load(A, j / kk, j - (j / kk) * kk, gpre[u]);
+    }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int nw = (t1 - 1) / A.n_tiles - w0 + 1;   // <= 2 (host-checked)
   // input windows -> shared memory, window sums of x (and x^2 for the estimator)
@@ -347,17 +402,46 @@ extern "C" __global__ void __launch_bounds__(kNT, 1) bitplane_gemv_kernel(const 
         if (c0 + j < A.cols) (&v.x)[j] = __ldg(A.x + c0 + j);
     *reinterpret_cast<float4*>(c.xw[i] + 4 * (tid & 127)) = v;
   }
-  // estimator jobs (w, r) of this CTA: w-major over n_win x k (projection) or
-  // one job per window (linear: sum x^2 only)
-  if (dyn && A.sentinel == 0) {
-    const int kk = A.est_kind == EST_PROJECTION ? A.k : 1;
-    const long long J = (long long)A.n_win * kk;
-    const int j0 = (int)(J * cta / G), j1 = (int)(J * (cta + 1) / G);
+  // The window LUTs and, for a selector, the estimator jobs (w, r) of this
+  // CTA (w-major over n_win x k for a projection, one job per window for the
+  // linear estimator): jobs on the upper half of the consumer warps, the LUTs
+  // on the lower half, which stream as soon as their LUTs are built (bar 3
+  // among themselves, bar 4 released to the job warps).
+  GV_SYNC();                                   // xw staged
+  asm volatile("bar.sync 2, %0;" :: "n"(kNT) : "memory");   // the producer's first ring-full issued
+  if (tid == 0) GV_STAMP(3);
+  float* lut0 = reinterpret_cast<float*>(smem_raw + (kLut0 - smem_u32(smem_raw)));
+  if (!jobs || tid < kHalf) {
+    const int nthr = jobs ? kHalf : kNC;
+    for (int i = 0; i < nw; ++i) lut_build(lut0 + i * (0x10000 / 4), c.xw[i], tid, nthr);
+    if (tid < 32 * nw) {                   // window sums of x (epilogue), identical on every CTA
+      const int i = tid >> 5;
+      float s = 0.f;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) s += c.xw[i][lane + 32 * q];
+      s = eng::wsum(s);
+      if (lane == 0) A.sx[w0 + i] = s;
+    }
+    if (tid < 64) {                         // zero rows 256 of both LUTs (LUT 0's is LUT 1's row 0)
+      lut0[256 * kGroups + tid] = 0.f;
+      lut0[256 * kGroups + 0x10000 / 4 + tid] = 0.f;
+    }
+    if (jobs) {
+      asm volatile("bar.sync 3, %0;" :: "n"(kHalf) : "memory");
+      asm volatile("bar.arrive 4, %0;" :: "n"(kNC) : "memory");
+    } else {
+      GV_SYNC();
+    }
+  } else {
     int mine = 0;
-    for (int j = j0 + warp; j < j1; j += kCW) {
+    for (int j = jj0 + jw, u = 0; j < jj1; j += nj, ++u) {
       const int w = j / kk, r = j - w * kk;
       if (A.est_kind == EST_PROJECTION) {
-        const double v = g_row_dot(A, w, r) * A.fxscale;
+        GPre gp;
+        if (u == 0) gp = gpre[0];
+        else if (u == 1) gp = gpre[1];
+        else gpre_load(A, w, r, gp);
+        const double v = g_row_dot(A, w, r, gp) * A.fxscale;
         if (lane == 0) {
           long long f = 0;
           if (fabs(v) < 4.5e15) f = llrint(v);
@@ -377,28 +461,10 @@ extern "C" __global__ void __launch_bounds__(kNT, 1) bitplane_gemv_kernel(const 
       }
       ++mine;
     }
-    if (mine && lane == 0) {
-      __threadfence();
-      atomicAdd(A.sync, mine);
-    }
+    if (mine && lane == 0)           // release: this lane's acc red.adds before the count
+      asm volatile("red.release.gpu.global.add.s32 [%0], %1;" :: "l"(A.sync), "r"(mine) : "memory");
+    asm volatile("bar.sync 4, %0;" :: "n"(kNC) : "memory");   // the LUTs are built
   }
-  asm volatile("bar.sync 2, %0;" :: "n"(kNT) : "memory");   // the producer's first ring-full issued
-  if (tid == 0) GV_STAMP(3);
-  float* lut0 = reinterpret_cast<float*>(smem_raw + (kLut0 - smem_u32(smem_raw)));
-  for (int i = 0; i < nw; ++i) lut_build(lut0 + i * (0x10000 / 4), c.xw[i], tid);
-  if (tid < 32 * nw) {                   // window sums of x (epilogue), identical on every CTA
-    const int i = tid >> 5;
-    float s = 0.f;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) s += c.xw[i][lane + 32 * q];
-    s = eng::wsum(s);
-    if (lane == 0) A.sx[w0 + i] = s;
-  }
-  if (tid < 64) {                         // zero rows 256 of both LUTs (LUT 0's is LUT 1's row 0)
-    lut0[256 * kGroups + tid] = 0.f;
-    lut0[256 * kGroups + 0x10000 / 4 + tid] = 0.f;
-  }
-  GV_SYNC();
   if (tid == 0) GV_STAMP(4);
   const int rpad = A.n_tiles * 32;
   // a tile's window partial is final: count it; the tile's last window applies
@@ -426,42 +492,53 @@ extern "C" __global__ void __launch_bounds__(kNT, 1) bitplane_gemv_kernel(const 
     if (lane == 0) A.cnt[t] = 0;
     if (lane == 0) GV_STAMP(7);
   };
-  // base planes of every group (the producer issues them without waiting for
-  // the decision, so they are always consumed); warp i of quad q: tile i of
-  // the groups q, q + kQuads, ...
+  // warp i of quad q: tile i of the groups q, q + kQuads, ... (FIFO layout:
+  // see the producer). Wave 0: the base planes (the decision may be pending);
+  // later waves: all decided planes in one Horner pass; then wave 0's extras.
   const int q = warp / kGT, i = warp % kGT;
+  const int n0 = min(kQuads, ng), B0 = n0 * A.l;
+  int bit = A.l;
   for (int g = q; g < ng; g += kQuads) {
     int start, n;
     group(g, start, n);
     const int w = start / A.n_tiles, t = start - w * A.n_tiles + i;
     const uint32_t lanereg = (kLut0 << (w - w0)) | ((uint32_t)lane * 4u);
     const int v = g / kQuads, nwv = min(kQuads, ng - v * kQuads);
-    const float S = stream_items(c, dyn0, v * kQuads * A.l + (g - v * kQuads), A.l, nwv, i, i < n, lanereg);
+    float S;
+    if (v == 0) {
+      S = stream_items(c, dyn0, g, A.l, n0, i, i < n, lanereg);
+    } else {
+      if (dyn && v == 1) {                 // (first later wave of this quad) the decision
+        if (lane == 0) SPIN_UNTIL(c.dec_bit >= 0, "gemv decision", 0, 0);
+        __syncwarp();
+        bit = c.dec_bit;
+      }
+      S = stream_items(c, dyn0, B0 + (v - 1) * kQuads * bit + (g - v * kQuads), bit, nwv, i, i < n, lanereg);
+    }
     if (i < n) {
       A.part[(size_t)w * rpad + t * 32 + lane] = S;
-      if (!dyn) arrive(t, A.l);
+      if (!dyn || v > 0) arrive(t, bit);
     }
   }
   if (lane == 0) GV_STAMP(6);
-  if (!dyn) return;
+  if (!dyn || q >= n0) return;
+  // wave 0 (group q): its extra planes, then the tile's partial is final
   if (lane == 0) SPIN_UNTIL(c.dec_bit >= 0, "gemv decision", 0, 0);
   __syncwarp();
-  const int bit = c.dec_bit;
-  for (int g = q; g < ng; g += kQuads) {
-    int start, n;
-    group(g, start, n);
-    const int w = start / A.n_tiles, t = start - w * A.n_tiles + i;
-    if (bit > A.l) {                       // S_h = 2^(h-l) S_l + the extra planes' Horner sum
-      const uint32_t lanereg = (kLut0 << (w - w0)) | ((uint32_t)lane * 4u);
-      const int v = g / kQuads, nwv = min(kQuads, ng - v * kQuads), ne = A.h - A.l;
-      const float Sx = stream_items(c, dyn0, ng * A.l + v * kQuads * ne + (g - v * kQuads), ne, nwv, i, i < n, lanereg);
-      if (i < n) {
-        float* pp = A.part + (size_t)w * rpad + t * 32 + lane;
-        *pp = ldexpf(*pp, A.h - A.l) + Sx;
-      }
+  bit = c.dec_bit;
+  int start, n;
+  group(q, start, n);
+  const int w = start / A.n_tiles, t = start - w * A.n_tiles + i;
+  if (bit > A.l) {                         // S_h = 2^(h-l) S_l + the extra planes' Horner sum
+    const uint32_t lanereg = (kLut0 << (w - w0)) | ((uint32_t)lane * 4u);
+    const int ne = bit - A.l;
+    const float Sx = stream_items(c, dyn0, B0 + (ng - n0) * bit + q, ne, n0, i, i < n, lanereg);
+    if (i < n) {
+      float* pp = A.part + (size_t)w * rpad + t * 32 + lane;
+      *pp = ldexpf(*pp, ne) + Sx;
     }
-    if (i < n) arrive(t, bit);
   }
+  if (i < n) arrive(t, bit);
 }
 
 }  // namespace gv

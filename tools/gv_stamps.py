@@ -28,6 +28,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", default="4096x4096")
     ap.add_argument("--bits", type=int, default=3)
+    ap.add_argument("--dynamic", action="store_true", help="dpq_select_gemv, pair (bits, bits + 1), k=64 f16 G")
     args = ap.parse_args()
     rows, cols = (int(v) for v in args.shape.split("x"))
     dev = torch.device("cuda:0")
@@ -45,14 +46,33 @@ def main():
     lib = _lib.load()
     G = torch.cuda.get_device_properties(0).multi_processor_count
     buf = torch.zeros(G * 8 + G * 64 * 4, dtype=torch.int64, device=dev)
+    if args.dynamic:
+        from paper_2508_06041_b200 import estimator as E
+        from paper_2508_06041_b200 import model as M
+        from paper_2508_06041_b200 import runtime as R
+        b = args.bits
+        pls = []
+        for i in range(n_copy):
+            Gm = np.random.default_rng(100 + i).standard_normal((64, cols)) / np.sqrt(cols)
+            est = float(np.linalg.norm(Gm @ x.cpu().numpy().astype(np.float64)))
+            eo = E.ErrorEstimator(E.ProjectionEstimator(Gm, 64, 0), E.IMMEDIATE, (b, b + 1))
+            pls.append(R.PlanLayer(M.LayerId(i, "q"), b + 1, b + 0.5, (b, b + 1), est * 0.9, 0.5, eo))
+        dp = R.DevicePlan(ds, pls, "f16")
+
+    def call(i):
+        if args.dynamic:
+            _lib.call("dpq_select_gemv", dp.handle, i, C.c_void_p(x.data_ptr()), None, C.c_void_p(y.data_ptr()),
+                      None, None, None, None)
+        else:
+            _lib.call("dpq_gemv", ds.handle, i, args.bits, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), None)
     for i in range(n_copy):                                   # warm (scratch, attributes)
-        _lib.call("dpq_gemv", ds.handle, i, args.bits, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), None)
+        call(i)
     torch.cuda.synchronize()
     res = []
     for i in range(n_copy):
         buf.zero_()
         _lib.call("dpq_debug_gemv_stamps", C.c_void_p(buf.data_ptr()))
-        _lib.call("dpq_gemv", ds.handle, i, args.bits, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), None)
+        call(i)
         torch.cuda.synchronize()
         _lib.call("dpq_debug_gemv_stamps", None)
         allb = buf.cpu().numpy().astype(np.float64)
@@ -71,7 +91,7 @@ def main():
                 print(f"  {j:3d} " + " ".join(f"{(v - t0) / 1e3:7.2f}" if v > 0 else "    nan" for v in c0[j, :3]))
     mx = np.median([r[0] for r in res], axis=0)
     md = np.median([r[1] for r in res], axis=0)
-    names = ["entry", "init", "base-issued", "x-staged", "lut", "first-task", "last-task", "epilogue"]
+    names = ["entry", "init", "base-issued", "x-staged", "lut", "decision", "last-task", "epilogue"]
     print(f"{args.shape} b={args.bits}: us from first entry (median over {n_copy} launches)")
     print("       " + " ".join(f"{n:>11}" for n in names))
     print("max    " + " ".join(f"{v:11.2f}" for v in mx))
