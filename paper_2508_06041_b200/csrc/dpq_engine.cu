@@ -50,6 +50,18 @@
 #ifndef DPQ_PF_ITEMS
 #define DPQ_PF_ITEMS 0             // (measured slower at 64-256) next op's first base items prefetched into L2 per CTA
 #endif
+#ifndef DPQ_SEQ_SLEEP
+#define DPQ_SEQ_SLEEP 100          // ns of back-off while a ring item is not yet issued (measured: -1.2%)
+#endif
+#ifndef DPQ_CONS_SLEEP
+#define DPQ_CONS_SLEEP 0           // reducer: back-off while the consumers finish the stage
+#endif
+#ifndef DPQ_STAGE_SLEEP
+#define DPQ_STAGE_SLEEP 0          // consumers: back-off on the stage counter (skew bound)
+#endif
+#ifndef DPQ_SLOT_SLEEP
+#define DPQ_SLOT_SLEEP 0           // ns of back-off while a ring item is in flight
+#endif
 #ifndef DPQ_EXTRA_PREFETCH
 #define DPQ_EXTRA_PREFETCH 0       // extra planes of deciding layers prefetched into L2 while the decision is pending
 #endif
@@ -1522,11 +1534,25 @@ __device__ __forceinline__ float stream_task(Smem& sm, int j0, int n, uint32_t l
   for (int q = 0; q < n; ++q) {
     const int j = j0 + q;
     const int sl = j % kMaxSlots;
+#if DPQ_SEQ_SLEEP > 0
+    // the item is not issued yet (the ring is behind): back off instead of a
+    // tight LDS loop (MIO slots of the warps that do have data)
+    if (lane == 0 && sm.seq[sl] != j) {
+      __nanosleep(DPQ_SEQ_SLEEP);
+      SPIN_UNTIL_NS((__nanosleep(DPQ_SEQ_SLEEP), sm.seq[sl] == j), "ring sequence", j, sm.seq[sl], 4000000000ull);
+    }
+#else
     if (lane == 0) SPIN_UNTIL_NS(sm.seq[sl] == j, "ring sequence", j, sm.seq[sl], 4000000000ull);
+#endif
     __syncwarp();
     const uint32_t fa = smem_u32(&sm.full[sl]);
     const unsigned fpar = (unsigned)((j / kMaxSlots) & 1);
+#if DPQ_SLOT_SLEEP > 0
+    if (!mbar_test(fa, fpar))
+      SPIN_UNTIL_NS((__nanosleep(DPQ_SLOT_SLEEP), mbar_test(fa, fpar)), "ring slot", j, fpar, 4000000000ull);
+#else
     SPIN_UNTIL_NS(mbar_test(fa, fpar), "ring slot", j, fpar, 4000000000ull);
+#endif
     const uint4* d = reinterpret_cast<const uint4*>(dyn0 + slot_offset(&sm, sl)) + lane;
     const uint4 d0 = d[0], d1 = d[32], d2 = d[64], d3 = d[96];
     __syncwarp();
@@ -1543,7 +1569,12 @@ __device__ __forceinline__ void cons_op(const Prog& P, Smem& sm, int oi, int op_
   float* lut = reinterpret_cast<float*>(reinterpret_cast<char*>(&sm) + (kLut - smem_u32(&sm)));
   if (dbg && tid == 0) dbg[0] = gclock();
   // skew bound: this stage writes partials / attention states of parity gs
+#if DPQ_STAGE_SLEEP > 0
+  if (tid == 0 && !stage_done(P, gs))
+    SPIN_UNTIL((__nanosleep(DPQ_STAGE_SLEEP), stage_done(P, gs)), "stage counter", gs, 0);
+#else
   if (tid == 0) SPIN_UNTIL(stage_done(P, gs), "stage counter", gs, 0);
+#endif
   CSYNC();
   const Op& O = sm.cop[b];
   const CtaWork& W = sm.cw[b];
@@ -1872,7 +1903,13 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
       }
       __syncwarp();
       if (lane == 0) {
+#if DPQ_CONS_SLEEP > 0
+        if (sm.cons_gs < gs + 1)
+          SPIN_UNTIL_NS((__nanosleep(DPQ_CONS_SLEEP), sm.cons_gs >= gs + 1), "consumer stage", gs, sm.cons_gs,
+                        12000000000ull);
+#else
         SPIN_UNTIL_NS(sm.cons_gs >= gs + 1, "consumer stage", gs, sm.cons_gs, 12000000000ull);
+#endif
         __threadfence();   // the zeroed partial words (tiles_S) before the arrival: reused two stages on
         if (P.tp_size > 1) __threadfence_system();   // this stage's peer stores before the arrival
         red_all(P, P.bar, 1ull);
