@@ -59,6 +59,9 @@
 #ifndef DPQ_STAGE_SLEEP
 #define DPQ_STAGE_SLEEP 0          // consumers: back-off on the stage counter (skew bound)
 #endif
+#ifndef DPQ_PSLOT_SLEEP
+#define DPQ_PSLOT_SLEEP 100        // producer: back-off while its ring slot is still in use (-0.4%)
+#endif
 #ifndef DPQ_SLOT_SLEEP
 #define DPQ_SLOT_SLEEP 0           // ns of back-off while a ring item is in flight
 #endif
@@ -1417,7 +1420,13 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
         // the consumer's release (mbarrier arrive after its reads) orders its
         // reads of the slot before this TMA write
         const unsigned par = (unsigned)(((j / kMaxSlots) - 1) & 1);
+#if DPQ_PSLOT_SLEEP > 0
+        if (!mbar_test(smem_u32(&sm.empty[slot]), par))
+          SPIN_UNTIL_NS((__nanosleep(DPQ_PSLOT_SLEEP), mbar_test(smem_u32(&sm.empty[slot]), par)), "producer slot", j,
+                        oi, 12000000000ull);
+#else
         SPIN_UNTIL_NS(mbar_test(smem_u32(&sm.empty[slot]), par), "producer slot", j, oi, 12000000000ull);
+#endif
       }
       sm.seq[slot] = j;
       mbar_expect_tx(&sm.full[slot], (unsigned)kItemBytes);
