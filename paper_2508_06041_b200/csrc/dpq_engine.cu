@@ -62,6 +62,9 @@
 #ifndef DPQ_PSLOT_SLEEP
 #define DPQ_PSLOT_SLEEP 100        // producer: back-off while its ring slot is still in use (-0.4%)
 #endif
+#ifndef DPQ_DEC_SLEEP
+#define DPQ_DEC_SLEEP 0            // consumers: back-off while the op's decision is pending
+#endif
 #ifndef DPQ_SLOT_SLEEP
 #define DPQ_SLOT_SLEEP 0           // ns of back-off while a ring item is in flight
 #endif
@@ -1642,7 +1645,12 @@ __device__ __forceinline__ void cons_op(const Prog& P, Smem& sm, int oi, int op_
   if (dbg && tid == 0) dbg[3] = gclock();
   const int n_base = W.cnt[0] * nb.v0 + W.cnt[1] * nb.v1 + W.cnt[2] * nb.v2;
   // extra planes of the layers that decided high
+#if DPQ_DEC_SLEEP > 0
+  if (lane == 0 && sm.dec_op < oi + 1)
+    SPIN_UNTIL_NS((__nanosleep(DPQ_DEC_SLEEP), sm.dec_op >= oi + 1), "decision", oi, 0, 8000000000ull);
+#else
   if (lane == 0) SPIN_UNTIL_NS(sm.dec_op >= oi + 1, "decision", oi, 0, 8000000000ull);
+#endif
   __syncwarp();
   __threadfence_block();
   const int* df = sm.dec_fin[oi % kDecRing];
