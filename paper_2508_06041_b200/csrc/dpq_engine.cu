@@ -68,6 +68,9 @@
 #ifndef DPQ_SLOT_SLEEP
 #define DPQ_SLOT_SLEEP 0           // ns of back-off while a ring item is in flight
 #endif
+#ifndef DPQ_FEEDS_FIRST
+#define DPQ_FEEDS_FIRST 1          // estimator feeds + statistics before the window LUT (1 all ops, 2 q|k|v and o; measured 1 best)
+#endif
 #ifndef DPQ_EXTRA_PREFETCH
 #define DPQ_EXTRA_PREFETCH 0       // extra planes of deciding layers prefetched into L2 while the decision is pending
 #endif
@@ -1625,12 +1628,22 @@ __device__ __forceinline__ void cons_op(const Prog& P, Smem& sm, int oi, int op_
   if (dbg && tid == 0) dbg[1] = gclock();
   // the window's LUT (all warps), then its estimator feeds + statistics
   // (tagged stores, off the CTA's critical path: no CSYNC after them)
+  // (DPQ_FEEDS_FIRST: the feeds before the LUT, 1 = every op, 2 = q|k|v and o,
+  // whose decision is on the critical path)
+  const bool feeds_first = DPQ_FEEDS_FIRST == 1 || (DPQ_FEEDS_FIRST == 2 && (O.inst % 4 == 0 || O.attn_in));
+  if (feeds_first) {
+    feed_finish(P, C, O, W, fp, sm.xw, gs + 1u);
+    if (dbg && lane == 0 && O.feed_rows > 0 && C.mode == MODE_DYNAMIC)
+      atomicMax(reinterpret_cast<unsigned long long*>(dbg + 20), gclock());
+  }
   lut_build(lut, sm.xw);
   CSYNC();
   if (dbg && tid == 0) dbg[2] = gclock();
-  feed_finish(P, C, O, W, fp, sm.xw, gs + 1u);
-  if (dbg && lane == 0 && O.feed_rows > 0 && C.mode == MODE_DYNAMIC)
-    atomicMax(reinterpret_cast<unsigned long long*>(dbg + 20), gclock());
+  if (!feeds_first) {
+    feed_finish(P, C, O, W, fp, sm.xw, gs + 1u);
+    if (dbg && lane == 0 && O.feed_rows > 0 && C.mode == MODE_DYNAMIC)
+      atomicMax(reinterpret_cast<unsigned long long*>(dbg + 20), gclock());
+  }
   const I3 nb = base_bits(O, C);
   const uint32_t lanereg = kLut | ((uint32_t)lane * 4u);
   const size_t par = (size_t)(gs & 1u) * P.slot_half + (size_t)lane * 2;
