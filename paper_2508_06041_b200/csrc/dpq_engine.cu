@@ -728,7 +728,10 @@ __device__ __forceinline__ const Feed* feed_of_row(const Prog& P, int inst, int 
 // i-th row -> warp kFeedW0 + i % kFeedWarps). The first kFeedPre rows of a
 // warp are loaded before the input window arrives (feed_prefetch) and
 // finished once it is staged (feed_finish); further rows are loaded then.
-constexpr int kFeedPre = 2;
+#ifndef DPQ_FEED_PRE
+#define DPQ_FEED_PRE 2
+#endif
+constexpr int kFeedPre = DPQ_FEED_PRE;
 struct FeedPre {
   bool pre;                // the warp's first kFeedPre rows were prefetched
   const Feed* F[kFeedPre];
