@@ -263,3 +263,26 @@ def test_gemv_kernel_selector_matches_engine_program(cols, monkeypatch):
         assert e1 == e2 and e1 == pytest.approx(ref_est, rel=1e-5)
         close_y(y1, np.asarray(y2, dtype=np.float64))
         close_y(y1, O.gemv(O.as_layer(q), want, x.astype(np.float32)))
+
+
+@pytest.mark.parametrize("shape", [(14336, 4096), (4096, 14336)])
+def test_gemv_kernel_selector_large_layers(shape, monkeypatch):
+    """dpq_select_gemv on cfg2 shapes (projection selector, f32 G, pair (3, 4)):
+    more than one wave of chunk groups per CTA, so the decided bits stream
+    base and extra planes together after the first wave. Bit, estimate and
+    output against the oracle, both decisions."""
+    rows, cols = shape
+    rng = np.random.default_rng(rows + 3 * cols)
+    W = rng.normal(0.0, 1.0 / np.sqrt(cols), shape)
+    q = Q.quantize_layer(W, 4, 3)
+    G = rng.normal(size=(64, cols)) / np.sqrt(cols)
+    x = rng.normal(size=cols)
+    ref_est = float(np.linalg.norm(G @ x.astype(np.float32).astype(np.float64)))
+    est_obj = E.ErrorEstimator(E.ProjectionEstimator(G, 64, 0), E.IMMEDIATE, (3, 4))
+    ol = O.as_layer(q)
+    for T, want in ((ref_est * 0.99, 4), (ref_est * 1.01, 3)):
+        pl = R.PlanLayer(LayerId(0, "up"), 4, 3.5, (3, 4), T, 0.5, est_obj)
+        y, bit, est, _ = _select(q, pl, x, "f32")
+        assert bit == want
+        assert est == pytest.approx(ref_est, rel=1e-5)
+        close_y(y, O.plane_sum_gemv(ol, want, x.astype(np.float32).astype(np.float64)))
