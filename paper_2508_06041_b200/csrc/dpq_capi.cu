@@ -307,6 +307,8 @@ struct dpq_session {
   Arena arena;
   Control* ctl = nullptr;
   Control* ctl_host = nullptr;       // pinned staging for the host-written fields
+  unsigned char* pin_io = nullptr;   // pinned per-step staging (dpq_session_step): control words in,
+                                     // logits + error flags out
   signed char* forced_dev = nullptr;
   float *x = nullptr, *qkv = nullptr, *attn = nullptr, *ug = nullptr, *logits = nullptr;
   float *embed = nullptr, *lm = nullptr, *cosv = nullptr, *sinv = nullptr;
