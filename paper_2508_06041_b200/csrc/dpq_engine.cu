@@ -71,6 +71,9 @@
 #ifndef DPQ_FEEDS_FIRST
 #define DPQ_FEEDS_FIRST 1          // estimator feeds + statistics before the window LUT (1 all ops, 2 q|k|v and o; measured 1 best)
 #endif
+#ifndef DPQ_LUT_PAIR
+#define DPQ_LUT_PAIR 1             // LUT build jobs of two row blocks (shared low-nibble sums; -0.6%)
+#endif
 #ifndef DPQ_EXTRA_PREFETCH
 #define DPQ_EXTRA_PREFETCH 0       // extra planes of deciding layers prefetched into L2 while the decision is pending
 #endif
@@ -404,6 +407,35 @@ __device__ __forceinline__ float plane_sum(const uint4 d0, const uint4 d1, const
 // [16 m, 16 m + 16) of slot g (low nibble subset sums + the high nibble's);
 // the 1024 jobs are spread over all consumer threads (conflict-free stores).
 __device__ __forceinline__ void lut_build(float* lut, const float* xw) {
+#if DPQ_LUT_PAIR
+  // job q = (slot g, row blocks 2 mm and 2 mm + 1): the low-nibble subset sums
+  // once for both (512 jobs, at most 2 per thread)
+  for (int q = threadIdx.x; q < 512; q += NT) {
+    const int g = q & 63, mm = q >> 6;
+    const float4 xa = *reinterpret_cast<const float4*>(xw + 8 * g);
+    const float4 xb = *reinterpret_cast<const float4*>(xw + 8 * g + 4);
+    float L[16];
+    L[0] = 0.f;
+#pragma unroll
+    for (int n = 1; n < 16; ++n) {
+      const int low = n & (-n);
+      L[n] = L[n ^ low] + (low == 1 ? xa.x : low == 2 ? xa.y : low == 4 ? xa.z : xa.w);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int m = 2 * mm + h;
+      float H = 0.f;
+      if (m & 1) H += xb.x;
+      if (m & 2) H += xb.y;
+      if (m & 4) H += xb.z;
+      if (m & 8) H += xb.w;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) lut[(16 * m + i) * kGroups + g] = L[i] + H;
+    }
+  }
+  if (threadIdx.x < 64) lut[256 * kGroups + threadIdx.x] = 0.f;
+  return;
+#endif
   for (int q = threadIdx.x; q < 1024; q += NT) {
     const int g = q & 63, m = q >> 6;
     const float4 xa = *reinterpret_cast<const float4*>(xw + 8 * g);
