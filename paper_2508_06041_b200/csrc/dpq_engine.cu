@@ -72,7 +72,7 @@
 #define DPQ_FEEDS_FIRST 1          // estimator feeds + statistics before the window LUT (1 all ops, 2 q|k|v and o; measured 1 best)
 #endif
 #ifndef DPQ_LUT_PAIR
-#define DPQ_LUT_PAIR 1             // LUT build jobs of two row blocks (shared low-nibble sums; -0.6%)
+#define DPQ_LUT_PAIR 1             // LUT build jobs of two (1) or four (2) row blocks sharing the low-nibble sums (1: -0.6%, 2: +0.4%)
 #endif
 #ifndef DPQ_EXTRA_PREFETCH
 #define DPQ_EXTRA_PREFETCH 0       // extra planes of deciding layers prefetched into L2 while the decision is pending
@@ -410,7 +410,8 @@ __device__ __forceinline__ void lut_build(float* lut, const float* xw) {
 #if DPQ_LUT_PAIR
   // job q = (slot g, row blocks 2 mm and 2 mm + 1): the low-nibble subset sums
   // once for both (512 jobs, at most 2 per thread)
-  for (int q = threadIdx.x; q < 512; q += NT) {
+  constexpr int kMB = DPQ_LUT_PAIR == 2 ? 4 : 2;      // row blocks per job
+  for (int q = threadIdx.x; q < 1024 / kMB; q += NT) {
     const int g = q & 63, mm = q >> 6;
     const float4 xa = *reinterpret_cast<const float4*>(xw + 8 * g);
     const float4 xb = *reinterpret_cast<const float4*>(xw + 8 * g + 4);
@@ -422,8 +423,8 @@ __device__ __forceinline__ void lut_build(float* lut, const float* xw) {
       L[n] = L[n ^ low] + (low == 1 ? xa.x : low == 2 ? xa.y : low == 4 ? xa.z : xa.w);
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int m = 2 * mm + h;
+    for (int h = 0; h < kMB; ++h) {
+      const int m = kMB * mm + h;
       float H = 0.f;
       if (m & 1) H += xb.x;
       if (m & 2) H += xb.y;
