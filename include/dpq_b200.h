@@ -101,7 +101,11 @@ int dpq_store_layer_bytes(const dpq_store* s, int layer, int b, int64_t* bytes);
 int dpq_quantize_device(int device, const float* W_dev, int rows, int cols, int n_bits,
                         uint16_t* codes_dev, float* lo_dev, float* hi_dev, void* stream);
 
-/* quant.gemv (quant.py:95-99): y = W_b x, reading only planes 0..b-1. */
+/* quant.gemv (quant.py:95-99): y = W_b x, reading only planes 0..b-1.
+ * Calls on one store share its scratch (tile counters, window partials,
+ * estimator sums): issue them on one stream (or order the streams). The
+ * launch uses programmatic dependent launch: the next call on the stream may
+ * start streaming its weights while this one drains. */
 int dpq_gemv(dpq_store* s, int layer, int b, const float* x_dev, float* y_dev, void* stream);
 /* quant.dequantize (quant.py:67-80): float64 [rows][cols]. */
 int dpq_dequantize(dpq_store* s, int layer, int b, double* out_dev, void* stream);
@@ -114,7 +118,8 @@ int dpq_plan_destroy(dpq_plan* p);
  * the estimate, the threshold compare and the selected-bit GEMV run in one
  * kernel; bit_out_dev (int32) / est_out_dev (float32, NaN if none) receive the
  * decision. est_in_dev: estimator input when it differs from x (async), or
- * NULL. exact_out_dev (nullable): ||(W_h - W_l) x|| (track_exact). */
+ * NULL. exact_out_dev (nullable): ||(W_h - W_l) x|| (track_exact). Same
+ * stream rule as dpq_gemv (the plan's store scratch). */
 int dpq_select_gemv(dpq_plan* p, int layer, const float* x_dev, const float* est_in_dev,
                     float* y_dev, int32_t* bit_out_dev, float* est_out_dev,
                     float* exact_out_dev, void* stream);
