@@ -511,7 +511,8 @@ def run_ours(args):
             and world == 1):
         try:
             line["roofline"]["traffic"] = json.load(open(traffic_path)).get("bytes_per_step")
-            line["roofline"]["traffic_source"] = "profiles/engine_traffic.json (ncu --set full capture)"
+            line["roofline"]["traffic_source"] = ("profiles/engine_traffic.json (ncu dram__bytes_read.sum + "
+                                                   "dram__bytes_write.sum per single-step engine_kernel launch, median)")
         except Exception:
             pass
     if rank == 0:
