@@ -92,9 +92,11 @@ struct Ctl {
   volatile int dec_bit;     // -1 until decided
 };
 
+// Byte LUT of a window (layout: dpq_common.cuh). Job q = (slot g, row blocks
+// 2 mm, 2 mm + 1): the low-nibble subset sums once for both blocks.
 __device__ __forceinline__ void lut_build(float* lut, const float* xw, int tid, int nthr) {
-  for (int q = tid; q < 1024; q += nthr) {
-    const int g = q & 63, m = q >> 6;
+  for (int q = tid; q < 512; q += nthr) {
+    const int g = q & 63, mm = q >> 6;
     const float4 xa = *reinterpret_cast<const float4*>(xw + 8 * g);
     const float4 xb = *reinterpret_cast<const float4*>(xw + 8 * g + 4);
     float L[16];
@@ -104,13 +106,17 @@ __device__ __forceinline__ void lut_build(float* lut, const float* xw, int tid, 
       const int low = n & (-n);
       L[n] = L[n ^ low] + (low == 1 ? xa.x : low == 2 ? xa.y : low == 4 ? xa.z : xa.w);
     }
-    float H = 0.f;
-    if (m & 1) H += xb.x;
-    if (m & 2) H += xb.y;
-    if (m & 4) H += xb.z;
-    if (m & 8) H += xb.w;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) lut[(16 * m + i) * kGroups + g] = L[i] + H;
+    for (int h = 0; h < 2; ++h) {
+      const int m = 2 * mm + h;
+      float H = 0.f;
+      if (m & 1) H += xb.x;
+      if (m & 2) H += xb.y;
+      if (m & 4) H += xb.z;
+      if (m & 8) H += xb.w;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) lut[(16 * m + i) * kGroups + g] = L[i] + H;
+    }
   }
 }
 
