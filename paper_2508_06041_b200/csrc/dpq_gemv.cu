@@ -34,6 +34,9 @@ using eng::g_diag;
 #ifndef DPQ_GV_CW
 #define DPQ_GV_CW 16
 #endif
+#ifndef DPQ_GV_ACQREL
+#define DPQ_GV_ACQREL 1
+#endif
 #ifndef DPQ_GV_GT
 #define DPQ_GV_GT 4
 #endif
@@ -478,6 +481,16 @@ extern "C" __global__ void __launch_bounds__(kNT, 1) bitplane_gemv_kernel(const 
   auto arrive = [&](int t, int bit) {
     __syncwarp();
     int last = 0;
+#if DPQ_GV_ACQREL
+    if (lane == 0) {           // one acq_rel atomic: the warp's partials before the count, and
+      int old;                 // (last window) the other windows' partials after it
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(A.cnt + t) : "memory");
+      last = old == A.n_win - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __syncwarp();
+#else
     if (lane == 0) {
       __threadfence();
       last = atomicAdd(A.cnt + t, 1) == A.n_win - 1;
@@ -485,6 +498,7 @@ extern "C" __global__ void __launch_bounds__(kNT, 1) bitplane_gemv_kernel(const 
     last = __shfl_sync(0xffffffffu, last, 0);
     if (!last) return;
     __threadfence();
+#endif
     double Sd = 0.0, sx = 0.0;
     for (int v = 0; v < A.n_win; ++v) {
       Sd += (double)__ldcg(A.part + (size_t)v * rpad + t * 32 + lane);
