@@ -74,6 +74,9 @@
 #ifndef DPQ_LUT_PAIR
 #define DPQ_LUT_PAIR 1             // LUT build jobs of two (1) or four (2) row blocks sharing the low-nibble sums (1: -0.6%, 2: +0.4%)
 #endif
+#ifndef DPQ_REL_ARRIVE
+#define DPQ_REL_ARRIVE 1           // release / acq_rel atomics instead of fence + atomic (stage arrival, head)
+#endif
 #ifndef DPQ_EXTRA_PREFETCH
 #define DPQ_EXTRA_PREFETCH 0       // extra planes of deciding layers prefetched into L2 while the decision is pending
 #endif
@@ -1976,9 +1979,19 @@ __device__ __forceinline__ void reducer(const Prog& P, Smem& sm, int cta, int G,
 #else
         SPIN_UNTIL_NS(sm.cons_gs >= gs + 1, "consumer stage", gs, sm.cons_gs, 12000000000ull);
 #endif
-        __threadfence();   // the zeroed partial words (tiles_S) before the arrival: reused two stages on
+        // the zeroed partial words (tiles_S) before the arrival: reused two stages on
+#if DPQ_REL_ARRIVE
+        if (P.tp_size == 1) {      // one release reduction (the warp's stores ordered by __syncwarp)
+          asm volatile("red.release.gpu.global.add.u64 [%0], %1;" :: "l"(P.bar), "l"(1ull) : "memory");
+        } else {
+          __threadfence_system();  // this stage's peer stores before the arrival
+          red_all(P, P.bar, 1ull);
+        }
+#else
+        __threadfence();
         if (P.tp_size > 1) __threadfence_system();   // this stage's peer stores before the arrival
         red_all(P, P.bar, 1ull);
+#endif
       }
       __syncwarp();
     }
@@ -2062,12 +2075,23 @@ __device__ __noinline__ void head_stage(const Prog& P, const ECtl& C, Smem& sm, 
       if (xs.x >> 16) P.tr_est[o] = xe;         // exact estimators: the estimate is the exact error
     }
   }
+#if DPQ_REL_ARRIVE
+  CSYNC();
+  if (tid == 0) {              // the CTA's logits before the count; the last CTA acquires the others'
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(P.head_cnt) : "memory");
+    sm.head_last = old == (unsigned)G - 1;
+  }
+  CSYNC();
+  if (!sm.head_last) return;
+#else
   __threadfence();
   CSYNC();
   if (tid == 0) sm.head_last = atomicAdd(P.head_cnt, 1u) == (unsigned)G - 1;
   CSYNC();
   if (!sm.head_last) return;
   __threadfence();
+#endif
   float best = -CUDART_INF_F;
   int bi = 0x7fffffff;
   for (int i = tid; i < P.vocab; i += NT) {
