@@ -2121,7 +2121,7 @@ __device__ __noinline__ void head_stage(const Prog& P, const ECtl& C, Smem& sm, 
       c->rot = C.rot + 1;
       c->has_prev = 1;
     }
-    __threadfence();
+    // (the release store orders this thread's control writes before the count)
     asm volatile("st.release.gpu.global.s32 [%0], %1;" :: "l"(&c->n_steps_done), "r"(C.n_steps_done + 1) : "memory");
   }
 }
