@@ -361,22 +361,24 @@ extern "C" __global__ void __launch_bounds__(kNT, 1) bitplane_gemv_kernel(const 
       if (A.est_kind == EST_PROJECTION) est = q > 0.0 ? q * eng::rsqrt_d(q) : 0.0;              // estimator.py:56-57
       else est = A.slope * (sq > 0.0 ? sq * eng::rsqrt_d(sq) : 0.0) + A.intercept;           // estimator.py:41-42
       bit = est > A.T ? A.h : A.l;                                                           // runtime.py:192
-      // the last CTA past this point clears the sums for the next call
-      if (lane == 0) {
-        __threadfence();
-        if (atomicAdd(A.sync + 1, 1) == G - 1) {
-          for (int r = 0; r < A.k; ++r) A.acc[r] = 0;
-          A.sync[0] = 0;
-          A.sync[1] = 0;
-        }
-      }
     }
-    if (lane == 0) {
+    if (lane == 0) {                         // the decision first (the consumers wait for it)
       c.dec_bit = bit;
       GV_STAMP(5);
       if (cta == 0) {
         if (A.bit_out) *A.bit_out = bit;
         if (A.est_out) *A.est_out = (float)est;
+      }
+      // then the last CTA past this point clears the sums for the next call
+      // (acq_rel: this CTA's reads of the sums before its count)
+      if (A.sentinel == 0) {
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(A.sync + 1) : "memory");
+        if (old == (unsigned)G - 1) {
+          for (int r = 0; r < A.k; ++r) A.acc[r] = 0;
+          A.sync[0] = 0;
+          A.sync[1] = 0;
+        }
       }
     }
     __syncwarp();
