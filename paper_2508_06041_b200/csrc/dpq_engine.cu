@@ -1447,8 +1447,17 @@ __device__ __forceinline__ void decide_op(const Prog& P, const ECtl& C, const Op
 // in lockstep): a batch spans <= kIssueLanes * 8 <= kMaxSlots consecutive FIFO
 // items, so the slot each lane waits for holds an item issued before the batch
 // (no lane can wait on an item another lane of the batch has yet to issue).
-constexpr int kIssueLanes = kMaxSlots / 8;
+#ifndef DPQ_ISSUE_LANES
+#define DPQ_ISSUE_LANES (DPQ_RING_SLOTS / 8)
+#endif
+constexpr int kIssueLanes = DPQ_ISSUE_LANES;   // lanes at 8 planes per task (measured: fewer is slower)
 static_assert(kIssueLanes * 8 <= kMaxSlots, "an issue batch must fit the ring");
+#ifndef DPQ_DYN_LANES
+#define DPQ_DYN_LANES 1
+#endif
+__device__ __forceinline__ int issue_lanes(int planes) {
+  return DPQ_DYN_LANES ? min(32, kMaxSlots / max(planes, 1)) : kIssueLanes;
+}
 
 __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G, int n_steps, int s0) {
   const int lane = threadIdx.x & 31;
@@ -1501,9 +1510,12 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
       }
       __syncwarp();
       u64* pdbg = P.dbg ? P.dbg + ((size_t)si * G + cta) * kDbgRec : nullptr;
-      for (int k0 = 0; k0 < W.n_tasks; k0 += kIssueLanes) {
+      // issue lanes per batch: a batch of nl tasks spans <= nl * (planes per
+      // task) <= kMaxSlots FIFO items (see above), so nl = kMaxSlots / planes
+      const int nlb = issue_lanes(max(nb.v0, max(nb.v1, nb.v2)));
+      for (int k0 = 0; k0 < W.n_tasks; k0 += nlb) {
         const int k = k0 + lane;
-        if (lane < kIssueLanes && k < W.n_tasks) {
+        if (lane < nlb && k < W.n_tasks) {
           const uint2 tk = sm.ptask[k];
           const int li = task_layer(tk);
           issue_task(k, fifo + task_before(tk, nb), 0, nb[li], li == 0 ? ps0 : li == 1 ? ps1 : ps2);
@@ -1536,10 +1548,11 @@ __device__ __forceinline__ void producer(const Prog& P, Smem& sm, int cta, int G
       if (pdbg && lane == 0) pdbg[6] = gclock();
       const I3 ex{fin.v0 - nb.v0, fin.v1 - nb.v1, fin.v2 - nb.v2};
       const int n_ext = W.cnt[0] * ex.v0 + W.cnt[1] * ex.v1 + W.cnt[2] * ex.v2;
+      const int nle = issue_lanes(max(ex.v0, max(ex.v1, ex.v2)));
       if (n_ext > 0)
-        for (int k0 = 0; k0 < W.n_tasks; k0 += kIssueLanes) {
+        for (int k0 = 0; k0 < W.n_tasks; k0 += nle) {
           const int k = k0 + lane;
-          if (lane < kIssueLanes && k < W.n_tasks) {
+          if (lane < nle && k < W.n_tasks) {
             const uint2 tk = sm.ptask[k];
             const int li = task_layer(tk);
             if (ex[li] > 0)
